@@ -1,0 +1,351 @@
+"""Benchmark of the B200 dual-bound engine (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one restarted-FISTA iteration of the perspective relaxation on the
+workload BASELINE.json's metric is quoted on (configs[1] = C2: least squares,
+fp64, n = p = 16000, Toeplitz rho 0.7, k=20, M=2, lambda2=0.1; synthetic data
+from the reference's generator with the paper's protocol).  X is 2.05 GB,
+larger than the 126 MB L2, so every pass streams HBM.
+
+ours       value  = K iterations / device time of a K-iteration solve with X resident
+                    (stop_on_gap=False so exactly K iterations run, bound checks included)
+           e2e    = iterations / time of full solves to the C2 target (relative gap
+                    <= 1e-6) through solve_relaxation on an instance whose X lives
+                    in pinned host memory (H2D of X and y + D2H of beta inside)
+reference  the CPU oracle port of the reference solver (oracle/l0_oracle.py, numpy +
+           C PAVA, all host threads), K iterations of the same workload
+N > 1      rows of X sharded over the ranks (NCCL all-reduce of the gradient); the
+           global problem is fixed, so scaling is "strong".
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "C2"
+# injected step constant 2 * 1.01 * lambda_max(X^T X) for C2 (SURVEY.md §8(d):
+# Lanczos 2.99073e5), rounded up so it stays a valid Lipschitz bound
+L_C2 = 2.9908e5
+REL_GAP = 1e-6
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(scale):
+    from paper_2502_09502_b200 import data
+    t0 = time.time()
+    cd = data.make_config(WORKLOAD, scale=scale)
+    log(f"[bench] generated {WORKLOAD} n={cd.n} p={cd.p} in {time.time() - t0:.1f}s")
+    return cd
+
+
+def base_config(cd, n_gpus):
+    return {"workload": "C2: least-squares root perspective relaxation, n=p=%d, Toeplitz rho=0.7, "
+                        "k=20, M=2, lambda2=0.1, SNR=5" % cd.n,
+            "n": cd.n, "p": cd.p, "k": cd.k, "M": cd.M, "lambda2": cd.lambda2,
+            "x_bytes": int(cd.X.nbytes), "lipschitz": L_C2,
+            "l2_policy": "inputs larger than L2 (X = %.2f GB vs 126 MB)" % (cd.X.nbytes / 1e9),
+            "parallelism": "rows%d" % n_gpus if n_gpus > 1 else "single"}
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("k2_dram_bytes_per_launch"), d.get("k1_dram_bytes_per_launch")
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference solver)
+# ---------------------------------------------------------------------------
+def cpu_baseline(cd, iters, warm=2):
+    import threadpoolctl
+    from oracle import l0_oracle
+    X = cd.X if cd.X.dtype == np.float64 else cd.X.astype(np.float64)
+    cores = os.cpu_count()
+    with threadpoolctl.threadpool_limits(cores):
+        l0_oracle.fista(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L_C2, max_iter=warm,
+                        gap_tol=1e-300, stop_on_gap=False)
+        t0 = time.perf_counter()
+        l0_oracle.fista(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L_C2, max_iter=iters,
+                        gap_tol=1e-300, stop_on_gap=False)
+        dt = time.perf_counter() - t0
+    return {"value": iters / dt, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"{iters} FISTA iterations of {WORKLOAD} (after {warm} warm-up) with the "
+                      f"numpy/OpenBLAS + C-PAVA oracle port, {cores} threads, {dt:.2f}s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cd = make_inputs(args.scale)
+    cb = cpu_baseline(cd, args.steps, warm=args.warmup)
+    line = {"metric": "FISTA iters/sec (C2, CPU reference solver)", "value": cb["value"],
+            "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+            "config": base_config(cd, 1), "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# ours
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        return run_ours_sharded(args, world, rank, local)
+    torch.cuda.set_device(0)
+    import paper_2502_09502_b200 as eng
+    eng.native.load()
+    cd = make_inputs(args.scale)
+    inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+    t0 = time.time()
+    inst.device_problem()
+    torch.cuda.synchronize()
+    log(f"[bench] upload {time.time() - t0:.2f}s")
+    K, W = args.steps, args.warmup
+
+    def fixed(iters, profile):
+        return eng.FistaOptions(lipschitz=L_C2, max_iterations=iters, gap_tolerance=1e-300,
+                                stop_on_gap=False, profile=profile)
+
+    # warm-up: W iterations (graph capture, caches)
+    eng.solve_relaxation(inst, opts=fixed(W, True), return_device=True)
+    torch.cuda.synchronize()
+    # timed region: exactly K iterations, CUDA events, clocks sampled
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    rep = eng.solve_relaxation(inst, opts=fixed(K, True), return_device=True)
+    end.record()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    clk = clocks.stop()
+    assert rep.iterations == K, rep.iterations
+    value = K / (ms / 1e3)
+    st = rep.stats
+    log(f"[bench] {K} its in {ms:.2f} ms -> {value:.1f} it/s; k1 {st['k1_ms'] / max(1, st['k1_count']):.4f} "
+        f"ms k2 {st['k2_ms'] / max(1, st['k2_count']):.4f} ms k3 {st['k3_ms'] / max(1, st['k3_count']):.4f} ms")
+
+    # roofline of the dominant kernel (algorithmic bytes / measured launch time)
+    peak, peak_src = measured_peak()
+    s = 8
+    n, p = cd.n, cd.p
+    k2_bytes = n * p * s + 8 * (3 * n + 5 * p)     # X, u_t, u_t-1, y, beta_t, beta_t-1, gamma, key
+    k1_bytes = n * p * s + 8 * (p + 2 * n)          # X, beta, y, u
+    k1_avg = st["k1_ms"] / max(1, st["k1_count"])
+    k2_avg = st["k2_ms"] / max(1, st["k2_count"])
+    k3_avg = st["k3_ms"] / max(1, st["k3_count"])
+    dom = "k2_transpose" if st["k2_ms"] >= st["k1_ms"] else "k1_forward"
+    dom_bytes, dom_ms = (k2_bytes, k2_avg) if dom == "k2_transpose" else (k1_bytes, k1_avg)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    t2, t1 = ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": (t2 if dom == "k2_transpose" else t1),
+                "algorithmic_bytes_per_launch": dom_bytes,
+                "launch_ms": dom_ms,
+                "other_kernels": {
+                    "k1_forward": {"launch_ms": k1_avg, "achieved_gbs": k1_bytes / (k1_avg / 1e3) / 1e9,
+                                   "frac": k1_bytes / (k1_avg / 1e3) / 1e9 / peak},
+                    "k2_transpose": {"launch_ms": k2_avg, "achieved_gbs": k2_bytes / (k2_avg / 1e3) / 1e9,
+                                     "frac": k2_bytes / (k2_avg / 1e3) / 1e9 / peak},
+                    "k3_prox_pava_envelope": {"launch_ms": k3_avg}},
+                "iteration_bytes_2pass": 2 * n * p * s,
+                "iteration_frac_of_hbm": (2 * n * p * s) / (ms / 1e3 / K) / 1e9 / peak}
+
+    # end to end through the public API with host-resident X (pinned)
+    Xpin = torch.from_numpy(cd.X).pin_memory()
+    e2e_iters, e2e_time = 0, 0.0
+    h2d = cd.X.nbytes + cd.y.nbytes
+    d2h = cd.p * 8
+    e2e_reps = []
+    for _ in range(args.e2e_solves):
+        inst_h = eng.ProblemInstance(Xpin, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = eng.solve_relaxation(inst_h, opts=eng.FistaOptions(
+            lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e_iters += r.iterations
+        e2e_time += dt
+        e2e_reps.append({"iterations": r.iterations, "seconds": dt, "rel_gap": r.gap / abs(r.primal_value),
+                         "termination": r.termination.value})
+        inst_h.release_device()
+        del inst_h
+    e2e = {"value": e2e_iters / e2e_time, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h,
+           "step": "one solve_relaxation call to relative gap 1e-6 from host (pinned) X",
+           "solves": e2e_reps}
+    log(f"[bench] e2e {e2e['value']:.1f} it/s {e2e_reps}")
+
+    cb = cpu_baseline(cd, args.cpu_iters) if not args.no_cpu else None
+    line = {"metric": "FISTA iters/sec (C2 root relaxation, HBM-bound GEMV passes)",
+            "value": value, "unit": "iters/s", "n_gpus": 1, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+            "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
+            "restarts": rep.restarts, "final_gap": rep.gap}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours_sharded(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2502_09502_b200 import distributed as shard
+    import paper_2502_09502_b200 as eng
+    eng.native.load()
+    cd = make_inputs(args.scale)
+    r0, r1 = shard.row_range(cd.n, world, rank)
+    inst = shard.ShardedInstance(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
+                                 cd.M, cd.lambda2, n_global=cd.n)
+    inst.device_problem()
+    K, W = args.steps, args.warmup
+    opts = lambda it: eng.FistaOptions(lipschitz=L_C2, max_iterations=it, gap_tolerance=1e-300,
+                                       stop_on_gap=False)
+    shard.solve_relaxation_sharded(inst, opts=opts(W))
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    rep = shard.solve_relaxation_sharded(inst, opts=opts(K))
+    end.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = torch.tensor([start.elapsed_time(end)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    if rank == 0:
+        line = {"metric": "FISTA iters/sec (C2 root relaxation, rows sharded)",
+                "value": K / (ms / 1e3), "unit": "iters/s", "n_gpus": world, "steps": K,
+                "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference generator, seed 0)",
+                "config": base_config(cd, world), "gpu_launches": int(rep.stats["gpu_launches"])}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink C2 (testing only)")
+    ap.add_argument("--e2e-solves", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=10)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

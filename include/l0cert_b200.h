@@ -1,0 +1,174 @@
+/*
+ * l0cert_b200.h — C ABI of the B200-native dual-bound engine.
+ *
+ * The reference (`l0cert`, pure Python) has no FFI of its own; its hot path is
+ * the in-process API listed below.  Each entry point here is what a binding of
+ * that API would call (ctypes from Python).  Reference
+ * interfaces replaced, by /root/reference/pkg/src/l0cert file:line:
+ *
+ *   l0_fista_solve        fista.py:76-222   solve_relaxation (+ FistaOptions :43-61,
+ *                                           RelaxationReport :64-73, Termination :35-40,
+ *                                           NodeState model.py:119-149)
+ *   l0_prox               prox.py:101-201   _prox_gstar_core / prox_gstar / prox_g /
+ *                                           prox_gstar_node / prox_g_node
+ *   l0_g_value            perspective.py:114-132   g_value
+ *   l0_g_conjugate        perspective.py:143-159   g_conjugate
+ *   l0_safe_lower_bound   perspective.py:162-190   safe_lower_bound
+ *   l0_loss_value         model.py:159-181 / :208-218  loss_value, loss_gradient
+ *   l0_loss_conjugate     model.py:226-280          loss_conjugate_at_neg
+ *   l0_power_iteration    model.py:283-306          _power_iteration_lambda_max
+ *   l0_matvec/rmatvec     the numpy X @ v / X.T @ r call sites fista.py:141,156,162,165,209
+ *
+ * Conventions
+ *   - Every pointer named d_* is DEVICE memory owned by the caller; h_* is host.
+ *   - X is row-major (n rows, leading dimension ld >= p elements, ld*elem a
+ *     multiple of 16 bytes, base 16-byte aligned, padding columns finite),
+ *     dtype L0_F64 or L0_F32 (fp32 storage, fp64 arithmetic).  All vectors fp64.
+ *   - `stream` is a cudaStream_t.  Calls are asynchronous unless they return a
+ *     host value (h_*), in which case they synchronise the stream.
+ *   - Return value: L0_OK or an l0_status; l0_last_error() describes the last
+ *     failure of the calling thread.
+ *   - Workspaces are caller-provided device buffers (size from the *_bytes
+ *     queries); a workspace must not be shared by concurrent calls.
+ */
+#ifndef L0CERT_B200_H
+#define L0CERT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum l0_status {
+  L0_OK = 0,
+  L0_INVALID = 1,      /* InvalidInputError (errors.py:8-10)          */
+  L0_NUMERICAL = 2,    /* NumericalError (errors.py:18-24)             */
+  L0_INFEASIBLE = 3,   /* InfeasibleNodeError (errors.py:27-29)        */
+  L0_UNSUPPORTED = 4,  /* UnsupportedOperationError (errors.py:13-15) */
+  L0_CUDA = 5,         /* CUDA runtime failure                          */
+  L0_ABORTED = 6       /* the trace callback asked to stop              */
+};
+enum l0_loss { L0_SQUARED_ERROR = 0, L0_LOGISTIC = 1, L0_SQUARED_HINGE = 2 };
+enum l0_dtype { L0_F64 = 0, L0_F32 = 1 };
+enum l0_termination {
+  L0_CONVERGED = 0, L0_ITERATION_LIMIT = 1, L0_TIME_LIMIT = 2,
+  L0_PRIMAL_BELOW_INCUMBENT = 3, L0_DUAL_ABOVE_INCUMBENT = 4
+};
+/* per-coordinate node class: free / fixed to one / fixed to zero */
+enum l0_node_class { L0_FREE = 0, L0_FIXED_ONE = 1, L0_FIXED_ZERO = 2 };
+
+typedef struct l0_problem l0_problem;
+
+/* FistaOptions (fista.py:43-61) plus engine extensions. */
+typedef struct l0_fista_opts {
+  int64_t max_iterations;       /* fista.py:45 */
+  double gap_tolerance;         /* fista.py:46, absolute */
+  double time_limit;            /* fista.py:47, seconds (INFINITY: none) */
+  double early_primal_cutoff;   /* fista.py:48, NaN = None */
+  double early_dual_cutoff;     /* fista.py:49, NaN = None */
+  int32_t bound_check_interval; /* fista.py:50 */
+  int32_t restart;              /* fista.py:51 */
+  double lipschitz;             /* fista.py:52; must be > 0 (L = max(L, 1e-12) applied) */
+  /* extensions */
+  double gap_tolerance_rel;     /* also stop when gap <= rel * |primal| (0: off) */
+  int32_t stop_on_gap;          /* 0: fixed-iteration mode (no gap stop) */
+  int32_t chunk_iterations;     /* iterations per captured CUDA graph (0: auto) */
+  int32_t profile;              /* 1: time K1/K2/K3 with CUDA events (report fields) */
+  int32_t reserved;
+} l0_fista_opts;
+
+/* NodeState (model.py:119-149): host index arrays, sorted unique, disjoint. */
+typedef struct l0_node {
+  const int64_t* h_fixed_one;
+  int64_t n_fixed_one;
+  const int64_t* h_fixed_zero;
+  int64_t n_fixed_zero;
+  double parent_bound;          /* model.py:132 (-INFINITY default) */
+} l0_node;
+
+/* RelaxationReport (fista.py:64-73) plus engine metrics. */
+typedef struct l0_report {
+  double primal_value;
+  double dual_bound;
+  double gap;
+  int64_t iterations;
+  int64_t restarts;
+  int32_t termination;          /* l0_termination */
+  int32_t status;               /* l0_status of the solve */
+  int64_t error_iteration;      /* NumericalError.iteration (errors.py:22-24) */
+  double wall_time;             /* fista.py:73 */
+  int64_t gpu_launches;         /* kernels launched by the solve */
+  int64_t topk_fallbacks;       /* envelope top-k window misses (diagnostic) */
+  double k1_ms, k2_ms, k3_ms;   /* profile: summed kernel time (CUDA events) */
+  int64_t k1_count, k2_count, k3_count;
+} l0_report;
+
+typedef struct l0_trace_record {
+  double iteration, primal, dual, gap, restarted;   /* fista.py:186-192 */
+} l0_trace_record;
+
+/* Called at every bound check, in order (fista.py:185-194).  A nonzero
+ * return aborts the solve (the caller re-raises its own exception). */
+typedef int (*l0_trace_cb)(const l0_trace_record* rec, void* user);
+
+const char* l0_last_error(void);
+int32_t l0_abi_version(void);
+
+/* ---- problem (ProblemInstance minus k/M/lambda2, model.py:75-116) ---------- */
+int32_t l0_problem_create(const void* d_X, int32_t dtype, int64_t n, int64_t p, int64_t ld,
+                          const double* d_y, int32_t loss, l0_problem** out);
+int32_t l0_problem_workspace_bytes(const l0_problem* prob, uint64_t* bytes);
+int32_t l0_problem_set_workspace(l0_problem* prob, void* d_ws, uint64_t bytes);
+int32_t l0_problem_destroy(l0_problem* prob);
+/* row-sharded mode: this rank holds rows [row0, row0+n) of a global X; the
+ * gradient and loss are all-reduced over NCCL (unique id of 128 bytes). */
+int32_t l0_problem_set_comm(l0_problem* prob, const void* h_nccl_unique_id, int32_t nranks,
+                            int32_t rank);
+
+/* ---- hot path ----------------------------------------------------------------- */
+int32_t l0_fista_solve(l0_problem* prob, int64_t k, double M, double lambda2,
+                       const l0_fista_opts* opts, const l0_node* node /* nullable */,
+                       const double* d_warm_start /* nullable, p */, double* d_beta_out /* p */,
+                       l0_report* report, l0_trace_cb cb /* nullable */, void* user,
+                       void* stream);
+
+/* ---- operators ---------------------------------------------------------------- */
+int32_t l0_matvec(l0_problem* prob, const double* d_v, double* d_out, void* stream);
+int32_t l0_rmatvec(l0_problem* prob, const double* d_r, double* d_out, void* stream);
+int32_t l0_power_iteration(l0_problem* prob, const double* d_v0, double tol, int64_t max_iter,
+                           double* h_lambda, int64_t* h_iterations, void* stream);
+int32_t l0_safe_lower_bound(l0_problem* prob, const double* d_beta, int64_t k_free, double M,
+                            double lambda2, const uint8_t* d_node_class /* nullable */,
+                            double* h_out, void* stream);
+
+int32_t l0_ops_workspace_bytes(int64_t len, uint64_t* bytes);
+/* g_mode=0: out = prox_{rho g*}(in) (prox_gstar[_node]); g_mode=1: out =
+ * prox_{g/rho}(in) = in - prox_{rho g*}(rho in)/rho (prox_g[_node]).  k is the
+ * budget of the free coordinates.  perm/pool report the stable descending
+ * sort and the merged PAVA pool [a*, c*] in sorted positions (-1: none). */
+int32_t l0_prox(const double* d_in, int64_t p, double rho, int64_t k, double M,
+                const uint8_t* d_node_class, int32_t g_mode, double* d_out,
+                int32_t* d_perm_out, int64_t* h_pool_out, void* d_ws, uint64_t ws_bytes,
+                void* stream);
+int32_t l0_g_value(const double* d_beta, int64_t p, int64_t k_free, double M,
+                   const uint8_t* d_node_class, const int32_t* d_fixed_one, int64_t n_fixed_one,
+                   double* h_out, void* d_ws, uint64_t ws_bytes, void* stream);
+int32_t l0_g_conjugate(const double* d_alpha, int64_t p, int64_t k_free, double M,
+                       const uint8_t* d_node_class, double* h_out, void* d_ws, uint64_t ws_bytes,
+                       void* stream);
+/* prox=0: out = H_M(x) (prox.py:27-32); prox=1: out = hprox(x, w, M) (prox.py:35-43) */
+int32_t l0_huber(const double* d_x, int64_t n, double w, double M, int32_t prox, double* d_out,
+                 void* stream);
+int32_t l0_loss_value(int32_t loss, const double* d_u, const double* d_y, int64_t n,
+                      double* h_value, double* d_grad /* nullable */, int32_t* h_nonfinite,
+                      void* d_ws, uint64_t ws_bytes, void* stream);
+int32_t l0_loss_conjugate(int32_t loss, const double* d_zeta, const double* d_y, int64_t n,
+                          double* h_out, void* d_ws, uint64_t ws_bytes, void* stream);
+int32_t l0_all_finite(const void* d_x, int32_t dtype, int64_t rows, int64_t cols, int64_t ld,
+                      int32_t* h_ok, void* d_ws, uint64_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L0CERT_B200_H */

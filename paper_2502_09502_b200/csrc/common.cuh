@@ -1,0 +1,223 @@
+// Shared device-side definitions for the B200 dual-bound engine.
+//
+// Numerical contract: every elementwise formula
+// that the reference evaluates with numpy is evaluated here with one IEEE
+// rounding per operation in the same order (the __d*_rn intrinsics are never
+// contracted into FMA), so prox inputs, Huber values, losses and the momentum
+// step are bit-identical to the reference on identical inputs.  Reductions
+// (dot products, sums) use fixed-order trees: results are deterministic
+// run-to-run and differ from numpy/OpenBLAS only by summation order.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace l0 {
+
+enum Loss : int { SQUARED_ERROR = 0, LOGISTIC = 1, SQUARED_HINGE = 2 };
+enum Dtype : int { F64 = 0, F32 = 1 };
+enum Status : int {
+  ST_OK = 0, ST_INVALID = 1, ST_NUMERICAL = 2, ST_INFEASIBLE = 3, ST_UNSUPPORTED = 4, ST_CUDA = 5
+};
+enum Termination : int {
+  TERM_CONVERGED = 0, TERM_ITERATION_LIMIT = 1, TERM_TIME_LIMIT = 2,
+  TERM_PRIMAL_BELOW = 3, TERM_DUAL_ABOVE = 4
+};
+// per-coordinate node class (fista.py:109-128)
+enum NodeClass : uint8_t { FREE = 0, FIXED_ONE = 1, FIXED_ZERO = 2 };
+
+constexpr double kFeasRtol = 1e-9;     // perspective.py:23
+constexpr double kZeroAtol = 1e-9;     // perspective.py:25
+constexpr double kDomainSlack = 1e-12; // model.py:39
+
+// ---------------------------------------------------------------------------
+// exact (uncontracted) double arithmetic
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// np.sign: -1, 0, +1 (0 for +-0; NaN never reaches here)
+__device__ __forceinline__ double dsign(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
+
+// prox.py:35-43 — argmin_v (v-x)^2/2 + w H_M(v), x >= 0
+__device__ __forceinline__ double hprox(double x, double w, double M) {
+  double opw = dadd(1.0, w);
+  return (x <= dmul(M, opw)) ? ddiv(x, opw) : dsub(x, dmul(w, M));
+}
+
+// prox.py:27-32 — Huber H_M(x)
+__device__ __forceinline__ double huber(double x, double M) {
+  double a = fabs(x);
+  return (a <= M) ? dmul(dmul(0.5, x), x) : dsub(dmul(M, a), dmul(dmul(0.5, M), M));
+}
+
+// numpy's logaddexp(0, t) (npy_logaddexp with x = 0)
+__device__ __forceinline__ double logaddexp0(double t) {
+  if (t == 0.0) return 0.6931471805599453;  // x == y: x + log(2)
+  double tmp = -t;                          // x - y
+  if (tmp > 0.0) return log1p(exp(-tmp));
+  return dadd(t, log1p(exp(tmp)));
+}
+
+// scipy.special.expit: 1 / (1 + exp(-x))
+__device__ __forceinline__ double expit(double x) { return ddiv(1.0, dadd(1.0, exp(-x))); }
+
+// model.py:164-172 — per-sample loss term (summed by the caller)
+__device__ __forceinline__ double loss_term(int loss, double u, double y) {
+  if (loss == SQUARED_ERROR) { double d = dsub(u, y); return dmul(d, d); }
+  if (loss == LOGISTIC) return logaddexp0(dmul(-y, u));
+  double m = fmax(0.0, dsub(1.0, dmul(y, u)));
+  return dmul(m, m);
+}
+
+// model.py:190-195 — dF/du
+__device__ __forceinline__ double loss_grad(int loss, double u, double y) {
+  if (loss == SQUARED_ERROR) return dmul(2.0, dsub(u, y));
+  if (loss == LOGISTIC) return dmul(-y, expit(dmul(-y, u)));
+  double m = fmax(0.0, dsub(1.0, dmul(y, u)));
+  return dmul(dmul(-2.0, y), m);
+}
+
+// xlogy(r, r) with 0 log 0 = 0
+__device__ __forceinline__ double xlogx(double r) { return r == 0.0 ? 0.0 : dmul(r, log(r)); }
+
+// F*(-zeta) accumulators (model.py:239-253).  acc[0], acc[1] are sums, acc[2]
+// counts out-of-domain samples.  The conjugate is
+//   SE:     0.25 * acc0 - acc1   (acc0 = zeta.zeta, acc1 = y.zeta)
+//   others: acc0                  (+inf when acc2 > 0)
+__device__ __forceinline__ void conj_accumulate(int loss, double zeta, double y, double acc[3]) {
+  if (loss == SQUARED_ERROR) {
+    acc[0] = dadd(acc[0], dmul(zeta, zeta));
+    acc[1] = dadd(acc[1], dmul(y, zeta));
+  } else if (loss == LOGISTIC) {
+    double r = ddiv(zeta, y);
+    if (r < -kDomainSlack || r > dadd(1.0, kDomainSlack)) { acc[2] += 1.0; return; }
+    r = fmin(fmax(r, 0.0), 1.0);
+    acc[0] = dadd(acc[0], dadd(xlogx(r), xlogx(dsub(1.0, r))));
+  } else {
+    double z = dmul(-y, zeta);
+    if (z > kDomainSlack) { acc[2] += 1.0; return; }
+    z = fmin(z, 0.0);
+    acc[0] = dadd(acc[0], dadd(z, dmul(dmul(0.25, z), z)));
+  }
+}
+
+__device__ __forceinline__ double conj_finish(int loss, const double acc[3]) {
+  if (acc[2] > 0.0) return CUDART_INF;
+  if (loss == SQUARED_ERROR) return dsub(dmul(0.25, acc[0]), acc[1]);
+  return acc[0];
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum, fixed order (warp trees, then warp 0 over warp results).
+// `scratch` needs blockDim.x/32 doubles; result valid in every thread.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double x = lane < nw ? scratch[lane] : 0.0;
+    x = warp_sum(x);
+    if (lane == 0) scratch[0] = x;
+  }
+  __syncthreads();
+  double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* scratch) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double x = lane < nw ? scratch[lane] : -CUDART_INF;
+    x = warp_max(x);
+    if (lane == 0) scratch[0] = x;
+  }
+  __syncthreads();
+  double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Engine-wide structures (device memory)
+// ---------------------------------------------------------------------------
+
+// Per-solve scalars, read by the kernels from device memory so one captured
+// CUDA graph serves every solve on the same problem.
+struct Params {
+  double L, rho, two_l2, M;
+  double gap_tol, gap_tol_rel;
+  double early_primal, early_dual;  // NaN = unset
+  double parent_bound;
+  int64_t max_iter;
+  int64_t k;          // instance k
+  int64_t k_rem;      // prox budget over free coordinates: min(k - |F1|, |free|)
+  int64_t k_g;        // envelope budget over free coordinates: k - |F1| (unclipped)
+  int64_t n_free;     // number of free coordinates
+  int64_t n_fone;     // number of fixed-one coordinates
+  int bci;
+  int restart;
+  int stop_on_gap;
+  int node_mode;      // 0: trivial node
+  int loss;
+  int pad_;
+};
+
+// Trace record pushed at every bound check (fista.py:185-194)
+struct TraceRec {
+  double iteration, primal, dual, gap, restarted;
+};
+
+constexpr int kTraceCap = 256;
+
+// Iteration state machine (device memory; mirrored to pinned host memory at
+// the end of every captured chunk).
+struct State {
+  int64_t t;              // iterations completed
+  int64_t restarts;
+  int64_t err_iter;
+  int64_t trace_count;    // records ever written (ring index = count % kTraceCap)
+  int64_t phi;
+  int done;
+  int termination;
+  int err;                // Status
+  int dual_pending;       // a bound evaluation at beta_t is due (K2 adds the zeta column)
+  int check_pending;      // ... and it is a bound CHECK (max, gap, trace, tests)
+  int dual_only;          // no further iterations: K2 computes zeta only, K3 the bound only
+  int stop_term;          // termination applied after the pending check (-1: none)
+  int last_restarted;
+  int topk_fallbacks;     // diagnostics: g top-k window verification misses
+  int pad_;
+  double obj;             // composite objective at beta_t
+  double g_next;          // g(beta_next) from the prox kernel
+  double best_dual;
+  double gap;
+  double last_dual;
+  double loss_cur;
+  TraceRec trace[kTraceCap];
+};
+
+}  // namespace l0

@@ -1,0 +1,105 @@
+// Engine-wide kernel arguments and layout constants (shared by all .cu files).
+#pragma once
+
+#include "common.cuh"
+
+namespace l0 {
+
+// K1 (forward X.beta): CTA = 8 warps over a column slab of kK1Slab columns
+// whose beta slice is staged in shared memory; warps stream rows.
+constexpr int kK1Threads = 256;
+constexpr int kK1Slab = 2048;
+// K2 (transpose X^T r): CTA = 8 warps over one 256-column slab; each lane
+// accumulates 8 columns in registers, the warps split the chunk's rows, and a
+// fixed-order shared-memory tree combines the 8 warps.  Narrow slabs keep the
+// cross-CTA partials small (chunks x p values).
+constexpr int kK2Threads = 256;
+constexpr int kK2Slab = 256;
+constexpr int kK2StageRows = 256;                       // rows of r staged per pass
+constexpr int kPvAlign = 2048;                          // p-vector stride alignment
+constexpr int kTargetCtas = 148 * 4;
+
+enum KMode : int {
+  MODE_ITER = 0,    // FISTA iteration (ring buffers, fused epilogues)
+  MODE_INIT = 1,    // initial u_0 / objective
+  MODE_PLAIN = 2,   // standalone matvec on explicit vectors
+};
+
+struct EngineArgs {
+  // problem
+  const void* X;
+  const double* y;
+  int64_t n, p, ld;
+  int dtype;
+  int loss;
+  // launch layout
+  int k1_slabs, k1_chunks, k1_grid;   // work items = slabs x chunks, persistent grid
+  int k2_slabs, k2_chunks, k2_grid;
+  int64_t k1_rows, k2_rows;   // rows per chunk
+  int64_t pv;                 // stride of p-vectors (multiple of kPvAlign, >= ld)
+  // FISTA vectors
+  double* beta;      // ring [3][pv]
+  double* u;         // ring [3][n]
+  double* gam;       // gamma after the gradient step [pv]
+  double* key;       // sort keys |rho*gamma| (or -1 for fixed coords) [pv]
+  double* gv;        // [g (pv) | v = X^T zeta (pv) | F* acc (4) | loss, bad (2)] — one all-reduce
+  double* k2_part;   // [2][k2_chunks][pv]
+  double* k2_fpart;  // [k2_chunks][4]
+  double* u_part;    // [k1_slabs][n]
+  double* loss_part; // [k1_chunks][2] (sum, non-finite count)
+  unsigned* cnt;     // counters, see cnt_* helpers (zeroed once; kernels leave them zeroed)
+  // prox
+  double* xs;        // sorted keys [pv]
+  int* perm;         // sorted coordinate ids [pv]
+  int* iota;         // 0..p-1 (device sort path)
+  double* tail;      // tail prefix sums [pv]
+  double* scratch;   // [pv] scratch (Huber values, |beta|)
+  const uint8_t* mask;  // node classes, nullable
+  const int* fone;      // fixed-one ids (sorted), Params::n_fone of them
+  // control
+  State* st;
+  const Params* prm;
+  int multi;         // row-sharded: global epilogues run as separate kernels
+  int plain_rhs2;    // PLAIN K2: number of RHS columns
+  // PLAIN-mode vectors
+  const double* in_vec;
+  double* out_vec;
+  const double* in_vec2;
+  double* out_vec2;
+};
+
+// counter block: [k2 work, k2 exit, k2 all | k1 work, k1 exit, k1 all | k2 slabs... | k1 chunks...]
+__device__ __forceinline__ unsigned* cnt_k2_work(const EngineArgs& a) { return a.cnt + 0; }
+__device__ __forceinline__ unsigned* cnt_k2_exit(const EngineArgs& a) { return a.cnt + 1; }
+__device__ __forceinline__ unsigned* cnt_k2_all(const EngineArgs& a) { return a.cnt + 2; }
+__device__ __forceinline__ unsigned* cnt_k1_work(const EngineArgs& a) { return a.cnt + 3; }
+__device__ __forceinline__ unsigned* cnt_k1_exit(const EngineArgs& a) { return a.cnt + 4; }
+__device__ __forceinline__ unsigned* cnt_k1_all(const EngineArgs& a) { return a.cnt + 5; }
+__device__ __forceinline__ unsigned* cnt_k2_slab(const EngineArgs& a) { return a.cnt + 8; }
+__device__ __forceinline__ unsigned* cnt_k1_chunk(const EngineArgs& a) { return a.cnt + 8 + a.k2_slabs; }
+inline int64_t counter_words(int k2_slabs, int k1_chunks) { return 8 + k2_slabs + k1_chunks; }
+
+__device__ __forceinline__ int64_t ring(int64_t t) { return ((t % 3) + 3) % 3; }
+
+// FISTA momentum coefficient (fista.py:161): phi / (phi + 3.0)
+__device__ __forceinline__ double momentum(int64_t phi) {
+  double f = (double)phi;
+  return ddiv(f, dadd(f, 3.0));
+}
+
+// bound check cadence (fista.py:182)
+__device__ __forceinline__ bool is_check(int64_t t, int bci) { return t == 1 || (t % bci) == 0; }
+
+// Launch helpers (defined in gemv.cu / prox.cu)
+cudaError_t launch_k1(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_k2(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_grad_step(const EngineArgs& a, cudaStream_t s);
+int k1_blocks_per_sm(int dtype);
+int k2_blocks_per_sm(int dtype);
+cudaError_t launch_objective(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_prox_iter(const EngineArgs& a, void* sort_tmp, size_t sort_tmp_bytes,
+                             cudaStream_t s);
+size_t prox_sort_tmp_bytes(int64_t p);
+bool prox_block_path(int64_t p);
+
+}  // namespace l0

@@ -1,0 +1,639 @@
+// Host side of the engine: problem layout, workspace carving, the FISTA driver
+// loop (CUDA graphs of `chunk` iterations, device-resident control state), and
+// NCCL row sharding.  fista.py:76-222 is the behaviour being reproduced.
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <nccl.h>
+
+#include "control.cuh"
+#include "engine.cuh"
+#include "prox.cuh"
+#include "l0cert_b200.h"
+
+namespace l0 {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define L0_CUDA_TRY(expr)                                                            \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return set_error(ST_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr int L0_ABORTED_CODE = 6;
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (only row-sharded solves need it)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { *err = "cannot dlopen libnccl.so.2"; return false; }
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    if (!commInitRank || !allReduce || !commDestroy) { *err = "NCCL symbols missing"; return false; }
+    return true;
+  }
+};
+static NcclApi g_nccl;
+
+// ---------------------------------------------------------------------------
+// problem
+// ---------------------------------------------------------------------------
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int G = 0;
+  int profile = 0;
+  int64_t kernels = 0;
+  std::vector<cudaEvent_t> ev;  // profile: [iter][k2b,k2e,k3b,k3e,k1b,k1e]
+};
+
+struct Problem {
+  EngineArgs a{};
+  int sm_count = 148;
+  uint64_t ws_bytes = 0;
+  void* ws = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  Params* d_prm = nullptr;
+  double* d_small = nullptr;  // 64 doubles of scratch
+  double* d_vec_n = nullptr;  // n doubles
+  double* d_vec_p = nullptr;  // pv doubles
+  uint8_t* d_mask = nullptr;
+  int* d_fone = nullptr;
+  State* h_st[2] = {nullptr, nullptr};  // pinned mirrors (double-buffered chunks)
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_chunk[2] = {nullptr, nullptr};
+  Graph graph[2];
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+}  // namespace l0
+
+struct l0_problem : l0::Problem {};
+
+namespace l0 {
+
+static int compute_layout(Problem& P) {
+  EngineArgs& a = P.a;
+  const int64_t n = a.n, p = a.p;
+  a.pv = round_up(std::max(p, a.ld), kPvAlign);
+  int dev = 0;
+  L0_CUDA_TRY(cudaGetDevice(&dev));
+  L0_CUDA_TRY(cudaDeviceGetAttribute(&P.sm_count, cudaDevAttrMultiProcessorCount, dev));
+  const int sms = P.sm_count > 0 ? P.sm_count : 148;
+  // K1: kK1Slab-wide slabs, ~8 items per resident CTA
+  a.k1_slabs = (int)ceil_div(p, kK1Slab);
+  int64_t k1_res = (int64_t)sms * k1_blocks_per_sm(a.dtype);
+  int64_t chunks = std::max<int64_t>(1, ceil_div(k1_res * 8, a.k1_slabs));
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, 8)));
+  a.k1_rows = ceil_div(n, chunks);
+  a.k1_chunks = (int)ceil_div(n, a.k1_rows);
+  a.k1_grid = (int)std::min<int64_t>(k1_res, (int64_t)a.k1_slabs * a.k1_chunks);
+  // K2: 256-column slabs
+  a.k2_slabs = (int)ceil_div(p, kK2Slab);
+  int64_t k2_res = (int64_t)sms * k2_blocks_per_sm(a.dtype);
+  chunks = std::max<int64_t>(1, ceil_div(k2_res * 8, a.k2_slabs));
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, 16)));
+  a.k2_rows = ceil_div(n, chunks);
+  a.k2_chunks = (int)ceil_div(n, a.k2_rows);
+  a.k2_grid = (int)std::min<int64_t>(k2_res, (int64_t)a.k2_slabs * a.k2_chunks);
+  P.sort_tmp_bytes = std::max(prox_sort_tmp_bytes(std::max<int64_t>(p, 1)), (size_t)256);
+  size_t keys_only = 0;
+  cub::DeviceRadixSort::SortKeysDescending<double>(nullptr, keys_only, (const double*)nullptr,
+                                                   (double*)nullptr, (int)std::max<int64_t>(p, 1));
+  P.sort_tmp_bytes = std::max(P.sort_tmp_bytes, keys_only);
+  return ST_OK;
+}
+
+// carve the workspace; returns bytes needed (and assigns pointers when base != null)
+static uint64_t carve(Problem& P, char* base) {
+  EngineArgs& a = P.a;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) -> char* {
+    off = (off + 255) & ~uint64_t(255);
+    char* r = base ? base + off : nullptr;
+    off += bytes;
+    return r;
+  };
+  const int64_t n = a.n, pv = a.pv;
+  P.d_prm = (Params*)take(sizeof(Params));
+  a.st = (State*)take(sizeof(State));
+  a.beta = (double*)take(8ull * 3 * pv);
+  a.u = (double*)take(8ull * 3 * n);
+  a.gam = (double*)take(8ull * pv);
+  a.key = (double*)take(8ull * pv);
+  a.xs = (double*)take(8ull * pv);
+  a.tail = (double*)take(8ull * pv);
+  a.scratch = (double*)take(8ull * pv);
+  a.gv = (double*)take(8ull * (2 * pv + 8));
+  a.k2_part = (double*)take(8ull * 2 * a.k2_chunks * pv);
+  a.k2_fpart = (double*)take(8ull * 4 * a.k2_chunks);
+  a.u_part = (double*)take(8ull * a.k1_slabs * n);
+  a.loss_part = (double*)take(8ull * 2 * a.k1_chunks);
+  a.cnt = (unsigned*)take(4ull * counter_words(a.k2_slabs, a.k1_chunks));
+  a.perm = (int*)take(4ull * pv);
+  a.iota = (int*)take(4ull * pv);
+  P.d_mask = (uint8_t*)take(pv);
+  P.d_fone = (int*)take(4ull * pv);
+  P.sort_tmp = take(P.sort_tmp_bytes);
+  P.d_small = (double*)take(8ull * 64);
+  P.d_vec_n = (double*)take(8ull * n);
+  P.d_vec_p = (double*)take(8ull * pv);
+  a.prm = P.d_prm;
+  return off + 256;
+}
+
+static void destroy_graphs(Problem& P) {
+  for (auto& g : P.graph) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto e : g.ev) cudaEventDestroy(e);
+    g = Graph{};
+  }
+}
+
+// one FISTA iteration's launches (captured into the chunk graph)
+static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
+  EngineArgs& a = P.a;
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
+  L0_CUDA_TRY(launch_k2(a, MODE_ITER, s));
+  if (a.multi) {
+    ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)(2 * a.pv + 3), ncclDouble, ncclSum,
+                                      P.comm, s);
+    if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (gradient) failed");
+    L0_CUDA_TRY(launch_grad_step(a, s));
+  }
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
+  L0_CUDA_TRY(launch_prox_iter(a, P.sort_tmp, P.sort_tmp_bytes, s));
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[4], s, cudaEventRecordExternal));
+  L0_CUDA_TRY(launch_k1(a, MODE_ITER, s));
+  if (a.multi) {
+    ncclResult_t r = g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
+                                      ncclSum, P.comm, s);
+    if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (loss) failed");
+    L0_CUDA_TRY(launch_objective(a, MODE_ITER, s));
+  }
+  if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[5], s, cudaEventRecordExternal));
+  return ST_OK;
+}
+
+static int build_graph(Problem& P, int which, int G, int profile) {
+  Graph& g = P.graph[which];
+  if (g.exec && g.G == G && g.profile == profile) return ST_OK;
+  if (g.exec) {
+    cudaGraphExecDestroy(g.exec);
+    for (auto e : g.ev) cudaEventDestroy(e);
+    g = Graph{};
+  }
+  if (profile) {
+    g.ev.resize((size_t)G * 6);
+    for (auto& e : g.ev) L0_CUDA_TRY(cudaEventCreate(&e));
+  }
+  cudaStream_t s = P.stream;
+  L0_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = ST_OK;
+  for (int i = 0; i < G && rc == ST_OK; ++i)
+    rc = launch_iteration(P, s, profile ? &g.ev[(size_t)i * 6] : nullptr);
+  if (rc == ST_OK) {
+    cudaError_t e = cudaMemcpyAsync(P.h_st[which], P.a.st, sizeof(State), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = set_error(ST_CUDA, cudaGetErrorString(e));
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (rc != ST_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return set_error(ST_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+  size_t nn = 0;
+  L0_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  L0_CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_error(ST_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+  g.G = G;
+  g.profile = profile;
+  g.kernels = kernels;
+  return ST_OK;
+}
+
+// g(beta) of an arbitrary vector (standalone path: sort |beta| then the
+// envelope kernel), written to *d_out
+static int envelope_of(Problem& P, const double* d_beta, int64_t kg, int64_t nf, double M,
+                       const uint8_t* d_mask, const int* d_fone, int64_t n_fone, double* d_out,
+                       cudaStream_t s, int64_t* launches) {
+  EngineArgs& a = P.a;
+  const int64_t p = a.p;
+  int* flags = reinterpret_cast<int*>(P.d_small);
+  L0_CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
+  const int blocks = (int)std::min<int64_t>(ceil_div(p, 256), 1024);
+  k_abs_free<<<blocks, 256, 0, s>>>(d_beta, p, d_mask, M, a.scratch, flags);
+  L0_CUDA_TRY(cudaGetLastError());
+  size_t bytes = P.sort_tmp_bytes;
+  L0_CUDA_TRY(cub::DeviceRadixSort::SortKeysDescending(P.sort_tmp, bytes, a.scratch, P.d_vec_p,
+                                                       (int)p, 0, 64, s));
+  k_g_value_final<<<1, 1024, 0, s>>>(P.d_vec_p, p, nf, kg, M, d_beta, d_fone, n_fone, flags,
+                                     d_out);
+  L0_CUDA_TRY(cudaGetLastError());
+  if (launches) *launches += 4;
+  return ST_OK;
+}
+
+static int auto_chunk(const Problem& P, int bci) {
+  const EngineArgs& a = P.a;
+  const double bytes = 2.0 * (double)a.n * (double)a.ld * (a.dtype == F64 ? 8.0 : 4.0);
+  const double t_it = bytes / 6.0e12 + 40e-6;  // seconds, rough
+  int G = (int)std::ceil(4e-3 / t_it);
+  G = std::max(4, std::min(G, 100));
+  (void)bci;
+  return G;
+}
+
+}  // namespace l0
+
+using namespace l0;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* l0_last_error(void) { return g_last_error.c_str(); }
+int32_t l0_abi_version(void) { return 1; }
+
+int32_t l0_problem_create(const void* d_X, int32_t dtype, int64_t n, int64_t p, int64_t ld,
+                          const double* d_y, int32_t loss, l0_problem** out) {
+  if (!out) return set_error(ST_INVALID, "out is null");
+  *out = nullptr;
+  if (!d_X || !d_y) return set_error(ST_INVALID, "X and y must be device pointers");
+  if (dtype != F64 && dtype != F32) return set_error(ST_INVALID, "dtype must be L0_F64 or L0_F32");
+  if (n < 1 || p < 1) return set_error(ST_INVALID, "n and p must be positive");
+  if (p > (int64_t)INT32_MAX - 4096) return set_error(ST_INVALID, "p too large");
+  const int64_t es = dtype == F64 ? 8 : 4;
+  if (ld < p || (ld * es) % 16 != 0) return set_error(ST_INVALID, "ld must be >= p and a multiple of 16 bytes");
+  if (((uintptr_t)d_X) % 16 != 0) return set_error(ST_INVALID, "X must be 16-byte aligned");
+  if (loss < 0 || loss > 2) return set_error(ST_UNSUPPORTED, "loss must be squared_error, logistic or squared_hinge");
+  l0_problem* P = new l0_problem();
+  P->a.X = d_X;
+  P->a.y = d_y;
+  P->a.n = n;
+  P->a.p = p;
+  P->a.ld = ld;
+  P->a.dtype = dtype;
+  P->a.loss = loss;
+  int rc = compute_layout(*P);
+  if (rc != ST_OK) { delete P; return rc; }
+  P->ws_bytes = carve(*P, nullptr);
+  cudaError_t e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->ev_out, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&P->ev_chunk[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&P->h_st[i], sizeof(State));
+  }
+  if (e != cudaSuccess) {
+    l0_problem_destroy(P);
+    return set_error(ST_CUDA, cudaGetErrorString(e));
+  }
+  *out = P;
+  return ST_OK;
+}
+
+int32_t l0_problem_workspace_bytes(const l0_problem* prob, uint64_t* bytes) {
+  if (!prob || !bytes) return set_error(ST_INVALID, "null argument");
+  *bytes = prob->ws_bytes;
+  return ST_OK;
+}
+
+int32_t l0_problem_set_workspace(l0_problem* P, void* d_ws, uint64_t bytes) {
+  if (!P || !d_ws) return set_error(ST_INVALID, "null argument");
+  if (bytes < P->ws_bytes) return set_error(ST_INVALID, "workspace too small");
+  destroy_graphs(*P);
+  P->ws = d_ws;
+  carve(*P, (char*)d_ws);
+  EngineArgs& a = P->a;
+  L0_CUDA_TRY(cudaMemsetAsync(a.cnt, 0, 4 * counter_words(a.k2_slabs, a.k1_chunks), P->stream));
+  L0_CUDA_TRY(cudaMemsetAsync(a.gv, 0, 8 * (2 * a.pv + 8), P->stream));
+  k_iota<<<(int)std::min<int64_t>(ceil_div(a.pv, 256), 1024), 256, 0, P->stream>>>(a.iota, a.pv);
+  L0_CUDA_TRY(cudaGetLastError());
+  L0_CUDA_TRY(cudaStreamSynchronize(P->stream));
+  return ST_OK;
+}
+
+int32_t l0_problem_destroy(l0_problem* P) {
+  if (!P) return ST_OK;
+  destroy_graphs(*P);
+  if (P->comm && g_nccl.commDestroy) g_nccl.commDestroy(P->comm);
+  for (int i = 0; i < 2; ++i) {
+    if (P->h_st[i]) cudaFreeHost(P->h_st[i]);
+    if (P->ev_chunk[i]) cudaEventDestroy(P->ev_chunk[i]);
+  }
+  if (P->ev_in) cudaEventDestroy(P->ev_in);
+  if (P->ev_out) cudaEventDestroy(P->ev_out);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+  return ST_OK;
+}
+
+int32_t l0_problem_set_comm(l0_problem* P, const void* h_id, int32_t nranks, int32_t rank) {
+  if (!P || !h_id) return set_error(ST_INVALID, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(ST_INVALID, "bad rank");
+  if (nranks == 1) {
+    P->a.multi = 0;
+    return ST_OK;
+  }
+  std::string err;
+  if (!g_nccl.load(&err)) return set_error(ST_CUDA, err);
+  ncclUniqueId id;
+  std::memcpy(&id, h_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = g_nccl.commInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess)
+    return set_error(ST_CUDA, std::string("ncclCommInitRank: ") +
+                                  (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  destroy_graphs(*P);
+  P->comm = comm;
+  P->nranks = nranks;
+  P->rank = rank;
+  P->a.multi = 1;
+  return ST_OK;
+}
+
+static int check_ready(const l0_problem* P) {
+  if (!P) return set_error(ST_INVALID, "null problem");
+  if (!P->ws) return set_error(ST_INVALID, "problem has no workspace (l0_problem_set_workspace)");
+  return ST_OK;
+}
+
+int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
+                       const l0_fista_opts* o, const l0_node* node, const double* d_warm,
+                       double* d_beta_out, l0_report* rep, l0_trace_cb cb, void* user,
+                       void* stream) {
+  int rc = check_ready(P);
+  if (rc) return rc;
+  if (!o || !rep || !d_beta_out) return set_error(ST_INVALID, "null argument");
+  std::memset(rep, 0, sizeof(*rep));
+  EngineArgs& a = P->a;
+  const int64_t p = a.p;
+  // ---- validation (model.py:102-107, fista.py:55-61, perspective.py:36-47) ----
+  if (!(k >= 1 && k <= p)) return set_error(ST_INVALID, "k must satisfy 1 <= k <= p");
+  if (!(M > 0 && std::isfinite(M))) return set_error(ST_INVALID, "M must be a positive finite real");
+  if (!(lambda2 > 0 && std::isfinite(lambda2)))
+    return set_error(ST_INVALID, "lambda2 must be a positive finite real");
+  if (!(o->gap_tolerance > 0)) return set_error(ST_INVALID, "gap_tolerance must be positive");
+  if (o->bound_check_interval < 1) return set_error(ST_INVALID, "bound_check_interval must be >= 1");
+  if (o->max_iterations < 1) return set_error(ST_INVALID, "max_iterations must be >= 1");
+  if (!(o->lipschitz > 0) || std::isnan(o->lipschitz))
+    return set_error(ST_INVALID, "lipschitz constant must be provided and positive");
+
+  std::vector<uint8_t> mask;
+  std::vector<int> fone;
+  int64_t n1 = 0, n0 = 0;
+  double parent_bound = -INFINITY;
+  if (node) {
+    parent_bound = node->parent_bound;
+    n1 = node->n_fixed_one;
+    n0 = node->n_fixed_zero;
+    if (n1 + n0 > 0) {
+      mask.assign((size_t)p, (uint8_t)FREE);
+      for (int64_t i = 0; i < n1; ++i) {
+        int64_t j = node->h_fixed_one[i];
+        if (j < 0 || j >= p) return set_error(ST_INVALID, "fixed_one index out of range");
+        if (mask[j] != FREE) return set_error(ST_INVALID, "duplicate fixed index");
+        mask[j] = FIXED_ONE;
+        fone.push_back((int)j);
+      }
+      for (int64_t i = 0; i < n0; ++i) {
+        int64_t j = node->h_fixed_zero[i];
+        if (j < 0 || j >= p) return set_error(ST_INVALID, "fixed_zero index out of range");
+        if (mask[j] != FREE) return set_error(ST_INVALID, "fixed_one and fixed_zero must be disjoint");
+        mask[j] = FIXED_ZERO;
+      }
+      std::sort(fone.begin(), fone.end());
+    }
+  }
+  if (n1 > k) return set_error(ST_INFEASIBLE, "|fixed_one| exceeds the budget k");
+  const bool node_mode = (n1 + n0) > 0;
+  const int64_t nfree = p - n1 - n0;
+
+  Params hp{};
+  hp.L = std::max(o->lipschitz, 1e-12);   // fista.py:101
+  hp.two_l2 = 2.0 * lambda2;              // fista.py:98
+  hp.rho = hp.L / hp.two_l2;              // fista.py:102
+  hp.M = M;
+  hp.gap_tol = o->gap_tolerance;
+  hp.gap_tol_rel = o->gap_tolerance_rel;
+  hp.early_primal = o->early_primal_cutoff;
+  hp.early_dual = o->early_dual_cutoff;
+  hp.parent_bound = parent_bound;
+  hp.max_iter = o->max_iterations;
+  hp.k = k;
+  hp.k_g = k - n1;
+  hp.k_rem = std::min(k - n1, nfree);
+  hp.n_free = nfree;
+  hp.n_fone = n1;
+  hp.bci = o->bound_check_interval;
+  hp.restart = o->restart ? 1 : 0;
+  hp.stop_on_gap = o->stop_on_gap ? 1 : 0;
+  hp.node_mode = node_mode ? 1 : 0;
+  hp.loss = a.loss;
+  // the captured graphs always see the node buffers; Params::node_mode gates their use
+  a.mask = P->d_mask;
+  a.fone = P->d_fone;
+  const uint8_t* h_mask_ptr = node_mode ? P->d_mask : nullptr;
+  const int* h_fone_ptr = node_mode ? P->d_fone : nullptr;
+
+  auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t user_s = (cudaStream_t)stream;
+  cudaStream_t s = P->stream;
+  L0_CUDA_TRY(cudaEventRecord(P->ev_in, user_s));
+  L0_CUDA_TRY(cudaStreamWaitEvent(s, P->ev_in, 0));
+  L0_CUDA_TRY(cudaMemcpyAsync(P->d_prm, &hp, sizeof(Params), cudaMemcpyHostToDevice, s));
+  if (node_mode) {
+    L0_CUDA_TRY(cudaMemcpyAsync(P->d_mask, mask.data(), (size_t)p, cudaMemcpyHostToDevice, s));
+    if (!fone.empty())
+      L0_CUDA_TRY(cudaMemcpyAsync(P->d_fone, fone.data(), 4 * fone.size(), cudaMemcpyHostToDevice, s));
+  }
+  int64_t launches = 0;
+  k_state_init<<<1, 1, 0, s>>>(a.st, parent_bound);
+  ++launches;
+  const size_t vb = 8ull * (size_t)p;
+  if (d_warm) {
+    L0_CUDA_TRY(cudaMemcpyAsync(a.beta, d_warm, vb, cudaMemcpyDeviceToDevice, s));
+    L0_CUDA_TRY(cudaMemcpyAsync(a.beta + 2 * a.pv, d_warm, vb, cudaMemcpyDeviceToDevice, s));
+    // g(beta_0) for the initial composite objective (fista.py:143)
+    rc = envelope_of(*P, a.beta, hp.k_g, nfree, M, h_mask_ptr, h_fone_ptr, n1, &a.st->g_next, s,
+                     &launches);
+    if (rc) return rc;
+  } else {
+    L0_CUDA_TRY(cudaMemsetAsync(a.beta, 0, vb, s));
+    L0_CUDA_TRY(cudaMemsetAsync(a.beta + 2 * a.pv, 0, vb, s));
+  }
+  L0_CUDA_TRY(launch_k1(a, MODE_INIT, s));  // u_0 = X beta_0, F(u_0), objective
+  ++launches;
+  if (a.multi) {
+    if (g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble, ncclSum, P->comm,
+                         s) != ncclSuccess)
+      return set_error(ST_CUDA, "ncclAllReduce (initial loss) failed");
+    L0_CUDA_TRY(launch_objective(a, MODE_INIT, s));
+    ++launches;
+  }
+
+  // ---- chunked iteration: graph replays, double-buffered state mirrors ------
+  const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100)
+                                        : auto_chunk(*P, o->bound_check_interval);
+  for (int w = 0; w < 2; ++w) {
+    rc = build_graph(*P, w, G, o->profile ? 1 : 0);
+    if (rc) return rc;
+  }
+  int64_t trace_seen = 0;
+  int64_t chunks = 0;
+  bool aborted = false, stop_sent = false;
+  int64_t t_before[2] = {0, 0};
+  int64_t t_prev = 0;
+  State* last = nullptr;
+  int inflight = 0;
+  int next = 0;
+  auto launch_chunk = [&](int w) -> int {
+    L0_CUDA_TRY(cudaGraphLaunch(P->graph[w].exec, s));
+    L0_CUDA_TRY(cudaEventRecord(P->ev_chunk[w], s));
+    return ST_OK;
+  };
+  // keep two chunks in flight
+  for (int w = 0; w < 2; ++w) {
+    rc = launch_chunk(w);
+    if (rc) return rc;
+    ++inflight;
+  }
+  while (inflight > 0) {
+    const int w = next;
+    next ^= 1;
+    L0_CUDA_TRY(cudaEventSynchronize(P->ev_chunk[w]));
+    --inflight;
+    ++chunks;
+    State* h = P->h_st[w];
+    last = h;
+    // profile: accumulate the kernel times of the iterations this chunk executed
+    if (o->profile) {
+      const int64_t did = std::max<int64_t>(0, std::min<int64_t>(G, h->t - t_prev));
+      Graph& g = P->graph[w];
+      for (int64_t i = 0; i < did; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 0], g.ev[i * 6 + 1]) == cudaSuccess) { rep->k2_ms += ms; rep->k2_count++; }
+        if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 2], g.ev[i * 6 + 3]) == cudaSuccess) { rep->k3_ms += ms; rep->k3_count++; }
+        if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 4], g.ev[i * 6 + 5]) == cudaSuccess) { rep->k1_ms += ms; rep->k1_count++; }
+      }
+    }
+    t_prev = h->t;
+    (void)t_before;
+    // trace records, in order (fista.py:185-194)
+    if (cb && !aborted) {
+      for (; trace_seen < h->trace_count; ++trace_seen) {
+        const TraceRec& r = h->trace[trace_seen % kTraceCap];
+        l0_trace_record rec{r.iteration, r.primal, r.dual, r.gap, r.restarted};
+        if (cb(&rec, user) != 0) {
+          aborted = true;
+          break;
+        }
+      }
+    }
+    if (h->done || aborted) {
+      // drain the other in-flight chunk (all no-ops or the tail)
+      if (inflight > 0) {
+        L0_CUDA_TRY(cudaEventSynchronize(P->ev_chunk[next]));
+        --inflight;
+        ++chunks;
+        if (P->h_st[next]->t >= h->t) last = P->h_st[next];
+      }
+      break;
+    }
+    const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (!stop_sent && elapsed > o->time_limit) {  // fista.py:204-206 (checked per chunk)
+      k_request_stop<<<1, 1, 0, s>>>(a.st, P->d_prm, TERM_TIME_LIMIT);
+      L0_CUDA_TRY(cudaGetLastError());
+      ++launches;
+      stop_sent = true;
+    }
+    rc = launch_chunk(w);
+    if (rc) return rc;
+    ++inflight;
+  }
+  launches += chunks * P->graph[0].kernels;
+  const State* h = last;
+  if (aborted) {
+    L0_CUDA_TRY(cudaStreamSynchronize(s));
+    rep->status = L0_ABORTED_CODE;
+    return set_error(L0_ABORTED_CODE, "aborted by the trace callback");
+  }
+  // ---- report (fista.py:213-222) -------------------------------------------
+  rep->primal_value = h->obj;
+  rep->dual_bound = h->best_dual;
+  rep->gap = h->gap;
+  rep->iterations = h->t;
+  rep->restarts = h->restarts;
+  rep->termination = h->termination;
+  rep->status = h->err;
+  rep->error_iteration = h->err_iter;
+  rep->topk_fallbacks = h->topk_fallbacks;
+  L0_CUDA_TRY(cudaMemcpyAsync(d_beta_out, a.beta + ((h->t % 3)) * a.pv, vb,
+                              cudaMemcpyDeviceToDevice, s));
+  L0_CUDA_TRY(cudaEventRecord(P->ev_out, s));
+  L0_CUDA_TRY(cudaStreamWaitEvent(user_s, P->ev_out, 0));
+  L0_CUDA_TRY(cudaStreamSynchronize(s));
+  rep->gpu_launches = launches;
+  rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (h->err != ST_OK) {
+    if (h->err == ST_NUMERICAL)
+      return set_error(ST_NUMERICAL, "composite objective became non-finite at iteration " +
+                                         std::to_string(h->err_iter) +
+                                         "; the step-size constant is likely too small");
+    if (h->err == ST_INVALID) return set_error(ST_INVALID, "u contains non-finite entries");
+    if (h->err == ST_UNSUPPORTED)
+      return set_error(ST_UNSUPPORTED, "budget k too large for the on-chip envelope kernel");
+    return set_error(h->err, "solve failed");
+  }
+  return ST_OK;
+}
+
+}  // extern "C"

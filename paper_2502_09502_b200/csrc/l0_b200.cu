@@ -1,0 +1,7 @@
+// Unity translation unit of libl0b200.so: one TU so every device function is
+// visible to every kernel without relocatable device code.
+#include "gemv.cu"
+#include "prox.cu"
+#include "ops.cu"
+#include "engine_host.cu"
+#include "abi_ops.cu"

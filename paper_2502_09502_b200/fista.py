@@ -1,0 +1,183 @@
+"""Restarted FISTA on the perspective relaxation — drop-in for l0cert.fista.
+
+``solve_relaxation(instance, node=None, warm_start=None, opts=None)`` keeps the
+signature, options, report, trace-hook records and exceptions of
+/root/reference/pkg/src/l0cert/fista.py:35-222.  The whole loop runs on the
+B200: one C-ABI call (``l0_fista_solve``) replays CUDA graphs of K2 (transpose
+pass + gradient step), K3 (bound check, sort, PAVA, scatter, envelope) and K1
+(forward pass, loss, objective, restart) with the control state resident on
+the device; the host only reads the state between graph replays.
+
+Differences a caller can observe (documented in DESIGN.md):
+* ``time_limit`` is checked between graph replays (a few ms apart), not after
+  every iteration;
+* ``trace_hook`` is called with the same records, in order, but in batches;
+* engine-only options: ``gap_tolerance_rel``, ``stop_on_gap``,
+  ``chunk_iterations``, ``profile`` (defaults reproduce the reference).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import native
+from .errors import InvalidInputError, NumericalError, UnsupportedOperationError
+from .model import NodeState, ProblemInstance, is_solver_grade, lipschitz_constant
+from .perspective import EnvelopeParams
+
+__all__ = ["FistaOptions", "Termination", "RelaxationReport", "solve_relaxation"]
+
+
+class Termination(Enum):
+    CONVERGED = "converged"
+    ITERATION_LIMIT = "iteration_limit"
+    TIME_LIMIT = "time_limit"
+    PRIMAL_BELOW_INCUMBENT = "primal_below_incumbent"
+    DUAL_ABOVE_INCUMBENT = "dual_above_incumbent"
+
+
+@dataclass
+class FistaOptions:
+    max_iterations: int = 100_000
+    gap_tolerance: float = 1e-6
+    time_limit: float = np.inf
+    early_primal_cutoff: Optional[float] = None
+    early_dual_cutoff: Optional[float] = None
+    bound_check_interval: int = 10
+    restart: bool = True
+    lipschitz: Optional[float] = None
+    trace_hook: Optional[Callable[[dict], None]] = None
+    # ---- engine extensions (defaults = reference behaviour) ----
+    gap_tolerance_rel: float = 0.0      # also stop at gap <= rel * |primal|
+    stop_on_gap: bool = True            # False: fixed-iteration runs
+    chunk_iterations: int = 0           # iterations per CUDA graph replay (0: auto)
+    profile: bool = False               # time K1/K2/K3 with CUDA events
+
+    def __post_init__(self):
+        if self.gap_tolerance <= 0:
+            raise InvalidInputError("gap_tolerance must be positive")
+        if self.bound_check_interval < 1:
+            raise InvalidInputError("bound_check_interval must be >= 1")
+        if self.max_iterations < 1:
+            raise InvalidInputError("max_iterations must be >= 1")
+
+
+@dataclass
+class RelaxationReport:
+    beta: np.ndarray
+    primal_value: float
+    dual_bound: float
+    gap: float
+    iterations: int
+    restarts: int
+    termination: Termination
+    wall_time: float = field(default=0.0)
+    # engine metrics (not in the reference report)
+    stats: dict = field(default_factory=dict, repr=False)
+
+
+_TERM = {i: Termination(v) for i, v in enumerate(native.TERMINATIONS)}
+
+
+def _opt(x) -> float:
+    return math.nan if x is None else float(x)
+
+
+def solve_relaxation(instance: ProblemInstance, node: Optional[NodeState] = None,
+                     warm_start=None, opts: Optional[FistaOptions] = None,
+                     return_device: bool = False) -> RelaxationReport:
+    """Solve the (node-restricted) perspective relaxation on the B200
+    (fista.py:76-222).  ``return_device=True`` leaves ``report.beta`` as a CUDA
+    tensor instead of copying it to a numpy array."""
+    opts = opts or FistaOptions()
+    if not is_solver_grade(instance.loss):
+        raise UnsupportedOperationError(
+            f"{instance.loss.value} is bound-grade; the relaxation solver needs a "
+            "Lipschitz-smooth gradient")
+    p = instance.p
+    EnvelopeParams.for_instance(instance, node)          # InfeasibleNodeError (fista.py:97)
+    L = opts.lipschitz if opts.lipschitz is not None else lipschitz_constant(instance)
+
+    import torch
+    from . import _device
+    lib = native.load()
+    dp = instance.device_problem()
+
+    if warm_start is None and node is not None and node.warm_start is not None:
+        warm_start = node.warm_start
+    warm = None
+    if warm_start is not None:
+        warm = _device.to_cuda_f64(warm_start)
+        if tuple(warm.shape) != (p,):
+            raise InvalidInputError("warm start has the wrong dimension")
+
+    o = native.FistaOpts()
+    o.max_iterations = int(opts.max_iterations)
+    o.gap_tolerance = float(opts.gap_tolerance)
+    o.time_limit = float(opts.time_limit)
+    o.early_primal_cutoff = _opt(opts.early_primal_cutoff)
+    o.early_dual_cutoff = _opt(opts.early_dual_cutoff)
+    o.bound_check_interval = int(opts.bound_check_interval)
+    o.restart = 1 if opts.restart else 0
+    o.lipschitz = float(L)
+    o.gap_tolerance_rel = float(opts.gap_tolerance_rel)
+    o.stop_on_gap = 1 if opts.stop_on_gap else 0
+    o.chunk_iterations = int(opts.chunk_iterations)
+    o.profile = 1 if opts.profile else 0
+
+    nd = None
+    keep = []
+    if node is not None:
+        nd = native.Node()
+        f1 = np.ascontiguousarray(node.fixed_one, dtype=np.int64)
+        f0 = np.ascontiguousarray(node.fixed_zero, dtype=np.int64)
+        keep += [f1, f0]
+        nd.h_fixed_one = f1.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        nd.n_fixed_one = f1.size
+        nd.h_fixed_zero = f0.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        nd.n_fixed_zero = f0.size
+        nd.parent_bound = float(node.parent_bound)
+
+    hook = opts.trace_hook
+    raised = []
+
+    def _cb(rec_ptr, _user):
+        r = rec_ptr.contents
+        try:
+            hook({"iteration": int(r.iteration), "primal": float(r.primal),
+                  "dual": float(r.dual), "gap": float(r.gap), "restarted": bool(r.restarted)})
+        except BaseException as exc:  # re-raised after the engine unwinds
+            raised.append(exc)
+            return 1
+        return 0
+
+    cb = native.TRACE_CB(_cb) if hook is not None else native.TRACE_CB()
+    beta_out = torch.empty(p, dtype=torch.float64, device=dp.X.device)
+    rep = native.Report()
+    rc = lib.l0_fista_solve(dp.handle, int(instance.k), float(instance.M),
+                            float(instance.lambda2), ctypes.byref(o),
+                            ctypes.byref(nd) if nd is not None else None,
+                            _device.ptr(warm), beta_out.data_ptr(), ctypes.byref(rep), cb, None,
+                            _device.stream_handle())
+    if raised:
+        raise raised[0]
+    if rc == native.NUMERICAL:
+        raise NumericalError(native.last_error(), iteration=int(rep.error_iteration))
+    native.check(rc)
+    beta = beta_out if return_device else beta_out.cpu().numpy()
+    stats = {"gpu_launches": int(rep.gpu_launches), "topk_fallbacks": int(rep.topk_fallbacks),
+             "lipschitz": float(L)}
+    if opts.profile:
+        stats.update(k1_ms=rep.k1_ms, k2_ms=rep.k2_ms, k3_ms=rep.k3_ms, k1_count=rep.k1_count,
+                     k2_count=rep.k2_count, k3_count=rep.k3_count)
+    return RelaxationReport(beta=beta, primal_value=float(rep.primal_value),
+                            dual_bound=float(rep.dual_bound), gap=float(rep.gap),
+                            iterations=int(rep.iterations), restarts=int(rep.restarts),
+                            termination=_TERM[int(rep.termination)],
+                            wall_time=float(rep.wall_time), stats=stats)

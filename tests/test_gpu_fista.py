@@ -1,0 +1,185 @@
+"""Trajectory-level parity of the B200 solve_relaxation.
+
+Every case runs the drop-in API on the GPU and compares with the reference's
+own trajectory (golden fixture, same injected L) and with the CPU oracle:
+
+* objective within 1e-12 relative at every bound check;
+* dual bound within 1e-9 relative (fp64 and fp32-storage modes) at every
+  bound check before the plateau (relative gap >= 1e-6), and at the end;
+* final beta within 1e-9 * max|beta|, identical support {|beta_j| > 1e-9 M};
+* iteration count and termination identical;
+* restart counts reported (post-plateau restarts compare ulp-equal
+  objectives and may flip).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2502_09502_b200 import data as mydata
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(engine, golden, name, dtype="fp64"):
+    data, meta = golden
+    spec = meta["cases"][name]
+    if spec["gen"] == "inline":
+        X, y = data[f"traj/{name}/X"], data[f"traj/{name}/y"]
+    else:
+        cd = mydata.make_config(spec["config"], scale=spec["scale"])
+        X, y = cd.X, cd.y
+        if dtype == "fp64":
+            X = X.astype(np.float64)
+    inst = engine.ProblemInstance(X, y, engine.LossKind(spec["loss"]), spec["k"], spec["M"],
+                                  spec["lambda2"], dtype=dtype)
+    return spec, inst
+
+
+def _solve(engine, spec, inst, L, **extra):
+    opts = dict(spec["opts"])
+    node = None
+    if spec.get("node"):
+        nz = spec["node"]
+        node = engine.NodeState(fixed_one=tuple(nz[1]), fixed_zero=tuple(nz[0]),
+                                parent_bound=nz[2] if len(nz) > 2 else -np.inf)
+    warm = None
+    if spec.get("warm_seed") is not None:
+        warm = np.random.default_rng(spec["warm_seed"]).standard_normal(inst.p) * 0.05
+        warm[list(node.fixed_zero)] = 0.0
+    rec = []
+    o = engine.FistaOptions(lipschitz=L, trace_hook=rec.append, **opts, **extra)
+    rep = engine.solve_relaxation(inst, node=node, warm_start=warm, opts=o)
+    return rep, rec
+
+
+def _compare(rep, rec, trace, scalars, ref_beta, spec, dual_rtol=1e-9):
+    primal, dual, gap, iters, restarts, L = scalars
+    assert rep.termination.value == spec["termination"]
+    assert rep.iterations == int(iters)
+    assert len(rec) == trace.shape[0]
+    for r, ref in zip(rec, trace):
+        assert r["iteration"] == int(ref[0])
+        assert r["primal"] == pytest.approx(ref[1], rel=1e-12, abs=1e-12)
+        if math.isfinite(ref[2]):
+            rel_gap = abs(ref[3]) / max(1.0, abs(ref[1]))
+            if rel_gap >= 1e-6:
+                assert r["dual"] == pytest.approx(ref[2], rel=dual_rtol, abs=1e-9)
+        else:
+            assert not math.isfinite(r["dual"])
+    assert rep.primal_value == pytest.approx(primal, rel=1e-12, abs=1e-12)
+    if math.isfinite(dual):
+        assert rep.dual_bound == pytest.approx(dual, rel=dual_rtol, abs=1e-9)
+    scale = max(1e-300, float(np.max(np.abs(ref_beta))))
+    np.testing.assert_allclose(rep.beta, ref_beta, rtol=0, atol=1e-9 * max(scale, 1.0))
+    M = spec["M"]
+    assert np.array_equal(np.abs(rep.beta) > 1e-9 * M, np.abs(ref_beta) > 1e-9 * M)
+
+
+TRAJ = ["spec_1d", "spec_2x2", "spec_y0", "c1", "c1_default_tol", "c1_literal", "c1_norestart",
+        "c2_small", "c3_small", "c3_small_bci7", "c4_node0", "c4_node1", "c4_node2",
+        "c4_node_warm", "c4_primal_cut", "c4_dual_cut"]
+
+
+@pytest.mark.parametrize("name", TRAJ)
+def test_trajectory_vs_reference(engine, golden, name):
+    data, _ = golden
+    spec, inst = _instance(engine, golden, name)
+    scalars = data[f"traj/{name}/scalars"]
+    rep, rec = _solve(engine, spec, inst, float(scalars[5]))
+    _compare(rep, rec, data[f"traj/{name}/trace"], scalars, data[f"traj/{name}/beta"], spec)
+
+
+@pytest.mark.parametrize("name", ["c3_small", "c4_node0", "c4_node_warm"])
+def test_fp32_storage_mode_matches(engine, golden, name):
+    """fp32 X storage + fp64 arithmetic reproduces the fp64 solve on the
+    fp64-widened matrix (the golden was produced on X32.astype(float64))."""
+    data, meta = golden
+    if meta["cases"][name]["gen"] != "config":
+        pytest.skip("inline case")
+    spec, inst = _instance(engine, golden, name, dtype="fp32")
+    scalars = data[f"traj/{name}/scalars"]
+    rep, rec = _solve(engine, spec, inst, float(scalars[5]))
+    _compare(rep, rec, data[f"traj/{name}/trace"], scalars, data[f"traj/{name}/beta"], spec)
+
+
+def test_spec_known_answers(engine):
+    SE = engine.LossKind.SQUARED_ERROR
+    inst = engine.ProblemInstance(np.array([[1.0]]), np.array([1.0]), SE, 1, 2.0, 1.0)
+    rep = engine.solve_relaxation(inst)
+    assert rep.primal_value == pytest.approx(0.5, abs=1e-6) and rep.gap <= 1e-6
+    inst = engine.ProblemInstance(np.eye(2), np.array([1.0, 1.0]), SE, 2, 10.0, 1.0)
+    rep = engine.solve_relaxation(inst)
+    assert rep.primal_value == pytest.approx(1.0, abs=1e-6)
+    np.testing.assert_allclose(rep.beta, [0.5, 0.5], atol=1e-6)
+    inst = engine.ProblemInstance(np.eye(3), np.zeros(3), SE, 2, 2.0, 1.0)
+    rep = engine.solve_relaxation(inst)
+    assert rep.iterations == 1 and np.all(rep.beta == 0.0) and rep.gap == 0.0
+
+
+def test_lockstep_iterates_vs_oracle(engine, oracle):
+    """beta_t after exactly t iterations equals the oracle's beta_t (pre-plateau)."""
+    cd = mydata.make_config("C1", scale=0.5)
+    L = 2.0 * 1.01 * float(np.linalg.eigvalsh(cd.X.T @ cd.X)[-1])
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+    seen = {}
+
+    def keep(t, beta, obj, restarted):
+        seen[t] = (beta.copy(), obj, restarted)
+
+    oracle.fista(cd.X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=40, gap_tol=1e-300,
+                 on_iteration=keep)
+    for t in (1, 2, 3, 7, 15, 40):
+        rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
+            lipschitz=L, max_iterations=t, gap_tolerance=1e-300))
+        ref_beta, ref_obj, _ = seen[t]
+        assert rep.iterations == t
+        assert rep.primal_value == pytest.approx(ref_obj, rel=1e-12)
+        np.testing.assert_allclose(rep.beta, ref_beta, rtol=0, atol=1e-10 * np.max(np.abs(ref_beta)))
+
+
+def test_numerical_error_on_bad_step(engine, oracle):
+    cd = mydata.make_config("C1", scale=0.25)
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+    L_bad = 1e-6
+    with pytest.raises(oracle.PowerIterationError) as ref_err:
+        oracle.fista(cd.X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L_bad, max_iter=2000)
+    with pytest.raises(engine.NumericalError) as err:
+        engine.solve_relaxation(inst, opts=engine.FistaOptions(lipschitz=L_bad, max_iterations=2000))
+    assert err.value.iteration == ref_err.value.iteration
+
+
+def test_time_limit_and_hook_exception(engine):
+    cd = mydata.make_config("C1", scale=0.5)
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+    rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
+        lipschitz=1e4, max_iterations=10**6, gap_tolerance=1e-300, time_limit=0.05))
+    assert rep.termination is engine.Termination.TIME_LIMIT
+    assert rep.iterations > 0 and math.isfinite(rep.dual_bound)
+
+    class Stop(Exception):
+        pass
+
+    def hook(r):
+        if r["iteration"] >= 20:
+            raise Stop()
+
+    with pytest.raises(Stop):
+        engine.solve_relaxation(inst, opts=engine.FistaOptions(lipschitz=1e4, trace_hook=hook,
+                                                                gap_tolerance=1e-300))
+
+
+def test_solver_validation_errors(engine):
+    SE = engine.LossKind.SQUARED_ERROR
+    inst = engine.ProblemInstance(np.eye(3), np.ones(3), SE, 2, 2.0, 1.0)
+    with pytest.raises(engine.InvalidInputError):
+        engine.solve_relaxation(inst, warm_start=np.zeros(2), opts=engine.FistaOptions(lipschitz=2.0))
+    with pytest.raises(engine.InfeasibleNodeError):
+        engine.solve_relaxation(inst, node=engine.NodeState(fixed_one=(0, 1, 2)),
+                                opts=engine.FistaOptions(lipschitz=2.0))
+    with pytest.raises(engine.InvalidInputError):
+        engine.FistaOptions(gap_tolerance=0.0)
+    pois = engine.ProblemInstance(np.eye(2), np.ones(2), engine.LossKind.POISSON, 1, 1.0, 1.0)
+    with pytest.raises(engine.UnsupportedOperationError):
+        engine.solve_relaxation(pois)
