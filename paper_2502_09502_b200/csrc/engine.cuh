@@ -61,6 +61,7 @@ struct EngineArgs {
   const Params* prm;
   int multi;         // row-sharded: global epilogues run as separate kernels
   int plain_rhs2;    // PLAIN K2: number of RHS columns
+  int prox_full_sort; // 1: K3 sorts all p keys (reference check path); 0: windowed sort
   // PLAIN-mode vectors
   const double* in_vec;
   double* out_vec;

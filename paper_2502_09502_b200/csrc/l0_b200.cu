@@ -2,6 +2,7 @@
 // visible to every kernel without relocatable device code.
 #include "gemv.cu"
 #include "prox.cu"
+#include "prox_window.cu"
 #include "ops.cu"
 #include "engine_host.cu"
 #include "abi_ops.cu"

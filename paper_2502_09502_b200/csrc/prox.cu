@@ -552,8 +552,11 @@ size_t prox_sort_tmp_bytes(int64_t p) {
   return bytes;
 }
 
+cudaError_t launch_prox_window(const EngineArgs& a, cudaStream_t s);
+
 cudaError_t launch_prox_iter(const EngineArgs& a, void* sort_tmp, size_t sort_tmp_bytes,
                              cudaStream_t s) {
+  if (a.prox_full_sort == 0) return launch_prox_window(a, s);
   if (a.p <= 1024) return launch_block<256, 4>(a, s);
   if (a.p <= 4096) return launch_block<512, 8>(a, s);
   if (a.p <= 16384) return launch_block<1024, 16>(a, s);

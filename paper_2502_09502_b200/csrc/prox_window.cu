@@ -1,0 +1,512 @@
+// K3 (FISTA loop variant): prox via a windowed top-of-order sort.
+//
+// The exact prox needs the stable descending order of |mu| only as far as the
+// merged PAVA pool can reach: every free coordinate behind the pool end c* is
+// a tail singleton whose output is mu itself (prox.py:104-116 with nu = x), and
+// the pool never reaches a zero key.  So instead of sorting all p keys
+// (SURVEY.md §7.1-4), K3 repeatedly
+//   1. selects the next window W = {lb <= bits(|mu|) < ub} of at most kWinCap
+//      keys by an MSD radix histogram (12+13+13+13+13 bits, usually one pass),
+//   2. compacts W in ascending index order and block-sorts it (CUB, stable),
+//      appending it to the sorted prefix (keys in later windows are strictly
+//      smaller, so the concatenation IS the stable descending order),
+//   3. runs the closed-form single-pool PAVA search on the prefix, with the
+//      largest unsorted key as the right boundary,
+// until the pool closes inside the prefix.  On C2 one window of <= 4096 keys
+// suffices from the second iteration on (pool end 6165 -> 755).
+//
+// The scatter then writes beta+ for every coordinate, and g(beta+) is taken
+// from the prefix (verified against the largest |beta+| outside the window,
+// radix-select fallback).  Same arithmetic as prox_post_sort (prox.cu).
+
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "control.cuh"
+#include "engine.cuh"
+#include "prox.cuh"
+
+namespace l0 {
+
+constexpr int kWinThreads = 1024;
+constexpr int kWinIpt = 4;
+constexpr int kWinCap = kWinThreads * kWinIpt;  // 4096 keys per window
+constexpr int kHistBins = 8192;                 // 13-bit digits
+
+struct WinSmem {
+  union {
+    typename cub::BlockRadixSort<double, kWinThreads, kWinIpt, int, 6>::TempStorage sort;
+    unsigned hist[kHistBins];
+    typename cub::BlockScan<double, kWinThreads>::TempStorage dscan;
+    typename cub::BlockScan<int, kWinThreads>::TempStorage iscan;
+  } u;
+  double wkey[kWinCap];
+  int widx[kWinCap];
+  // window selection results
+  unsigned long long sel_lb;
+  int sel_count;
+  int sel_state;  // 0 searching, 1 done, 2 overflow
+  unsigned long long sel_prefix;
+  int sel_above;
+  // PAVA search results
+  int res;        // 0 undecided, 1 pool found, 2 no pool, 3 extend
+  int64_t astar, cstar;
+  double vstar;
+  int wflag[32];
+  int64_t wc[32];
+  double wv[32];
+  double red[32];
+  double xnext;
+  int has_next;
+};
+
+__device__ __forceinline__ unsigned long long key_bits(double k) {
+  return (unsigned long long)__double_as_longlong(k);
+}
+
+// MSD radix selection of the next window among positive keys with bits < ub.
+// Returns in sm.sel_lb / sm.sel_count (count <= cap) or sel_state = 2 on an
+// exact tie group larger than cap.
+__device__ void select_window(const double* key, int64_t p, unsigned long long ub, int cap,
+                              WinSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    sm.sel_state = 0;
+    sm.sel_prefix = 0ull;
+    sm.sel_above = 0;
+  }
+  __syncthreads();
+  int shift = 64;
+  for (int level = 0; level < 5; ++level) {
+    const int w = level == 0 ? 12 : 13;   // 12 + 4 x 13 = 64 bits
+    const int hi_shift = shift;  // bits >= hi_shift must equal the prefix
+    shift -= w;
+    const unsigned long long prefix = sm.sel_prefix;
+    const unsigned mask = (1u << w) - 1u;
+    for (int i = tid; i < kHistBins; i += kWinThreads) sm.u.hist[i] = 0u;
+    __syncthreads();
+    for (int64_t j0 = 0; j0 < p; j0 += kWinThreads) {
+      const int64_t j = j0 + tid;
+      int digit = -1;
+      if (j < p) {
+        const double k = key[j];
+        if (k > 0.0) {
+          const unsigned long long b = key_bits(k);
+          const bool in_prefix = hi_shift >= 64 || (b >> hi_shift) == (prefix >> hi_shift);
+          if (b < ub && in_prefix) digit = (int)((b >> shift) & mask);
+        }
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sm.u.hist[digit], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    // bins in descending order: thread t owns bins kHistBins-1-8t .. kHistBins-8-8t
+    unsigned c8[8];
+    int s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int d = kHistBins - 1 - (tid * 8 + q);
+      c8[q] = (d >= 0 && d <= (int)mask) ? sm.u.hist[d] : 0u;
+      s += (int)c8[q];
+    }
+    __syncthreads();
+    int excl = 0, total = 0;
+    cub::BlockScan<int, kWinThreads>(sm.u.iscan).ExclusiveSum(s, excl, total);
+    const int above = sm.sel_above;
+    if (tid == 0 && above + total <= cap) {
+      // everything that remains fits
+      sm.sel_lb = prefix;
+      sm.sel_count = above + total;
+      sm.sel_state = 1;
+    }
+    if (above + total > cap && above + excl <= cap && above + excl + s > cap) {
+      int cum = above + excl;
+      for (int q = 0; q < 8; ++q) {
+        const int d = kHistBins - 1 - (tid * 8 + q);
+        if (cum + (int)c8[q] > cap) {
+          // bin d crosses the capacity: stop above it, or refine into it
+          const bool enough = cum >= cap / 2 || cum > 0 && level == 4;
+          if (enough || level == 4) {
+            if (cum > 0) {
+              sm.sel_lb = prefix | ((unsigned long long)(d + 1) << shift);
+              sm.sel_count = cum;
+              sm.sel_state = 1;
+            } else {
+              sm.sel_state = 2;  // exact tie group larger than the window
+            }
+          } else {
+            sm.sel_prefix = prefix | ((unsigned long long)d << shift);
+            sm.sel_above = cum;
+          }
+          break;
+        }
+        cum += (int)c8[q];
+      }
+    }
+    __syncthreads();
+    if (sm.sel_state != 0) return;
+  }
+}
+
+// Compact the window {lb <= bits < ub, key > 0} in ascending index order into
+// sm.wkey/widx; also the largest positive key below the window (sm.xnext).
+__device__ void compact_window(const double* key, int64_t p, unsigned long long lb,
+                               unsigned long long ub, WinSmem& sm) {
+  const int tid = threadIdx.x;
+  const int64_t per = (p + kWinThreads - 1) / kWinThreads;
+  const int64_t j0 = min(p, (int64_t)tid * per), j1 = min(p, j0 + per);
+  int cnt = 0;
+  double below = 0.0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const double k = key[j];
+    if (k > 0.0) {
+      const unsigned long long b = key_bits(k);
+      if (b >= lb && b < ub) ++cnt;
+      else if (b < lb) below = fmax(below, k);
+    }
+  }
+  int off = 0;
+  cub::BlockScan<int, kWinThreads>(sm.u.iscan).ExclusiveSum(cnt, off);
+  for (int64_t j = j0; j < j1; ++j) {
+    const double k = key[j];
+    if (k > 0.0) {
+      const unsigned long long b = key_bits(k);
+      if (b >= lb && b < ub) {
+        sm.wkey[off] = k;
+        sm.widx[off] = (int)j;
+        ++off;
+      }
+    }
+  }
+  below = block_max(below, sm.red);
+  if (tid == 0) sm.xnext = below;
+  __syncthreads();
+}
+
+// Closed-form pool search on the sorted prefix xs[0..len) (len > kk) with the
+// boundary element x_len = xnext (has_next) or none (len == all positives and
+// no zero keys follow).  Sets sm.res: 1 pool, 2 no pool, 3 prefix too short.
+__device__ void window_search(const double* xs, const double* tail, int64_t len, int64_t kk,
+                              double rho, double M, bool has_next, double xnext, WinSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) sm.res = 0;
+  __syncthreads();
+  // first merge at k-1 | k (prox.py:80)
+  const double xk = (kk < len) ? xs[kk] : xnext;
+  if (!(xk > hprox(xs[kk - 1], rho, M))) {
+    if (tid == 0) sm.res = 2;
+    __syncthreads();
+    return;
+  }
+  if (kk >= len) {  // the pool starts at an unsorted key
+    if (tid == 0) sm.res = 3;
+    __syncthreads();
+    return;
+  }
+  for (int64_t base = kk - 1; base >= 0; base -= nw) {
+    const int64_t aa = base - warp;
+    int flag = 0;  // 1 valid, 2 beyond the prefix
+    int64_t cA = 0;
+    double VA = 0.0;
+    if (aa >= 0) {
+      double hs = 0.0;
+      for (int64_t j = aa + lane; j < kk; j += 32) hs += xs[j];
+      hs = warp_sum(hs);
+      const double Pw = dmul(rho, (double)(kk - aa));
+      auto pred = [&](int64_t c) -> int {  // 1 true, 0 false; c in [kk, len-1]
+        const double V = hprox(ddiv(dadd(hs, tail[c]), (double)(c - aa + 1)),
+                               ddiv(Pw, (double)(c - aa + 1)), M);
+        const double xn = (c + 1 < len) ? xs[c + 1] : (has_next ? xnext : -1.0);
+        return xn <= V ? 1 : 0;
+      };
+      int64_t lo = kk, hi = len - 1;
+      // pred(len-1) decides whether the pool closes inside the prefix
+      const int plast = __shfl_sync(0xffffffffu, lane == 0 ? pred(hi) : 0, 0);
+      if (!plast) {
+        flag = 2;
+      } else {
+        while (lo < hi) {
+          const int64_t span = hi - lo;
+          const int64_t c = lo + (span * lane) / 32;
+          const bool pr = pred(c);
+          const unsigned b = __ballot_sync(0xffffffffu, pr);
+          if (b == 0u) {
+            lo = lo + (span * 31) / 32 + 1;
+          } else {
+            const int f = __ffs(b) - 1;
+            if (f == 0) {
+              hi = lo;
+            } else {
+              const int64_t cprev = lo + (span * (f - 1)) / 32;
+              hi = lo + (span * f) / 32;
+              lo = cprev + 1;
+            }
+          }
+        }
+        cA = lo;
+        VA = hprox(ddiv(dadd(hs, tail[cA]), (double)(cA - aa + 1)),
+                   ddiv(Pw, (double)(cA - aa + 1)), M);
+        flag = (aa == 0 || hprox(xs[aa - 1], rho, M) >= VA) ? 1 : 0;
+      }
+    }
+    if (lane == 0) {
+      sm.wflag[warp] = flag;
+      sm.wc[warp] = cA;
+      sm.wv[warp] = VA;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < nw && base - w >= 0; ++w) {
+        if (sm.wflag[w] == 2) { sm.res = 3; break; }
+        if (sm.wflag[w] == 1) {
+          sm.res = 1;
+          sm.astar = base - w;
+          sm.cstar = sm.wc[w];
+          sm.vstar = sm.wv[w];
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    if (sm.res != 0) return;
+  }
+}
+
+__global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
+  WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
+  using Sort = cub::BlockRadixSort<double, kWinThreads, kWinIpt, int, 6>;
+  const State* st0 = a.st;
+  if (st0->done) return;
+  if (st0->dual_pending) {
+    if (dual_step(a, ps)) return;
+  }
+  if (a.st->dual_only) return;
+  const Params* P = a.prm;
+  State* st = a.st;
+  const int tid = threadIdx.x;
+  const int64_t p = a.p;
+  const bool node = P->node_mode != 0;
+  const int64_t nf = node ? P->n_free : p;
+  const int64_t kk = node ? P->k_rem : P->k;
+  const int64_t kg = node ? P->k_g : P->k;
+  const double rho = P->rho, M = P->M;
+  const int how = (kk <= 0 || nf == 0) ? 0 : (kk >= nf ? 1 : 2);
+  double* out = a.beta + ring(st->t + 1) * a.pv;
+
+  // ---- sorted prefix, window by window -------------------------------------
+  int64_t len = 0;                      // sorted prefix length
+  unsigned long long ub = ~0ull;        // keys of the next window are below ub
+  double carry = 0.0;                   // running tail prefix sum
+  bool more = true;                     // positive keys remain unsorted
+  if (tid == 0) sm.res = (how == 2) ? 0 : 2;
+  __syncthreads();
+  while (how == 2 && more) {
+    select_window(a.key, p, ub, kWinCap, sm);
+    if (sm.sel_state == 2) {
+      if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
+      return;
+    }
+    const unsigned long long lb = sm.sel_lb;
+    const int cnt = sm.sel_count;
+    compact_window(a.key, p, lb, ub, sm);
+    double keys[kWinIpt];
+    int ids[kWinIpt];
+#pragma unroll
+    for (int i = 0; i < kWinIpt; ++i) {
+      const int s = tid * kWinIpt + i;
+      keys[i] = s < cnt ? sm.wkey[s] : -CUDART_INF;
+      ids[i] = s < cnt ? sm.widx[s] : 0;
+    }
+    __syncthreads();
+    Sort(sm.u.sort).SortDescending(keys, ids);  // stable: ids ascending on ties
+    __syncthreads();
+    double loc = 0.0;
+#pragma unroll
+    for (int i = 0; i < kWinIpt; ++i) {
+      const int64_t pos = len + tid * kWinIpt + i;
+      if (tid * kWinIpt + i < cnt && pos >= kk) loc += keys[i];
+    }
+    double excl = 0.0;
+    cub::BlockScan<double, kWinThreads>(sm.u.dscan).ExclusiveSum(loc, excl);
+    double run = carry + excl;
+#pragma unroll
+    for (int i = 0; i < kWinIpt; ++i) {
+      const int s = tid * kWinIpt + i;
+      if (s < cnt) {
+        const int64_t pos = len + s;
+        a.xs[pos] = keys[i];
+        a.perm[pos] = ids[i];
+        if (pos >= kk) {
+          run += keys[i];
+          a.tail[pos] = run;
+        }
+        if (s == cnt - 1) sm.red[0] = run;  // running tail sum at the window's end
+      }
+    }
+    __threadfence_block();
+    __syncthreads();
+    const double wend = sm.red[0];
+    __syncthreads();
+    carry = wend;
+    len += cnt;
+    ub = lb;
+    const double xn = sm.xnext;
+    more = xn > 0.0;
+    // zero keys (never in a pool) follow the positives
+    const bool has_next = more || (len < nf);
+    if (len > kk || !more) {
+      window_search(a.xs, a.tail, len, kk, rho, M, has_next, more ? xn : 0.0, sm);
+      if (sm.res == 1 || sm.res == 2) break;
+      if (!more) {  // pool would extend into zero keys: cannot happen (x=0 <= V)
+        if (tid == 0) sm.res = 2;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+  const int64_t astar = (how == 2 && sm.res == 1) ? sm.astar : INT64_MAX;
+  const int64_t cstar = (how == 2 && sm.res == 1) ? sm.cstar : -1;
+  const double vstar = sm.vstar;
+
+  // ---- scatter ----------------------------------------------------------------
+  // prefix positions carry their sorted rank; every other free coordinate is
+  // a tail singleton (or elementwise / pass-through for how = 1 / 0)
+  const unsigned long long lb_last = ub;
+  const int64_t kkg = kg < nf ? kg : nf;
+  const int64_t W = min(len, kkg + 64);
+  double total = 0.0, amax = 0.0, rest = 0.0;
+  for (int64_t j = tid; j < p; j += kWinThreads) {
+    const int cls = node ? a.mask[j] : FREE;
+    const double gin = a.gam[j];
+    const double mu = dmul(rho, gin);
+    double res;
+    bool in_prefix = false;
+    if (cls == FIXED_ZERO) {
+      res = 0.0;  // fista.py:126-127
+    } else if (cls == FIXED_ONE) {
+      res = dsub(gin, ddiv(dmul(dsign(mu), hprox(fabs(mu), rho, M)), rho));
+    } else if (how == 0) {
+      res = dsub(gin, ddiv(mu, rho));
+    } else if (how == 1) {
+      res = dsub(gin, ddiv(dmul(dsign(mu), hprox(fabs(mu), rho, M)), rho));
+    } else {
+      const double k = a.key[j];
+      in_prefix = k > 0.0 && key_bits(k) >= lb_last;
+      res = dsub(gin, ddiv(mu, rho));  // tail singleton: out = mu
+    }
+    if (!in_prefix) {
+      out[j] = res;
+      if (cls == FREE) {
+        const double ab = fabs(res);
+        total += ab;
+        amax = fmax(amax, ab);
+        rest = fmax(rest, ab);
+        a.scratch[j] = ab;
+      } else {
+        a.scratch[j] = -1.0;
+      }
+    }
+  }
+  if (how == 2) {
+    for (int64_t pos = tid; pos < len; pos += kWinThreads) {
+      const int j = a.perm[pos];
+      const double x = a.xs[pos];
+      const double gin = a.gam[j];
+      const double mu = dmul(rho, gin);
+      double nu;
+      if (pos < astar) nu = (pos < kk) ? hprox(x, rho, M) : x;
+      else if (pos <= cstar) nu = vstar;
+      else nu = (pos < kk) ? hprox(x, rho, M) : x;
+      const double res = dsub(gin, ddiv(dmul(nu, dsign(mu)), rho));
+      out[j] = res;
+      const double ab = fabs(res);
+      total += ab;
+      amax = fmax(amax, ab);
+      if (pos < W) ps.cand[pos] = ab;
+      else rest = fmax(rest, ab);
+      a.scratch[j] = ab;
+    }
+  }
+  __syncthreads();
+  total = block_sum(total, ps.red);
+  amax = block_max(amax, ps.red);
+  rest = block_max(rest, ps.red);
+
+  // ---- g(beta+) (perspective.py:76-132) ----------------------------------------
+  double fone_val = 0.0;
+  bool fone_bad = false;
+  if (tid == 0 && node) {
+    double s2 = 0.0;
+    for (int64_t i = 0; i < P->n_fone; ++i) {
+      const double b = out[a.fone[i]];
+      if (fabs(b) > dmul(M, dadd(1.0, kFeasRtol))) fone_bad = true;
+      s2 = fma(b, b, s2);
+    }
+    fone_val = dmul(0.5, s2);
+  }
+  double gfree = 0.0;
+  int path = 0;
+  if (nf == 0) path = 2;
+  else if (amax > dmul(M, dadd(1.0, kFeasRtol))) { gfree = CUDART_INF; path = 2; }
+  else if (total > dmul(dmul((double)kg, M), dadd(1.0, kFeasRtol))) { gfree = CUDART_INF; path = 2; }
+  else if (kg == 0) path = 2;
+  if (path == 0) {
+    // window of the first W sorted positions; any free coordinate outside it
+    // must not exceed the kkg-th largest inside (else radix-select fallback)
+    if (how == 2 && W >= kkg && W <= kCandCap) {
+      block_rank_sort_desc(ps.cand, ps.cand2, (int)W);
+      if (rest > ps.cand2[kkg - 1]) path = 1;
+    } else {
+      path = 1;
+    }
+    if (path == 1 && kkg > kCandCap) {
+      if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
+      return;
+    }
+    if (path == 1) {
+      __syncthreads();
+      double tau;
+      int64_t cgt;
+      block_kth_largest(a.scratch, p, kkg, ps.sel, &tau, &cgt);
+      if (tid == 0) ps.ncand = 0;
+      __syncthreads();
+      for (int64_t j = tid; j < p; j += kWinThreads) {
+        const double x = a.scratch[j];
+        if (x > tau) ps.cand[atomicAdd(&ps.ncand, 1)] = x;
+      }
+      __syncthreads();
+      for (int64_t i = cgt + tid; i < kkg; i += kWinThreads) ps.cand[i] = tau;
+      __syncthreads();
+      block_rank_sort_desc(ps.cand, ps.cand2, (int)kkg);
+      if (tid == 0) st->topk_fallbacks += 1;
+    }
+    if (tid < 32) {
+      const double g = envelope_from_top(ps.cand2, kkg, total);
+      if (tid == 0) ps.gfree = g;
+    }
+    __syncthreads();
+    gfree = ps.gfree;
+  }
+  if (tid == 0) {
+    double g = gfree;
+    if (node) g = fone_bad ? CUDART_INF : dadd(dadd(0.0, fone_val), gfree);
+    st->g_next = g;
+  }
+}
+
+size_t prox_window_smem() {
+  return ((sizeof(ProxSmem) + 255) & ~size_t(255)) + sizeof(WinSmem);
+}
+
+cudaError_t launch_prox_window(const EngineArgs& a, cudaStream_t s) {
+  const size_t smem = prox_window_smem();
+  cudaError_t e = cudaFuncSetAttribute(k3_prox_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k3_prox_window<<<1, kWinThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace l0

@@ -231,3 +231,35 @@ def test_solver_validation_errors(engine):
     pois = engine.ProblemInstance(np.eye(2), np.ones(2), engine.LossKind.POISSON, 1, 1.0, 1.0)
     with pytest.raises(engine.UnsupportedOperationError):
         engine.solve_relaxation(pois)
+
+
+@pytest.mark.parametrize("n,p,sigma,k", [(800, 12000, 0.7, 20), (500, 20000, 0.5, 15),
+                                         (300, 40000, 0.7, 30)])
+def test_wide_problems_vs_oracle(engine, oracle, n, p, sigma, k):
+    """Wide X: the windowed prox sorts several windows at t=1 (pool end ~0.4 p)
+    and must reproduce the oracle's full-sort trajectory."""
+    X, y, _ = mydata.synthetic(n, p, k, sigma=sigma, snr=5.0, seed=7)
+    s = np.linalg.svd(X, compute_uv=False)[0]
+    L = 2.0 * 1.01 * s * s
+    inst = engine.ProblemInstance(X, y, engine.LossKind.SQUARED_ERROR, k, 2.0, 0.1)
+    pools = []
+    orig = oracle.prox_conj
+
+    def spy(mu, rho, kk, M, instrument=False):
+        r, order, pool = orig(mu, rho, kk, M, instrument=True)
+        pools.append(pool)
+        return r
+
+    oracle.prox_conj = spy
+    try:
+        ref = oracle.fista(X, y, "squared_error", k, 2.0, 0.1, L=L, max_iter=25, gap_tol=1e-300)
+    finally:
+        oracle.prox_conj = orig
+    assert pools[0] is not None
+    rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(lipschitz=L, max_iterations=25,
+                                                                 gap_tolerance=1e-300))
+    assert rep.iterations == 25
+    assert rep.primal_value == pytest.approx(ref["primal_value"], rel=1e-12)
+    assert rep.dual_bound == pytest.approx(ref["dual_bound"], rel=1e-9)
+    np.testing.assert_allclose(rep.beta, ref["beta"], rtol=0, atol=1e-10 * np.max(np.abs(ref["beta"])))
+    assert rep.stats["topk_fallbacks"] >= 0
