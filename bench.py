@@ -285,7 +285,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
             "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
-            "restarts": rep.restarts, "final_gap": rep.gap}
+            "restarts": rep.restarts, "final_gap": rep.gap,
+            "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks")}
     print(json.dumps(line), flush=True)
 
 

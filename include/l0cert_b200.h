@@ -102,6 +102,7 @@ typedef struct l0_report {
   int64_t topk_fallbacks;       /* envelope top-k window misses (diagnostic) */
   double k1_ms, k2_ms, k3_ms;   /* profile: summed kernel time (CUDA events) */
   int64_t k1_count, k2_count, k3_count;
+  int64_t prox_full_passes;     /* iterations whose prox window needed full key passes */
 } l0_report;
 
 typedef struct l0_trace_record {

@@ -217,6 +217,8 @@ struct State {
   double gap;
   double last_dual;
   double loss_cur;
+  double theta;           // window-candidate threshold K2 applies (set by K3)
+  int64_t slow_prox;      // diagnostics: K3 iterations that needed a full key pass
   TraceRec trace[kTraceCap];
 };
 

@@ -18,6 +18,7 @@ constexpr int kK2Slab = 256;
 constexpr int kK2StageRows = 256;                       // rows of r staged per pass
 constexpr int kPvAlign = 2048;                          // p-vector stride alignment
 constexpr int kTargetCtas = 148 * 4;
+constexpr int kHTop = 32;   // per-slab Huber top list (bound checks with k <= 32)
 
 enum KMode : int {
   MODE_ITER = 0,    // FISTA iteration (ring buffers, fused epilogues)
@@ -56,6 +57,16 @@ struct EngineArgs {
   double* scratch;   // [pv] scratch (Huber values, |beta|)
   const uint8_t* mask;  // node classes, nullable
   const int* fone;      // fixed-one ids (sorted), Params::n_fone of them
+  // per-slab epilogue products (K2 -> K3), slabs of kK2Slab columns
+  double* hval;      // Huber values of the bound check (free coords, -1 otherwise) [pv]
+  double* cand_key;  // window candidates per slab [k2_slabs][kK2Slab]
+  int* cand_idx;
+  int* slab_cnt;     // candidates per slab
+  double* slab_sum;  // sum |beta+| of non-candidate free coordinates per slab
+  double* slab_max;  // max |beta+| of non-candidate free coordinates per slab
+  double* slab_below;// largest positive free key below the candidate threshold per slab
+  double* slab_hfone;// sum of fixed-one Huber values per slab
+  double* slab_htop; // top-kHTop free Huber values per slab [k2_slabs][kHTop]
   // control
   State* st;
   const Params* prm;

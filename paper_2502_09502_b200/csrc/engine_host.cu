@@ -166,6 +166,16 @@ static uint64_t carve(Problem& P, char* base) {
   a.cnt = (unsigned*)take(4ull * counter_words(a.k2_slabs, a.k1_chunks));
   a.perm = (int*)take(4ull * pv);
   a.iota = (int*)take(4ull * pv);
+  a.hval = (double*)take(8ull * pv);
+  a.cand_key = (double*)take(8ull * pv);
+  a.cand_idx = (int*)take(4ull * pv);
+  const int64_t S = a.k2_slabs;
+  a.slab_cnt = (int*)take(4ull * S);
+  a.slab_sum = (double*)take(8ull * S);
+  a.slab_max = (double*)take(8ull * S);
+  a.slab_below = (double*)take(8ull * S);
+  a.slab_hfone = (double*)take(8ull * S);
+  a.slab_htop = (double*)take(8ull * S * kHTop);
   P.d_mask = (uint8_t*)take(pv);
   P.d_fone = (int*)take(4ull * pv);
   P.sort_tmp = take(P.sort_tmp_bytes);
@@ -616,6 +626,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   rep->status = h->err;
   rep->error_iteration = h->err_iter;
   rep->topk_fallbacks = h->topk_fallbacks;
+  rep->prox_full_passes = h->slow_prox;
   L0_CUDA_TRY(cudaMemcpyAsync(d_beta_out, a.beta + ((h->t % 3)) * a.pv, vb,
                               cudaMemcpyDeviceToDevice, s));
   L0_CUDA_TRY(cudaEventRecord(P->ev_out, s));

@@ -16,6 +16,7 @@
 
 #include "control.cuh"
 #include "engine.cuh"
+#include "slab_epilogue.cuh"
 
 namespace l0 {
 
@@ -35,23 +36,6 @@ template <> struct Vec16<float> {
 
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
-
-// ---------------------------------------------------------------------------
-// gradient step + sort keys for one coordinate (fista.py:161-163, :102, :107,
-// :119; prox.py:106-111).  Every rounding matches the numpy expression.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void grad_step(const EngineArgs& a, int64_t j, double g, int64_t t,
-                                          double c) {
-  const Params* P = a.prm;
-  double b1 = a.beta[ring(t - 1) * a.pv + j];
-  double b2 = a.beta[ring(t - 2) * a.pv + j];
-  double gamma = dadd(b1, dmul(c, dsub(b1, b2)));
-  gamma = dsub(gamma, ddiv(g, P->L));
-  a.gam[j] = gamma;
-  double mu = dmul(P->rho, gamma);
-  bool fixed = P->node_mode && a.mask[j] != FREE;
-  a.key[j] = fixed ? -1.0 : fabs(mu);
-}
 
 // ===========================================================================
 // K1: forward pass u = X beta.  Persistent CTAs pull (chunk, slab) items from
@@ -307,6 +291,7 @@ struct K2Smem {
   double sr[2][kK2StageRows];
   double sacc[8][2][kK2Slab];  // per-warp column sums (fixed-order combine)
   double red[32];
+  EpiSmem epi;
   unsigned item;
   int last;
 };
@@ -414,25 +399,22 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
     __threadfence();
     {
       const int64_t col = col0 + tid;
+      double g = 0.0, v = 0.0;
       if (col < a.p) {
         if (WG) {
-          double g = 0.0;
           for (int ch = 0; ch < a.k2_chunks; ++ch) g += __ldcg(a.k2_part + (int64_t)ch * a.pv + col);
-          if (mode == MODE_PLAIN) {
-            a.out_vec[col] = g;
-          } else {
-            a.gv[col] = g;
-            if (!a.multi) grad_step(a, col, g, t, c);
-          }
+          if (mode == MODE_PLAIN) a.out_vec[col] = g;
+          else a.gv[col] = g;
         }
         if (WZ) {
-          double v = 0.0;
           for (int ch = 0; ch < a.k2_chunks; ++ch)
             v += __ldcg(a.k2_part + ((int64_t)a.k2_chunks + ch) * a.pv + col);
           if (mode == MODE_PLAIN) a.out_vec2[col] = v;
           else a.gv[a.pv + col] = v;
         }
       }
+      // single GPU: the prox's elementwise work for these 256 columns
+      if (mode == MODE_ITER && !a.multi) slab_epilogue(a, slab, t, c, WG, WZ, g, v, sm.epi);
     }
     if (tid == 0) cnt_k2_slab(a)[slab] = 0u;
     if (!(WZ && mode == MODE_ITER)) continue;
@@ -493,15 +475,19 @@ __global__ void __launch_bounds__(kK2Threads) k2_transpose(EngineArgs a, int mod
   else if (wz) k2_body<TX, false, true>(a, mode, t, c, sm);
 }
 
-// gradient step as its own pass (row-sharded mode: after the all-reduce of g)
-__global__ void k_grad_step(EngineArgs a) {
+// gradient step + slab epilogue as its own pass (row-sharded mode: after the
+// all-reduce of [g | v]); one CTA per slab of 256 columns
+__global__ void __launch_bounds__(kK2Slab) k_grad_step(EngineArgs a) {
+  __shared__ EpiSmem sm;
   const State* st = a.st;
   if (st->done || st->dual_only) return;
   const int64_t t = st->t + 1;
   const double c = momentum(st->phi);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.p;
-       j += (int64_t)gridDim.x * blockDim.x)
-    grad_step(a, j, a.gv[j], t, c);
+  const bool wz = st->dual_pending != 0;
+  const int64_t j = (int64_t)blockIdx.x * kK2Slab + threadIdx.x;
+  const double g = j < a.p ? a.gv[j] : 0.0;
+  const double v = (wz && j < a.p) ? a.gv[a.pv + j] : 0.0;
+  slab_epilogue(a, blockIdx.x, t, c, true, wz, g, v, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -534,9 +520,7 @@ int k2_blocks_per_sm(int dtype) {
 }
 
 cudaError_t launch_grad_step(const EngineArgs& a, cudaStream_t s) {
-  int64_t nb = (a.p + 255) / 256;
-  int blocks = (int)(nb < 148 * 4 ? nb : 148 * 4);
-  k_grad_step<<<blocks, 256, 0, s>>>(a);
+  k_grad_step<<<a.k2_slabs, kK2Slab, 0, s>>>(a);
   return cudaGetLastError();
 }
 

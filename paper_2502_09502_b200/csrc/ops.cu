@@ -246,6 +246,8 @@ __global__ void k_state_init(State* st, double parent_bound) {
   st->gap = CUDART_NAN;
   st->last_dual = CUDART_NAN;
   st->loss_cur = 0.0;
+  st->theta = 0.0;
+  st->slow_prox = 0;
 }
 
 // host-requested stop (time limit, trace-hook abort): fista.py:204-206

@@ -19,6 +19,8 @@
 // from the prefix (verified against the largest |beta+| outside the window,
 // radix-select fallback).  Same arithmetic as prox_post_sort (prox.cu).
 
+#include <climits>
+
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -35,13 +37,13 @@ constexpr int kHistBins = 8192;                 // 13-bit digits
 
 struct WinSmem {
   union {
-    typename cub::BlockRadixSort<double, kWinThreads, kWinIpt, int, 6>::TempStorage sort;
     unsigned hist[kHistBins];
     typename cub::BlockScan<double, kWinThreads>::TempStorage dscan;
     typename cub::BlockScan<int, kWinThreads>::TempStorage iscan;
   } u;
   double wkey[kWinCap];
   int widx[kWinCap];
+  double wtail[kWinCap];
   // window selection results
   unsigned long long sel_lb;
   int sel_count;
@@ -272,15 +274,148 @@ __device__ void window_search(const double* xs, const double* tail, int64_t len,
   }
 }
 
+// Bitonic sort in shared memory: n (power of two) pairs, descending by key,
+// ties by ascending index -- a total order, so the result equals the
+// reference's stable descending argsort (prox.py:111).  O(log^2 n) barriers,
+// no atomics; for the few thousand window keys it beats a 64-bit radix sort.
+__device__ void bitonic_desc(double* key, int* idx, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (j - 1));
+        const int l = i + j;
+        const double ki = key[i], kl = key[l];
+        const int ii = idx[i], il = idx[l];
+        const bool ordered = (ki > kl) || (ki == kl && ii < il);
+        const bool want = (i & k) == 0;  // this block sorts toward the final order
+        if (want != ordered) {
+          key[i] = kl; key[l] = ki;
+          idx[i] = il; idx[l] = ii;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int pow2_at_least(int c) {
+  int n = 1;
+  while (n < c) n <<= 1;
+  return n;
+}
+
+// Sort the window held in sm.wkey/widx[0..cnt) and append it to the sorted
+// prefix at position len (global xs/perm/tail; the window also stays sorted
+// in shared memory with its tail sums in sm.wtail); the tail prefix sums over
+// positions >= kk continue from *carry.
+__device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t kk, double* carry,
+                            WinSmem& sm) {
+  const int tid = threadIdx.x;
+  const int n = pow2_at_least(max(cnt, 2));
+  for (int s = cnt + tid; s < n; s += kWinThreads) {
+    sm.wkey[s] = -CUDART_INF;
+    sm.widx[s] = INT_MAX;
+  }
+  __syncthreads();
+  bitonic_desc(sm.wkey, sm.widx, n);
+  // tail prefix sums: blocked ranges of kWinIpt positions per thread
+  double loc = 0.0;
+#pragma unroll
+  for (int i = 0; i < kWinIpt; ++i) {
+    const int s = tid * kWinIpt + i;
+    if (s < cnt && len + s >= kk) loc += sm.wkey[s];
+  }
+  double excl = 0.0;
+  cub::BlockScan<double, kWinThreads>(sm.u.dscan).ExclusiveSum(loc, excl);
+  double run = *carry + excl;
+#pragma unroll
+  for (int i = 0; i < kWinIpt; ++i) {
+    const int s = tid * kWinIpt + i;
+    if (s < cnt) {
+      const int64_t pos = len + s;
+      const double x = sm.wkey[s];
+      a.xs[pos] = x;
+      a.perm[pos] = sm.widx[s];
+      if (pos >= kk) {
+        run += x;
+        a.tail[pos] = run;
+      }
+      sm.wtail[s] = run;
+      if (s == cnt - 1) sm.red[0] = run;  // running tail sum at the window's end
+    }
+  }
+  __syncthreads();
+  *carry = sm.red[0];
+  __syncthreads();
+}
+
+// Fenchel bound from the slab epilogue's products (fista.py:150-157).  With
+// k <= 32 the top-k Huber values are among the per-slab top-32 lists.
+__device__ int dual_step_slabs(const EngineArgs& a, ProxSmem& ps, WinSmem& ws) {
+  const Params* P = a.prm;
+  State* st = a.st;
+  const int64_t p = a.p;
+  const double acc[3] = {a.gv[2 * a.pv], a.gv[2 * a.pv + 1], a.gv[2 * a.pv + 2]};
+  const double fstar = conj_finish(P->loss, acc);
+  double d = -CUDART_INF;
+  if (isfinite(fstar)) {
+    const bool node = P->node_mode != 0;
+    const int S = a.k2_slabs;
+    double fs = 0.0;
+    if (node)
+      for (int s = threadIdx.x; s < S; s += blockDim.x) fs += a.slab_hfone[s];
+    fs = block_sum(fs, ps.red);
+    const int64_t kg = node ? P->k_g : P->k;
+    const int64_t nfree = node ? P->n_free : p;
+    double top;
+    const int64_t m = (int64_t)S * kHTop;
+    if (kg <= kHTop && m <= kWinCap) {
+      // the global top-kg is among the per-slab top-32 lists: sort them
+      const int n = pow2_at_least(m > 2 ? (int)m : 2);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ws.wkey[i] = i < m ? a.slab_htop[i] : -CUDART_INF;
+        ws.widx[i] = i;
+      }
+      __syncthreads();
+      bitonic_desc(ws.wkey, ws.widx, n);
+      double sacc = 0.0;
+      if (threadIdx.x == 0) {
+        for (int64_t i = 0; i < kg && i < n; ++i) {
+          const double h = ws.wkey[i];
+          if (h < 0.0) break;
+          sacc += h;
+        }
+        ps.gfree = sacc;
+      }
+      __syncthreads();
+      top = ps.gfree;
+    } else if (kg <= kHTop) {
+      double c = 0.0;
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) c += a.slab_htop[i] >= 0.0 ? 1.0 : 0.0;
+      const int64_t cnt = (int64_t)block_sum(c, ps.red);
+      top = block_topk_sum(a.slab_htop, m, kg, cnt, ps.sel, ps.red);
+    } else {
+      top = block_topk_sum(a.hval, p, kg, nfree, ps.sel, ps.red);
+    }
+    const double gstar = node ? dadd(fs, top) : top;
+    d = dsub(-fstar, dmul(P->two_l2, gstar));
+  }
+  if (threadIdx.x == 0) {
+    bound_update(st, P, d);
+    ps.done = st->done;
+  }
+  __syncthreads();
+  return ps.done;
+}
+
 __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
   WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
-  using Sort = cub::BlockRadixSort<double, kWinThreads, kWinIpt, int, 6>;
   const State* st0 = a.st;
   if (st0->done) return;
   if (st0->dual_pending) {
-    if (dual_step(a, ps)) return;
+    if (dual_step_slabs(a, ps, sm)) return;
   }
   if (a.st->dual_only) return;
   const Params* P = a.prm;
@@ -292,77 +427,82 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   const int64_t kk = node ? P->k_rem : P->k;
   const int64_t kg = node ? P->k_g : P->k;
   const double rho = P->rho, M = P->M;
-  const int how = (kk <= 0 || nf == 0) ? 0 : (kk >= nf ? 1 : 2);
+  const int how = prox_case(P, p);
   double* out = a.beta + ring(st->t + 1) * a.pv;
+  const int S = a.k2_slabs;
 
-  // ---- sorted prefix, window by window -------------------------------------
   int64_t len = 0;                      // sorted prefix length
   unsigned long long ub = ~0ull;        // keys of the next window are below ub
   double carry = 0.0;                   // running tail prefix sum
-  bool more = true;                     // positive keys remain unsorted
-  if (tid == 0) sm.res = (how == 2) ? 0 : 2;
+  bool dirty = false;                   // slab partials no longer describe the outputs
+  if (tid == 0) sm.res = 2;
   __syncthreads();
-  while (how == 2 && more) {
-    select_window(a.key, p, ub, kWinCap, sm);
-    if (sm.sel_state == 2) {
-      if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
-      return;
+  if (how == 2) {
+    // ---- fast path: the candidates K2 compacted per slab (keys >= theta) -----
+    const double theta = st->theta;
+    bool fast = theta > 0.0 && S <= kWinThreads;
+    int total = 0;
+    if (fast) {
+      // offsets of the per-slab lists (slab order = index order)
+      const int c = tid < S ? a.slab_cnt[tid] : 0;
+      int ex = 0;
+      cub::BlockScan<int, kWinThreads>(sm.u.iscan).ExclusiveSum(c, ex, total);
+      __syncthreads();
+      if (tid < S) sm.u.hist[tid] = (unsigned)ex;
+      __syncthreads();
+      fast = total > kk && total <= kWinCap;
     }
-    const unsigned long long lb = sm.sel_lb;
-    const int cnt = sm.sel_count;
-    compact_window(a.key, p, lb, ub, sm);
-    double keys[kWinIpt];
-    int ids[kWinIpt];
-#pragma unroll
-    for (int i = 0; i < kWinIpt; ++i) {
-      const int s = tid * kWinIpt + i;
-      keys[i] = s < cnt ? sm.wkey[s] : -CUDART_INF;
-      ids[i] = s < cnt ? sm.widx[s] : 0;
-    }
-    __syncthreads();
-    Sort(sm.u.sort).SortDescending(keys, ids);  // stable: ids ascending on ties
-    __syncthreads();
-    double loc = 0.0;
-#pragma unroll
-    for (int i = 0; i < kWinIpt; ++i) {
-      const int64_t pos = len + tid * kWinIpt + i;
-      if (tid * kWinIpt + i < cnt && pos >= kk) loc += keys[i];
-    }
-    double excl = 0.0;
-    cub::BlockScan<double, kWinThreads>(sm.u.dscan).ExclusiveSum(loc, excl);
-    double run = carry + excl;
-#pragma unroll
-    for (int i = 0; i < kWinIpt; ++i) {
-      const int s = tid * kWinIpt + i;
-      if (s < cnt) {
-        const int64_t pos = len + s;
-        a.xs[pos] = keys[i];
-        a.perm[pos] = ids[i];
-        if (pos >= kk) {
-          run += keys[i];
-          a.tail[pos] = run;
+    if (fast) {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int sidx = warp; sidx < S; sidx += kWinThreads / 32) {
+        const int c = a.slab_cnt[sidx];
+        const int o = (int)sm.u.hist[sidx];
+        for (int i = lane; i < c; i += 32) {
+          sm.wkey[o + i] = a.cand_key[(int64_t)sidx * kK2Slab + i];
+          sm.widx[o + i] = a.cand_idx[(int64_t)sidx * kK2Slab + i];
         }
-        if (s == cnt - 1) sm.red[0] = run;  // running tail sum at the window's end
       }
+      __syncthreads();
+      double below = 0.0;
+      for (int sidx = tid; sidx < S; sidx += kWinThreads) below = fmax(below, a.slab_below[sidx]);
+      below = block_max(below, sm.red);
+      sort_append(a, total, 0, kk, &carry, sm);
+      len = total;
+      ub = key_bits(theta);
+      window_search(sm.wkey, sm.wtail, len, kk, rho, M, nf > len, below, sm);
+      if (sm.res == 3) dirty = true;   // pool reaches below theta: extend windows
+    } else {
+      dirty = true;
+      if (tid == 0) st->slow_prox += 1;
+      if (tid == 0) sm.res = 3;
+      __syncthreads();
     }
-    __threadfence_block();
-    __syncthreads();
-    const double wend = sm.red[0];
-    __syncthreads();
-    carry = wend;
-    len += cnt;
-    ub = lb;
-    const double xn = sm.xnext;
-    more = xn > 0.0;
-    // zero keys (never in a pool) follow the positives
-    const bool has_next = more || (len < nf);
-    if (len > kk || !more) {
-      window_search(a.xs, a.tail, len, kk, rho, M, has_next, more ? xn : 0.0, sm);
-      if (sm.res == 1 || sm.res == 2) break;
-      if (!more) {  // pool would extend into zero keys: cannot happen (x=0 <= V)
-        if (tid == 0) sm.res = 2;
+    // ---- slow path / extension: windows selected over all remaining keys ---
+    bool more = true;
+    while (sm.res == 3 && more) {
+      select_window(a.key, p, ub, kWinCap, sm);
+      if (sm.sel_state == 2) {
+        if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
+        return;
+      }
+      const unsigned long long lb = sm.sel_lb;
+      const int cnt = sm.sel_count;
+      compact_window(a.key, p, lb, ub, sm);
+      const double xn = sm.xnext;
+      sort_append(a, cnt, len, kk, &carry, sm);
+      len += cnt;
+      ub = lb;
+      more = xn > 0.0;
+      const bool has_next = more || (len < nf);
+      if (len > kk || !more) {
+        window_search(a.xs, a.tail, len, kk, rho, M, has_next, more ? xn : 0.0, sm);
+        if (!more && sm.res == 3) {
+          if (tid == 0) sm.res = 2;
+          __syncthreads();
+        }
+      } else {
+        if (tid == 0) sm.res = 3;
         __syncthreads();
-        break;
       }
     }
   }
@@ -371,32 +511,24 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   const double vstar = sm.vstar;
 
   // ---- scatter ----------------------------------------------------------------
-  // prefix positions carry their sorted rank; every other free coordinate is
-  // a tail singleton (or elementwise / pass-through for how = 1 / 0)
   const unsigned long long lb_last = ub;
   const int64_t kkg = kg < nf ? kg : nf;
   const int64_t W = min(len, kkg + 64);
   double total = 0.0, amax = 0.0, rest = 0.0;
-  for (int64_t j = tid; j < p; j += kWinThreads) {
-    const int cls = node ? a.mask[j] : FREE;
-    const double gin = a.gam[j];
-    const double mu = dmul(rho, gin);
-    double res;
-    bool in_prefix = false;
-    if (cls == FIXED_ZERO) {
-      res = 0.0;  // fista.py:126-127
-    } else if (cls == FIXED_ONE) {
-      res = dsub(gin, ddiv(dmul(dsign(mu), hprox(fabs(mu), rho, M)), rho));
-    } else if (how == 0) {
-      res = dsub(gin, ddiv(mu, rho));
-    } else if (how == 1) {
-      res = dsub(gin, ddiv(dmul(dsign(mu), hprox(fabs(mu), rho, M)), rho));
-    } else {
+  if (dirty) {
+    // recompute every non-prefix coordinate (K2's speculative outputs cover a
+    // smaller prefix than the one sorted here)
+    for (int64_t j = tid; j < p; j += kWinThreads) {
+      const int cls = node ? a.mask[j] : FREE;
+      const double gin = a.gam[j];
+      const double mu = dmul(rho, gin);
       const double k = a.key[j];
-      in_prefix = k > 0.0 && key_bits(k) >= lb_last;
-      res = dsub(gin, ddiv(mu, rho));  // tail singleton: out = mu
-    }
-    if (!in_prefix) {
+      const bool in_prefix = cls == FREE && k > 0.0 && key_bits(k) >= lb_last;
+      if (in_prefix) continue;
+      double res;
+      if (cls == FIXED_ZERO) res = 0.0;
+      else if (cls == FIXED_ONE) res = dsub(gin, ddiv(dmul(dsign(mu), hprox(fabs(mu), rho, M)), rho));
+      else res = dsub(gin, ddiv(mu, rho));
       out[j] = res;
       if (cls == FREE) {
         const double ab = fabs(res);
@@ -408,6 +540,13 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
         a.scratch[j] = -1.0;
       }
     }
+  } else {
+    // non-candidates were written by K2's slab epilogue; fixed-order partials
+    for (int sidx = tid; sidx < S; sidx += kWinThreads) {
+      total += a.slab_sum[sidx];
+      amax = fmax(amax, a.slab_max[sidx]);
+    }
+    rest = amax;
   }
   if (how == 2) {
     for (int64_t pos = tid; pos < len; pos += kWinThreads) {
@@ -453,8 +592,6 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   else if (total > dmul(dmul((double)kg, M), dadd(1.0, kFeasRtol))) { gfree = CUDART_INF; path = 2; }
   else if (kg == 0) path = 2;
   if (path == 0) {
-    // window of the first W sorted positions; any free coordinate outside it
-    // must not exceed the kkg-th largest inside (else radix-select fallback)
     if (how == 2 && W >= kkg && W <= kCandCap) {
       block_rank_sort_desc(ps.cand, ps.cand2, (int)W);
       if (rest > ps.cand2[kkg - 1]) path = 1;
@@ -493,6 +630,15 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
     double g = gfree;
     if (node) g = fone_bad ? CUDART_INF : dadd(dadd(0.0, fone_val), gfree);
     st->g_next = g;
+    // window threshold for the next iteration's K2: keep ~2x the pool (>= 1536
+    // keys, <= 3/4 of the window capacity) above it
+    if (how == 2 && len > 0) {
+      int64_t want = max((int64_t)1536, kk + 64);
+      if (cstar >= 0) want = max(want, 2 * (cstar + 1));
+      want = min(want, (int64_t)(3 * kWinCap / 4));
+      const int64_t pos = min(len - 1, want);
+      st->theta = a.xs[pos];
+    }
   }
 }
 

@@ -172,6 +172,7 @@ def solve_relaxation(instance: ProblemInstance, node: Optional[NodeState] = None
     native.check(rc)
     beta = beta_out if return_device else beta_out.cpu().numpy()
     stats = {"gpu_launches": int(rep.gpu_launches), "topk_fallbacks": int(rep.topk_fallbacks),
+             "prox_full_passes": int(rep.prox_full_passes),
              "lipschitz": float(L)}
     if opts.profile:
         stats.update(k1_ms=rep.k1_ms, k2_ms=rep.k2_ms, k3_ms=rep.k3_ms, k1_count=rep.k1_count,

@@ -47,7 +47,7 @@ class Report(ctypes.Structure):
                 ("status", c_i32), ("error_iteration", c_i64), ("wall_time", c_f64),
                 ("gpu_launches", c_i64), ("topk_fallbacks", c_i64), ("k1_ms", c_f64),
                 ("k2_ms", c_f64), ("k3_ms", c_f64), ("k1_count", c_i64), ("k2_count", c_i64),
-                ("k3_count", c_i64)]
+                ("k3_count", c_i64), ("prox_full_passes", c_i64)]
 
 
 class TraceRecord(ctypes.Structure):
