@@ -289,9 +289,11 @@ __device__ __forceinline__ void k2_accumulate(const EngineArgs& a, const double 
 
 struct K2Smem {
   double sr[2][kK2StageRows];
-  double sacc[8][2][kK2Slab];  // per-warp column sums (fixed-order combine)
+  union {
+    double sacc[8][2][kK2Slab];  // per-warp column sums (fixed-order combine)
+    EpiSmem epi;                 // slab epilogue (after the partials are published)
+  };
   double red[32];
-  EpiSmem epi;
   unsigned item;
   int last;
 };

@@ -27,6 +27,7 @@
 #include "control.cuh"
 #include "engine.cuh"
 #include "prox.cuh"
+#include "sortnet.cuh"
 
 namespace l0 {
 
@@ -44,6 +45,8 @@ struct WinSmem {
   double wkey[kWinCap];
   int widx[kWinCap];
   double wtail[kWinCap];
+  double mkey[kWinCap];   // merge ping-pong buffer
+  int midx[kWinCap];
   // window selection results
   unsigned long long sel_lb;
   int sel_count;
@@ -274,50 +277,22 @@ __device__ void window_search(const double* xs, const double* tail, int64_t len,
   }
 }
 
-// Bitonic sort in shared memory: n (power of two) pairs, descending by key,
-// ties by ascending index -- a total order, so the result equals the
-// reference's stable descending argsort (prox.py:111).  O(log^2 n) barriers,
-// no atomics; for the few thousand window keys it beats a 64-bit radix sort.
-__device__ void bitonic_desc(double* key, int* idx, int n) {
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
-        const int i = 2 * t - (t & (j - 1));
-        const int l = i + j;
-        const double ki = key[i], kl = key[l];
-        const int ii = idx[i], il = idx[l];
-        const bool ordered = (ki > kl) || (ki == kl && ii < il);
-        const bool want = (i & k) == 0;  // this block sorts toward the final order
-        if (want != ordered) {
-          key[i] = kl; key[l] = ki;
-          idx[i] = il; idx[l] = ii;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__device__ __forceinline__ int pow2_at_least(int c) {
-  int n = 1;
-  while (n < c) n <<= 1;
-  return n;
-}
-
 // Sort the window held in sm.wkey/widx[0..cnt) and append it to the sorted
 // prefix at position len (global xs/perm/tail; the window also stays sorted
 // in shared memory with its tail sums in sm.wtail); the tail prefix sums over
 // positions >= kk continue from *carry.
 __device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t kk, double* carry,
-                            WinSmem& sm) {
+                            WinSmem& sm, bool presorted = false) {
   const int tid = threadIdx.x;
-  const int n = pow2_at_least(max(cnt, 2));
-  for (int s = cnt + tid; s < n; s += kWinThreads) {
-    sm.wkey[s] = -CUDART_INF;
-    sm.widx[s] = INT_MAX;
+  if (!presorted) {
+    const int n = pow2_at_least(max(cnt, 2));
+    for (int s = cnt + tid; s < n; s += kWinThreads) {
+      sm.wkey[s] = -CUDART_INF;
+      sm.widx[s] = INT_MAX;
+    }
+    __syncthreads();
+    bitonic_desc(sm.wkey, sm.widx, n);
   }
-  __syncthreads();
-  bitonic_desc(sm.wkey, sm.widx, n);
   // tail prefix sums: blocked ranges of kWinIpt positions per thread
   double loc = 0.0;
 #pragma unroll
@@ -449,6 +424,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
       cub::BlockScan<int, kWinThreads>(sm.u.iscan).ExclusiveSum(c, ex, total);
       __syncthreads();
       if (tid < S) sm.u.hist[tid] = (unsigned)ex;
+      if (tid == 0) sm.u.hist[S] = (unsigned)total;
       __syncthreads();
       fast = total > kk && total <= kWinCap;
     }
@@ -463,10 +439,18 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
         }
       }
       __syncthreads();
+      // the runs arrive sorted (K2's slab epilogue): merge them
+      if (merge_runs(sm.wkey, sm.widx, sm.mkey, sm.midx, sm.u.hist, S, total)) {
+        for (int i = tid; i < total; i += kWinThreads) {
+          sm.wkey[i] = sm.mkey[i];
+          sm.widx[i] = sm.midx[i];
+        }
+        __syncthreads();
+      }
       double below = 0.0;
       for (int sidx = tid; sidx < S; sidx += kWinThreads) below = fmax(below, a.slab_below[sidx]);
       below = block_max(below, sm.red);
-      sort_append(a, total, 0, kk, &carry, sm);
+      sort_append(a, total, 0, kk, &carry, sm, true);
       len = total;
       ub = key_bits(theta);
       window_search(sm.wkey, sm.wtail, len, kk, rho, M, nf > len, below, sm);

@@ -1,0 +1,107 @@
+// Small in-block sorting networks for (key, index) pairs in shared memory.
+//
+// Order: descending key, ties by ascending index -- a total order, so every
+// result equals numpy's stable argsort of -|mu| (prox.py:111) on the same
+// keys, independent of input order.
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace l0 {
+
+// a precedes b in the sorted order
+__device__ __forceinline__ bool precedes(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__device__ __forceinline__ int pow2_at_least(int c) {
+  int n = 1;
+  while (n < c) n <<= 1;
+  return n;
+}
+
+// Bitonic sort of n (power of two) pairs; every thread of the block takes part.
+__device__ void bitonic_desc(double* key, int* idx, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (j - 1));
+        const int l = i + j;
+        const double ki = key[i], kl = key[l];
+        const int ii = idx[i], il = idx[l];
+        const bool ordered = precedes(ki, ii, kl, il);
+        const bool want = (i & k) == 0;  // this block sorts toward the final order
+        if (want != ordered) {
+          key[i] = kl; key[l] = ki;
+          idx[i] = il; idx[l] = ii;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Number of elements of the sorted run [lo, hi) that precede (k, i).
+__device__ __forceinline__ int count_preceding(const double* key, const int* idx, int lo, int hi,
+                                               double k, int i) {
+  int a = lo, b = hi;
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (precedes(key[m], idx[m], k, i)) a = m + 1;
+    else b = m;
+  }
+  return a - lo;
+}
+
+// Merge S sorted runs (run r = [off[r], off[r+1]), off[S] = total) by
+// pairwise co-ranking: every element's destination is its rank in its own run
+// plus its rank in the partner run (binary search).  log2(S) levels,
+// ping-ponging between (k0, i0) and (k1, i1); `off` (S + 1 entries, shared)
+// is rewritten.  Returns 0 if the result is in (k0, i0), 1 otherwise.
+__device__ int merge_runs(double* k0, int* i0, double* k1, int* i1, unsigned* off, int S,
+                          int total) {
+  int cur = 0;
+  while (S > 1) {
+    double* ks = cur ? k1 : k0;
+    int* is = cur ? i1 : i0;
+    double* kd = cur ? k0 : k1;
+    int* id = cur ? i0 : i1;
+    for (int q = threadIdx.x; q < total; q += blockDim.x) {
+      // run of q: last r with off[r] <= q
+      int a = 0, b = S - 1;
+      while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if ((int)off[m] <= q) a = m;
+        else b = m - 1;
+      }
+      const int r = a;
+      const int left = r & ~1;
+      const double k = ks[q];
+      const int i = is[q];
+      int dest;
+      if (left + 1 >= S) {
+        dest = q;  // odd run out: copied
+      } else {
+        const int sa = (int)off[left], sb = (int)off[left + 1], eb = (int)off[left + 2];
+        if (r == left) dest = sa + (q - sa) + count_preceding(ks, is, sb, eb, k, i);
+        else dest = sa + (q - sb) + count_preceding(ks, is, sa, sb, k, i);
+      }
+      kd[dest] = k;
+      id[dest] = i;
+    }
+    __syncthreads();
+    const int S2 = (S + 1) >> 1;
+    unsigned o = 0;
+    if ((int)threadIdx.x <= S2) o = ((int)threadIdx.x < S2) ? off[2 * threadIdx.x] : (unsigned)total;
+    __syncthreads();
+    if ((int)threadIdx.x <= S2) off[threadIdx.x] = o;
+    __syncthreads();
+    S = S2;
+    cur ^= 1;
+  }
+  return cur;
+}
+
+}  // namespace l0
