@@ -127,6 +127,9 @@ int32_t l0_problem_destroy(l0_problem* prob);
 int32_t l0_problem_set_comm(l0_problem* prob, const void* h_nccl_unique_id, int32_t nranks,
                             int32_t rank);
 
+/* diagnostics: clock64 phase stamps of the last prox kernel (L0_PROBE builds) */
+int32_t l0_debug_probe(l0_problem* prob, int64_t* h_out16);
+
 /* ---- hot path ----------------------------------------------------------------- */
 int32_t l0_fista_solve(l0_problem* prob, int64_t k, double M, double lambda2,
                        const l0_fista_opts* opts, const l0_node* node /* nullable */,

@@ -41,7 +41,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+    extra = ["-DL0_PROBE"] if os.environ.get("L0_PROBE") else []
+    cmd = [nvcc_path(), *ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}",
            os.path.join(CSRC, "l0_b200.cu"), "-o", OUT + ".tmp", "-ldl"]

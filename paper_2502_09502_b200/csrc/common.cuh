@@ -219,7 +219,14 @@ struct State {
   double loss_cur;
   double theta;           // window-candidate threshold K2 applies (set by K3)
   int64_t slow_prox;      // diagnostics: K3 iterations that needed a full key pass
+  long long probe[16];     // clock64 phase stamps of the last K3 (L0_PROBE builds)
   TraceRec trace[kTraceCap];
 };
+
+#ifdef L0_PROBE
+#define L0_STAMP(st, i) do { if (threadIdx.x == 0) (st)->probe[i] = clock64(); } while (0)
+#else
+#define L0_STAMP(st, i) do { } while (0)
+#endif
 
 }  // namespace l0

@@ -386,6 +386,12 @@ int32_t l0_problem_destroy(l0_problem* P) {
   return ST_OK;
 }
 
+int32_t l0_debug_probe(l0_problem* P, int64_t* out16) {
+  if (!P || !out16) return set_error(ST_INVALID, "null argument");
+  for (int i = 0; i < 16; ++i) out16[i] = P->h_st[0]->probe[i];
+  return ST_OK;
+}
+
 int32_t l0_problem_set_comm(l0_problem* P, const void* h_id, int32_t nranks, int32_t rank) {
   if (!P || !h_id) return set_error(ST_INVALID, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(ST_INVALID, "bad rank");

@@ -31,8 +31,8 @@
 
 namespace l0 {
 
-constexpr int kWinThreads = 1024;
-constexpr int kWinIpt = 4;
+constexpr int kWinThreads = 512;
+constexpr int kWinIpt = 8;
 constexpr int kWinCap = kWinThreads * kWinIpt;  // 4096 keys per window
 constexpr int kHistBins = 8192;                 // 13-bit digits
 
@@ -105,12 +105,13 @@ __device__ void select_window(const double* key, int64_t p, unsigned long long u
       if (digit >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sm.u.hist[digit], (unsigned)__popc(peers));
     }
     __syncthreads();
-    // bins in descending order: thread t owns bins kHistBins-1-8t .. kHistBins-8-8t
-    unsigned c8[8];
+    // bins in descending order: thread t owns bins kHistBins-1-B*t .. kHistBins-B-B*t
+    constexpr int B = kHistBins / kWinThreads;
+    unsigned c8[B];
     int s = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int d = kHistBins - 1 - (tid * 8 + q);
+    for (int q = 0; q < B; ++q) {
+      const int d = kHistBins - 1 - (tid * B + q);
       c8[q] = (d >= 0 && d <= (int)mask) ? sm.u.hist[d] : 0u;
       s += (int)c8[q];
     }
@@ -126,8 +127,8 @@ __device__ void select_window(const double* key, int64_t p, unsigned long long u
     }
     if (above + total > cap && above + excl <= cap && above + excl + s > cap) {
       int cum = above + excl;
-      for (int q = 0; q < 8; ++q) {
-        const int d = kHistBins - 1 - (tid * 8 + q);
+      for (int q = 0; q < B; ++q) {
+        const int d = kHistBins - 1 - (tid * B + q);
         if (cum + (int)c8[q] > cap) {
           // bin d crosses the capacity: stop above it, or refine into it
           const bool enough = cum >= cap / 2 || cum > 0 && level == 4;
@@ -281,17 +282,34 @@ __device__ void window_search(const double* xs, const double* tail, int64_t len,
 // prefix at position len (global xs/perm/tail; the window also stays sorted
 // in shared memory with its tail sums in sm.wtail); the tail prefix sums over
 // positions >= kk continue from *carry.
+template <int E>
+__device__ void sort_window_regs(WinSmem& sm, int cnt) {
+  double k[E];
+  int id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int s = e * kWinThreads + threadIdx.x;
+    k[e] = s < cnt ? sm.wkey[s] : -CUDART_INF;
+    id[e] = s < cnt ? sm.widx[s] : INT_MAX;
+  }
+  __syncthreads();
+  bitonic_regs<kWinThreads, E>(k, id, sm.mkey, sm.midx);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    sm.wkey[e * kWinThreads + threadIdx.x] = k[e];
+    sm.widx[e * kWinThreads + threadIdx.x] = id[e];
+  }
+  __syncthreads();
+}
+
 __device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t kk, double* carry,
                             WinSmem& sm, bool presorted = false) {
   const int tid = threadIdx.x;
   if (!presorted) {
-    const int n = pow2_at_least(max(cnt, 2));
-    for (int s = cnt + tid; s < n; s += kWinThreads) {
-      sm.wkey[s] = -CUDART_INF;
-      sm.widx[s] = INT_MAX;
-    }
-    __syncthreads();
-    bitonic_desc(sm.wkey, sm.widx, n);
+    if (cnt <= kWinThreads) sort_window_regs<1>(sm, cnt);
+    else if (cnt <= 2 * kWinThreads) sort_window_regs<2>(sm, cnt);
+    else if (cnt <= 4 * kWinThreads) sort_window_regs<4>(sm, cnt);
+    else sort_window_regs<8>(sm, cnt);
   }
   // tail prefix sums: blocked ranges of kWinIpt positions per thread
   double loc = 0.0;
@@ -389,6 +407,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
   const State* st0 = a.st;
   if (st0->done) return;
+  L0_STAMP(a.st, 0);
   if (st0->dual_pending) {
     if (dual_step_slabs(a, ps, sm)) return;
   }
@@ -412,6 +431,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   bool dirty = false;                   // slab partials no longer describe the outputs
   if (tid == 0) sm.res = 2;
   __syncthreads();
+  L0_STAMP(st, 1);
   if (how == 2) {
     // ---- fast path: the candidates K2 compacted per slab (keys >= theta) -----
     const double theta = st->theta;
@@ -439,21 +459,17 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
         }
       }
       __syncthreads();
-      // the runs arrive sorted (K2's slab epilogue): merge them
-      if (merge_runs(sm.wkey, sm.widx, sm.mkey, sm.midx, sm.u.hist, S, total)) {
-        for (int i = tid; i < total; i += kWinThreads) {
-          sm.wkey[i] = sm.mkey[i];
-          sm.widx[i] = sm.midx[i];
-        }
-        __syncthreads();
-      }
+      L0_STAMP(st, 2);
       double below = 0.0;
       for (int sidx = tid; sidx < S; sidx += kWinThreads) below = fmax(below, a.slab_below[sidx]);
       below = block_max(below, sm.red);
-      sort_append(a, total, 0, kk, &carry, sm, true);
+      L0_STAMP(st, 3);
+      sort_append(a, total, 0, kk, &carry, sm);
+      L0_STAMP(st, 4);
       len = total;
       ub = key_bits(theta);
       window_search(sm.wkey, sm.wtail, len, kk, rho, M, nf > len, below, sm);
+      L0_STAMP(st, 5);
       if (sm.res == 3) dirty = true;   // pool reaches below theta: extend windows
     } else {
       dirty = true;
@@ -494,6 +510,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   const int64_t cstar = (how == 2 && sm.res == 1) ? sm.cstar : -1;
   const double vstar = sm.vstar;
 
+  L0_STAMP(st, 6);
   // ---- scatter ----------------------------------------------------------------
   const unsigned long long lb_last = ub;
   const int64_t kkg = kg < nf ? kg : nf;
@@ -532,10 +549,11 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
     }
     rest = amax;
   }
+  const bool smem_prefix = !dirty;   // fast path: the whole prefix is the smem window
   if (how == 2) {
     for (int64_t pos = tid; pos < len; pos += kWinThreads) {
-      const int j = a.perm[pos];
-      const double x = a.xs[pos];
+      const int j = smem_prefix ? sm.widx[pos] : a.perm[pos];
+      const double x = smem_prefix ? sm.wkey[pos] : a.xs[pos];
       const double gin = a.gam[j];
       const double mu = dmul(rho, gin);
       double nu;
@@ -557,6 +575,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   amax = block_max(amax, ps.red);
   rest = block_max(rest, ps.red);
 
+  L0_STAMP(st, 7);
   // ---- g(beta+) (perspective.py:76-132) ----------------------------------------
   double fone_val = 0.0;
   bool fone_bad = false;
@@ -617,13 +636,18 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
     // window threshold for the next iteration's K2: keep ~2x the pool (>= 1536
     // keys, <= 3/4 of the window capacity) above it
     if (how == 2 && len > 0) {
-      int64_t want = max((int64_t)1536, kk + 64);
-      if (cstar >= 0) want = max(want, 2 * (cstar + 1));
+      // window for the next iteration: the pool plus a 25% (>= 64 keys) margin
+      int64_t want = kk + 64;
+      if (cstar >= 0) {
+        const int64_t c1 = cstar + 1;
+        want = max(want, c1 + max((int64_t)64, c1 / 4));
+      }
       want = min(want, (int64_t)(3 * kWinCap / 4));
       const int64_t pos = min(len - 1, want);
       st->theta = a.xs[pos];
     }
   }
+  L0_STAMP(st, 8);
 }
 
 size_t prox_window_smem() {

@@ -30,8 +30,6 @@ struct EpiSmem {
     typename cub::BlockRadixSort<double, kK2Slab, 1>::TempStorage sort;
   } u;
   double red[32];
-  double ckey[kK2Slab];
-  int cidx[kK2Slab];
 };
 
 // how the free coordinates are treated (prox.py:104-112): 0 pass-through,
@@ -82,22 +80,9 @@ __device__ void slab_epilogue(const EngineArgs& a, int slab, int64_t t, double c
     // candidate compaction in index order
     int pos = 0, count = 0;
     cub::BlockScan<int, kK2Slab>(sm.u.scan).ExclusiveSum(cand ? 1 : 0, pos, count);
-    // sort this slab's candidates (K3 merges the sorted runs)
-    __syncthreads();
     if (cand) {
-      sm.ckey[pos] = key;
-      sm.cidx[pos] = (int)j;
-    }
-    const int nsort = pow2_at_least(count > 2 ? count : 2);
-    if (tid >= count && tid < nsort) {
-      sm.ckey[tid] = -CUDART_INF;
-      sm.cidx[tid] = INT_MAX;
-    }
-    __syncthreads();
-    if (count > 1) bitonic_desc(sm.ckey, sm.cidx, nsort);
-    if (tid < count) {
-      a.cand_key[(int64_t)slab * kK2Slab + tid] = sm.ckey[tid];
-      a.cand_idx[(int64_t)slab * kK2Slab + tid] = sm.cidx[tid];
+      a.cand_key[(int64_t)slab * kK2Slab + pos] = key;
+      a.cand_idx[(int64_t)slab * kK2Slab + pos] = (int)j;
     }
     const double s = block_sum(ab, sm.red);
     const double m = block_max(ab, sm.red);

@@ -43,6 +43,65 @@ __device__ void bitonic_desc(double* key, int* idx, int n) {
   }
 }
 
+// Register bitonic sort of N = T * E pairs held E per thread (element e of
+// thread t is position e * T + t).  Strides < 32 exchange through warp
+// shuffles, strides 32..T/2 through shared memory (sk/si, N entries), strides
+// >= T inside the thread; only the shared-memory stages need barriers.
+// Requires blockDim.x == T.
+template <int T, int E>
+__device__ void bitonic_regs(double (&k)[E], int (&id)[E], double* sk, int* si) {
+  constexpr int N = T * E;
+  const int tid = threadIdx.x;
+#pragma unroll 1
+  for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= T) {
+        const int je = j / T;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+#pragma unroll
+          for (int e2 = e + 1; e2 < E; ++e2) {
+            if ((e ^ e2) == je) {                    // static indices: stays in registers
+              const int i = e * T + tid;               // lower position of the pair
+              const bool dir = (i & kk) == 0;
+              const bool ord = precedes(k[e], id[e], k[e2], id[e2]);
+              if (dir != ord) {
+                const double tk = k[e]; k[e] = k[e2]; k[e2] = tk;
+                const int ti = id[e]; id[e] = id[e2]; id[e2] = ti;
+              }
+            }
+          }
+        }
+      } else if (j >= 32) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) { sk[e * T + tid] = k[e]; si[e * T + tid] = id[e]; }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = e * T + tid;
+          const double pk = sk[i ^ j];
+          const int pi = si[i ^ j];
+          const bool first = precedes(k[e], id[e], pk, pi);   // mine precedes the partner
+          const bool lo = (i & j) == 0, dir = (i & kk) == 0;
+          if ((lo == dir) != first) { k[e] = pk; id[e] = pi; }
+        }
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = e * T + tid;
+          const double pk = __shfl_xor_sync(0xffffffffu, k[e], j);
+          const int pi = __shfl_xor_sync(0xffffffffu, id[e], j);
+          const bool first = precedes(k[e], id[e], pk, pi);
+          const bool lo = (i & j) == 0, dir = (i & kk) == 0;
+          if ((lo == dir) != first) { k[e] = pk; id[e] = pi; }
+        }
+      }
+    }
+  }
+}
+
 // Number of elements of the sorted run [lo, hi) that precede (k, i).
 __device__ __forceinline__ int count_preceding(const double* key, const int* idx, int lo, int hi,
                                                double k, int i) {
