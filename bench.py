@@ -300,9 +300,8 @@ def run_ours_sharded(args, world, rank, local):
     eng.native.load()
     cd = make_inputs(args.scale)
     r0, r1 = shard.row_range(cd.n, world, rank)
-    inst = shard.ShardedInstance(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
-                                 cd.M, cd.lambda2, n_global=cd.n)
-    inst.device_problem()
+    inst = shard.ShardedProblem(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
+                                cd.M, cd.lambda2, n_global=cd.n)
     K, W = args.steps, args.warmup
     opts = lambda it: eng.FistaOptions(lipschitz=L_C2, max_iterations=it, gap_tolerance=1e-300,
                                        stop_on_gap=False)

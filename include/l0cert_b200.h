@@ -122,10 +122,14 @@ int32_t l0_problem_create(const void* d_X, int32_t dtype, int64_t n, int64_t p, 
 int32_t l0_problem_workspace_bytes(const l0_problem* prob, uint64_t* bytes);
 int32_t l0_problem_set_workspace(l0_problem* prob, void* d_ws, uint64_t bytes);
 int32_t l0_problem_destroy(l0_problem* prob);
-/* row-sharded mode: this rank holds rows [row0, row0+n) of a global X; the
- * gradient and loss are all-reduced over NCCL (unique id of 128 bytes). */
+/* Row-sharded mode: this rank's problem holds a contiguous block of rows of
+ * the global X; every iteration all-reduces [X^T r | X^T zeta | F* terms] and
+ * the loss over NCCL (h_nccl_unique_id: 128 bytes from l0_nccl_unique_id on
+ * rank 0, broadcast by the caller).  nranks == 1 with a NULL id runs the
+ * sharded kernels with the all-reduces elided (single-GPU test of that path). */
 int32_t l0_problem_set_comm(l0_problem* prob, const void* h_nccl_unique_id, int32_t nranks,
                             int32_t rank);
+int32_t l0_nccl_unique_id(void* h_out128);
 
 /* diagnostics: clock64 phase stamps of the last prox kernel (L0_PROBE builds) */
 int32_t l0_debug_probe(l0_problem* prob, int64_t* h_out16);

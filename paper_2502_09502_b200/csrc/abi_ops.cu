@@ -251,10 +251,12 @@ int32_t l0_all_finite(const void* d_x, int32_t dtype, int64_t rows, int64_t cols
 }
 
 // ---- problem-level ops -----------------------------------------------------------
-static int problem_ready(l0_problem* P) {
+static int problem_ready(l0_problem* P, bool local_ok = false) {
   if (!P) return set_error(ST_INVALID, "null problem");
   if (!P->ws) return set_error(ST_INVALID, "problem has no workspace");
-  if (P->a.multi) return set_error(ST_UNSUPPORTED, "operator not available in row-sharded mode");
+  // matvecs act on this rank's rows; global reductions are the caller's
+  if (P->a.multi && !local_ok)
+    return set_error(ST_UNSUPPORTED, "operator needs a global reduction in row-sharded mode");
   return ST_OK;
 }
 
@@ -276,13 +278,13 @@ static int plain_k2(l0_problem* P, const double* r, double* out, cudaStream_t s)
 }
 
 int32_t l0_matvec(l0_problem* P, const double* d_v, double* d_out, void* stream) {
-  int rc = problem_ready(P);
+  int rc = problem_ready(P, true);
   if (rc) return rc;
   return plain_k1(P, d_v, d_out, (cudaStream_t)stream);
 }
 
 int32_t l0_rmatvec(l0_problem* P, const double* d_r, double* d_out, void* stream) {
-  int rc = problem_ready(P);
+  int rc = problem_ready(P, true);
   if (rc) return rc;
   return plain_k2(P, d_r, d_out, (cudaStream_t)stream);
 }

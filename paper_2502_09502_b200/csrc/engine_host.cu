@@ -50,6 +50,7 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   bool load(std::string* err) {
     if (h) return true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -62,6 +63,7 @@ struct NcclApi {
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     if (!commInitRank || !allReduce || !commDestroy) { *err = "NCCL symbols missing"; return false; }
     return true;
   }
@@ -200,9 +202,11 @@ static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
   if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
   L0_CUDA_TRY(launch_k2(a, MODE_ITER, s));
   if (a.multi) {
-    ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)(2 * a.pv + 3), ncclDouble, ncclSum,
-                                      P.comm, s);
-    if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (gradient) failed");
+    if (P.comm) {
+      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)(2 * a.pv + 3), ncclDouble, ncclSum,
+                                        P.comm, s);
+      if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (gradient) failed");
+    }
     L0_CUDA_TRY(launch_grad_step(a, s));
   }
   if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
@@ -212,9 +216,11 @@ static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
   if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[4], s, cudaEventRecordExternal));
   L0_CUDA_TRY(launch_k1(a, MODE_ITER, s));
   if (a.multi) {
-    ncclResult_t r = g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
-                                      ncclSum, P.comm, s);
-    if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (loss) failed");
+    if (P.comm) {
+      ncclResult_t r = g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
+                                        ncclSum, P.comm, s);
+      if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (loss) failed");
+    }
     L0_CUDA_TRY(launch_objective(a, MODE_ITER, s));
   }
   if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[5], s, cudaEventRecordExternal));
@@ -393,12 +399,20 @@ int32_t l0_debug_probe(l0_problem* P, int64_t* out16) {
 }
 
 int32_t l0_problem_set_comm(l0_problem* P, const void* h_id, int32_t nranks, int32_t rank) {
-  if (!P || !h_id) return set_error(ST_INVALID, "null argument");
+  if (!P) return set_error(ST_INVALID, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(ST_INVALID, "bad rank");
+  destroy_graphs(*P);
+  if (P->comm && g_nccl.commDestroy) g_nccl.commDestroy(P->comm);
+  P->comm = nullptr;
   if (nranks == 1) {
-    P->a.multi = 0;
+    // h_id == NULL: run the row-sharded code path on one rank with the
+    // all-reduces elided (tests the sharded kernels on a single GPU)
+    P->a.multi = h_id == nullptr ? 1 : 0;
+    P->nranks = 1;
+    P->rank = 0;
     return ST_OK;
   }
+  if (!h_id) return set_error(ST_INVALID, "NCCL unique id required for nranks > 1");
   std::string err;
   if (!g_nccl.load(&err)) return set_error(ST_CUDA, err);
   ncclUniqueId id;
@@ -408,11 +422,21 @@ int32_t l0_problem_set_comm(l0_problem* P, const void* h_id, int32_t nranks, int
   if (r != ncclSuccess)
     return set_error(ST_CUDA, std::string("ncclCommInitRank: ") +
                                   (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
-  destroy_graphs(*P);
   P->comm = comm;
   P->nranks = nranks;
   P->rank = rank;
   P->a.multi = 1;
+  return ST_OK;
+}
+
+int32_t l0_nccl_unique_id(void* h_out128) {
+  if (!h_out128) return set_error(ST_INVALID, "null argument");
+  std::string err;
+  if (!g_nccl.load(&err)) return set_error(ST_CUDA, err);
+  if (!g_nccl.getUniqueId) return set_error(ST_CUDA, "ncclGetUniqueId missing");
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return set_error(ST_CUDA, "ncclGetUniqueId failed");
+  std::memcpy(h_out128, &id, sizeof(id));
   return ST_OK;
 }
 
@@ -529,8 +553,8 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   L0_CUDA_TRY(launch_k1(a, MODE_INIT, s));  // u_0 = X beta_0, F(u_0), objective
   ++launches;
   if (a.multi) {
-    if (g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble, ncclSum, P->comm,
-                         s) != ncclSuccess)
+    if (P->comm && g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
+                                    ncclSum, P->comm, s) != ncclSuccess)
       return set_error(ST_CUDA, "ncclAllReduce (initial loss) failed");
     L0_CUDA_TRY(launch_objective(a, MODE_INIT, s));
     ++launches;

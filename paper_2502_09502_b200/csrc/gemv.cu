@@ -482,14 +482,16 @@ __global__ void __launch_bounds__(kK2Threads) k2_transpose(EngineArgs a, int mod
 __global__ void __launch_bounds__(kK2Slab) k_grad_step(EngineArgs a) {
   __shared__ EpiSmem sm;
   const State* st = a.st;
-  if (st->done || st->dual_only) return;
+  if (st->done) return;
+  const bool wg = st->dual_only == 0;       // final bound pass: Huber values only
+  const bool wz = st->dual_pending != 0;
+  if (!wg && !wz) return;
   const int64_t t = st->t + 1;
   const double c = momentum(st->phi);
-  const bool wz = st->dual_pending != 0;
   const int64_t j = (int64_t)blockIdx.x * kK2Slab + threadIdx.x;
-  const double g = j < a.p ? a.gv[j] : 0.0;
+  const double g = (wg && j < a.p) ? a.gv[j] : 0.0;
   const double v = (wz && j < a.p) ? a.gv[a.pv + j] : 0.0;
-  slab_epilogue(a, blockIdx.x, t, c, true, wz, g, v, sm);
+  slab_epilogue(a, blockIdx.x, t, c, wg, wz, g, v, sm);
 }
 
 // ---------------------------------------------------------------------------

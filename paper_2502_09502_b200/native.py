@@ -66,6 +66,7 @@ _PROTOS = {
     "l0_problem_set_workspace": (c_i32, [c_vp, c_vp, c_u64]),
     "l0_problem_destroy": (c_i32, [c_vp]),
     "l0_problem_set_comm": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
+    "l0_nccl_unique_id": (c_i32, [c_vp]),
     "l0_fista_solve": (c_i32, [c_vp, c_i64, c_f64, c_f64, ctypes.POINTER(FistaOpts),
                                ctypes.POINTER(Node), c_vp, c_vp, ctypes.POINTER(Report), TRACE_CB,
                                c_vp, c_vp]),
