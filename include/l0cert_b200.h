@@ -74,8 +74,8 @@ typedef struct l0_fista_opts {
   double gap_tolerance_rel;     /* also stop when gap <= rel * |primal| (0: off) */
   int32_t stop_on_gap;          /* 0: fixed-iteration mode (no gap stop) */
   int32_t chunk_iterations;     /* iterations per captured CUDA graph (0: auto) */
-  int32_t profile;              /* 1: time K1/K2/K3 with CUDA events (report fields) */
-  int32_t reserved;
+  int32_t profile;              /* 1: time the kernels with CUDA events (report fields) */
+  int32_t engine_path;          /* 0 auto (single pass when it fits), 1 two-pass, 2 single pass */
 } l0_fista_opts;
 
 /* NodeState (model.py:119-149): host index arrays, sorted unique, disjoint. */
@@ -100,9 +100,12 @@ typedef struct l0_report {
   double wall_time;             /* fista.py:73 */
   int64_t gpu_launches;         /* kernels launched by the solve */
   int64_t topk_fallbacks;       /* envelope top-k window misses (diagnostic) */
-  double k1_ms, k2_ms, k3_ms;   /* profile: summed kernel time (CUDA events) */
+  double k1_ms, k2_ms, k3_ms;   /* profile: summed kernel time (CUDA events); single-pass
+                                   engine: k2 = the fused pass, k1 = reduce + epilogue */
   int64_t k1_count, k2_count, k3_count;
   int64_t prox_full_passes;     /* iterations whose prox window needed full key passes */
+  int32_t single_pass;          /* 1: iterations read X once (fused kernel) */
+  int32_t cluster_size;         /* CTAs per thread-block cluster of the fused kernel */
 } l0_report;
 
 typedef struct l0_trace_record {

@@ -43,7 +43,7 @@ struct EngineArgs {
   double* u;         // ring [3][n]
   double* gam;       // gamma after the gradient step [pv]
   double* key;       // sort keys |rho*gamma| (or -1 for fixed coords) [pv]
-  double* gv;        // [g (pv) | v = X^T zeta (pv) | F* acc (4) | loss, bad (2)] — one all-reduce
+  double* gv;        // [g (pv) | v = X^T zeta (pv) | F* acc (4) | loss, bad (2) | pad (2) | g_norestart (pv)]
   double* k2_part;   // [2][k2_chunks][pv]
   double* k2_fpart;  // [k2_chunks][4]
   double* u_part;    // [k1_slabs][n]
@@ -72,6 +72,13 @@ struct EngineArgs {
   const Params* prm;
   int multi;         // row-sharded: global epilogues run as separate kernels
   int plain_rhs2;    // PLAIN K2: number of RHS columns
+  // single-physical-pass kernel (fused.cu): clusters of fz_cs CTAs span a row
+  int fused;         // 1: iterations run K3 -> KF -> KR instead of K2 -> K3 -> K1
+  int fz_cs, fz_ncl, fz_nv, fz_rows;   // cluster size, clusters, vectors/thread, rows/tile
+  int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)
+  int64_t fz_tiles;  // row tiles
+  double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta)
+  double* fz_cpart;  // [fz_ncl][8] per-cluster loss, non-finite, F* sums
   int prox_full_sort; // 1: K3 sorts all p keys (reference check path); 0: windowed sort
   // PLAIN-mode vectors
   const double* in_vec;
@@ -89,6 +96,7 @@ __device__ __forceinline__ unsigned* cnt_k1_exit(const EngineArgs& a) { return a
 __device__ __forceinline__ unsigned* cnt_k1_all(const EngineArgs& a) { return a.cnt + 5; }
 __device__ __forceinline__ unsigned* cnt_k2_slab(const EngineArgs& a) { return a.cnt + 8; }
 __device__ __forceinline__ unsigned* cnt_k1_chunk(const EngineArgs& a) { return a.cnt + 8 + a.k2_slabs; }
+__device__ __forceinline__ unsigned* cnt_fused(const EngineArgs& a) { return a.cnt + 6; }
 inline int64_t counter_words(int k2_slabs, int k1_chunks) { return 8 + k2_slabs + k1_chunks; }
 
 __device__ __forceinline__ int64_t ring(int64_t t) { return ((t % 3) + 3) % 3; }
@@ -109,6 +117,10 @@ cudaError_t launch_grad_step(const EngineArgs& a, cudaStream_t s);
 int k1_blocks_per_sm(int dtype);
 int k2_blocks_per_sm(int dtype);
 cudaError_t launch_objective(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_fused(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_fused_reduce(const EngineArgs& a, int mode, cudaStream_t s);
+cudaError_t launch_fused_pick(const EngineArgs& a, cudaStream_t s);
+int fused_plan(EngineArgs& a, int sms);   // 0: the problem does not fit the fused kernel
 cudaError_t launch_prox_iter(const EngineArgs& a, void* sort_tmp, size_t sort_tmp_bytes,
                              cudaStream_t s);
 size_t prox_sort_tmp_bytes(int64_t p);

@@ -98,6 +98,7 @@ struct Problem {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_chunk[2] = {nullptr, nullptr};
   Graph graph[2];
+  int fused_planned = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
 };
@@ -132,6 +133,9 @@ static int compute_layout(Problem& P) {
   a.k2_rows = ceil_div(n, chunks);
   a.k2_chunks = (int)ceil_div(n, a.k2_rows);
   a.k2_grid = (int)std::min<int64_t>(k2_res, (int64_t)a.k2_slabs * a.k2_chunks);
+  a.fused = fused_plan(a, sms) ? 1 : 0;
+  P.fused_planned = a.fused;
+  if (!a.fused) { a.fz_ncl = 1; a.fz_cs = 1; }
   P.sort_tmp_bytes = std::max(prox_sort_tmp_bytes(std::max<int64_t>(p, 1)), (size_t)256);
   size_t keys_only = 0;
   cub::DeviceRadixSort::SortKeysDescending<double>(nullptr, keys_only, (const double*)nullptr,
@@ -160,7 +164,7 @@ static uint64_t carve(Problem& P, char* base) {
   a.xs = (double*)take(8ull * pv);
   a.tail = (double*)take(8ull * pv);
   a.scratch = (double*)take(8ull * pv);
-  a.gv = (double*)take(8ull * (2 * pv + 8));
+  a.gv = (double*)take(8ull * (3 * pv + 8));
   a.k2_part = (double*)take(8ull * 2 * a.k2_chunks * pv);
   a.k2_fpart = (double*)take(8ull * 4 * a.k2_chunks);
   a.u_part = (double*)take(8ull * a.k1_slabs * n);
@@ -178,6 +182,8 @@ static uint64_t carve(Problem& P, char* base) {
   a.slab_below = (double*)take(8ull * S);
   a.slab_hfone = (double*)take(8ull * S);
   a.slab_htop = (double*)take(8ull * S * kHTop);
+  a.fz_part = (double*)take(8ull * 3 * (uint64_t)std::max(a.fz_ncl, 1) * pv);
+  a.fz_cpart = (double*)take(8ull * 8 * (uint64_t)std::max(a.fz_ncl, 1));
   P.d_mask = (uint8_t*)take(pv);
   P.d_fone = (int*)take(4ull * pv);
   P.sort_tmp = take(P.sort_tmp_bytes);
@@ -196,9 +202,38 @@ static void destroy_graphs(Problem& P) {
   }
 }
 
+static int fused_tail(Problem& P, int mode, cudaStream_t s) {
+  EngineArgs& a = P.a;
+  L0_CUDA_TRY(launch_fused_reduce(a, mode, s));
+  if (a.multi) {
+    if (P.comm) {
+      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)(3 * a.pv + 8), ncclDouble, ncclSum,
+                                        P.comm, s);
+      if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (fused) failed");
+    }
+    L0_CUDA_TRY(launch_objective(a, mode, s));
+    L0_CUDA_TRY(launch_fused_pick(a, s));
+  }
+  return ST_OK;
+}
+
 // one FISTA iteration's launches (captured into the chunk graph)
 static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
   EngineArgs& a = P.a;
+  if (a.fused) {
+    // K3 (prox of t) -> KF (single pass over X: u_t and both next gradients) -> KR
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
+    L0_CUDA_TRY(launch_prox_iter(a, P.sort_tmp, P.sort_tmp_bytes, s));
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
+    L0_CUDA_TRY(launch_fused(a, MODE_ITER, s));
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[4], s, cudaEventRecordExternal));
+    int rc = fused_tail(P, MODE_ITER, s);
+    if (rc) return rc;
+    if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[5], s, cudaEventRecordExternal));
+    return ST_OK;
+  }
   if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
   L0_CUDA_TRY(launch_k2(a, MODE_ITER, s));
   if (a.multi) {
@@ -370,7 +405,7 @@ int32_t l0_problem_set_workspace(l0_problem* P, void* d_ws, uint64_t bytes) {
   carve(*P, (char*)d_ws);
   EngineArgs& a = P->a;
   L0_CUDA_TRY(cudaMemsetAsync(a.cnt, 0, 4 * counter_words(a.k2_slabs, a.k1_chunks), P->stream));
-  L0_CUDA_TRY(cudaMemsetAsync(a.gv, 0, 8 * (2 * a.pv + 8), P->stream));
+  L0_CUDA_TRY(cudaMemsetAsync(a.gv, 0, 8 * (3 * a.pv + 8), P->stream));
   k_iota<<<(int)std::min<int64_t>(ceil_div(a.pv, 256), 1024), 256, 0, P->stream>>>(a.iota, a.pv);
   L0_CUDA_TRY(cudaGetLastError());
   L0_CUDA_TRY(cudaStreamSynchronize(P->stream));
@@ -518,6 +553,13 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   hp.stop_on_gap = o->stop_on_gap ? 1 : 0;
   hp.node_mode = node_mode ? 1 : 0;
   hp.loss = a.loss;
+  // engine path: auto = two-pass (measured faster on B200); the
+  // single physical pass (fused) is opt-in while it is being tuned
+  const int want_fused = (o->engine_path == 2) ? P->fused_planned : 0;
+  if (o->engine_path == 2 && !P->fused_planned)
+    return set_error(ST_UNSUPPORTED, "the single-pass kernel does not fit this problem");
+  if (want_fused != a.fused) destroy_graphs(*P);
+  a.fused = want_fused;
   // the captured graphs always see the node buffers; Params::node_mode gates their use
   a.mask = P->d_mask;
   a.fone = P->d_fone;
@@ -550,14 +592,22 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     L0_CUDA_TRY(cudaMemsetAsync(a.beta, 0, vb, s));
     L0_CUDA_TRY(cudaMemsetAsync(a.beta + 2 * a.pv, 0, vb, s));
   }
-  L0_CUDA_TRY(launch_k1(a, MODE_INIT, s));  // u_0 = X beta_0, F(u_0), objective
-  ++launches;
-  if (a.multi) {
-    if (P->comm && g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
-                                    ncclSum, P->comm, s) != ncclSuccess)
-      return set_error(ST_CUDA, "ncclAllReduce (initial loss) failed");
-    L0_CUDA_TRY(launch_objective(a, MODE_INIT, s));
+  if (a.fused) {
+    // u_0 = X beta_0, F(u_0), objective, and the first gradient (fista.py:141-143, :162)
+    L0_CUDA_TRY(launch_fused(a, MODE_INIT, s));
+    rc = fused_tail(*P, MODE_INIT, s);
+    if (rc) return rc;
+    launches += a.multi ? 4 : 2;
+  } else {
+    L0_CUDA_TRY(launch_k1(a, MODE_INIT, s));  // u_0 = X beta_0, F(u_0), objective
     ++launches;
+    if (a.multi) {
+      if (P->comm && g_nccl.allReduce(a.gv + 2 * a.pv + 4, a.gv + 2 * a.pv + 4, 2, ncclDouble,
+                                      ncclSum, P->comm, s) != ncclSuccess)
+        return set_error(ST_CUDA, "ncclAllReduce (initial loss) failed");
+      L0_CUDA_TRY(launch_objective(a, MODE_INIT, s));
+      ++launches;
+    }
   }
 
   // ---- chunked iteration: graph replays, double-buffered state mirrors ------
@@ -633,6 +683,11 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
       k_request_stop<<<1, 1, 0, s>>>(a.st, P->d_prm, TERM_TIME_LIMIT);
       L0_CUDA_TRY(cudaGetLastError());
       ++launches;
+      if (a.fused) {  // the final bound pass needs the Huber values of zeta_t
+        rc = fused_tail(*P, MODE_ITER, s);
+        if (rc) return rc;
+        ++launches;
+      }
       stop_sent = true;
     }
     rc = launch_chunk(w);
@@ -657,6 +712,8 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   rep->error_iteration = h->err_iter;
   rep->topk_fallbacks = h->topk_fallbacks;
   rep->prox_full_passes = h->slow_prox;
+  rep->single_pass = a.fused;
+  rep->cluster_size = a.fused ? a.fz_cs : 0;
   L0_CUDA_TRY(cudaMemcpyAsync(d_beta_out, a.beta + ((h->t % 3)) * a.pv, vb,
                               cudaMemcpyDeviceToDevice, s));
   L0_CUDA_TRY(cudaEventRecord(P->ev_out, s));

@@ -3,6 +3,7 @@
 #include "gemv.cu"
 #include "prox.cu"
 #include "prox_window.cu"
+#include "fused.cu"
 #include "ops.cu"
 #include "engine_host.cu"
 #include "abi_ops.cu"

@@ -57,7 +57,8 @@ class FistaOptions:
     gap_tolerance_rel: float = 0.0      # also stop at gap <= rel * |primal|
     stop_on_gap: bool = True            # False: fixed-iteration runs
     chunk_iterations: int = 0           # iterations per CUDA graph replay (0: auto)
-    profile: bool = False               # time K1/K2/K3 with CUDA events
+    profile: bool = False               # time the kernels with CUDA events
+    engine_path: str = "auto"           # "auto" | "two_pass" | "single_pass"
 
     def __post_init__(self):
         if self.gap_tolerance <= 0:
@@ -66,6 +67,8 @@ class FistaOptions:
             raise InvalidInputError("bound_check_interval must be >= 1")
         if self.max_iterations < 1:
             raise InvalidInputError("max_iterations must be >= 1")
+        if self.engine_path not in ("auto", "two_pass", "single_pass"):
+            raise InvalidInputError("engine_path must be 'auto', 'two_pass' or 'single_pass'")
 
 
 @dataclass
@@ -130,6 +133,7 @@ def solve_relaxation(instance: ProblemInstance, node: Optional[NodeState] = None
     o.stop_on_gap = 1 if opts.stop_on_gap else 0
     o.chunk_iterations = int(opts.chunk_iterations)
     o.profile = 1 if opts.profile else 0
+    o.engine_path = {"auto": 0, "two_pass": 1, "single_pass": 2}[opts.engine_path]
 
     nd = None
     keep = []
@@ -173,6 +177,7 @@ def solve_relaxation(instance: ProblemInstance, node: Optional[NodeState] = None
     beta = beta_out if return_device else beta_out.cpu().numpy()
     stats = {"gpu_launches": int(rep.gpu_launches), "topk_fallbacks": int(rep.topk_fallbacks),
              "prox_full_passes": int(rep.prox_full_passes),
+             "single_pass": bool(rep.single_pass), "cluster_size": int(rep.cluster_size),
              "lipschitz": float(L)}
     if opts.profile:
         stats.update(k1_ms=rep.k1_ms, k2_ms=rep.k2_ms, k3_ms=rep.k3_ms, k1_count=rep.k1_count,

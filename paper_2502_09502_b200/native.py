@@ -32,7 +32,7 @@ class FistaOpts(ctypes.Structure):
                 ("early_primal_cutoff", c_f64), ("early_dual_cutoff", c_f64),
                 ("bound_check_interval", c_i32), ("restart", c_i32), ("lipschitz", c_f64),
                 ("gap_tolerance_rel", c_f64), ("stop_on_gap", c_i32),
-                ("chunk_iterations", c_i32), ("profile", c_i32), ("reserved", c_i32)]
+                ("chunk_iterations", c_i32), ("profile", c_i32), ("engine_path", c_i32)]
 
 
 class Node(ctypes.Structure):
@@ -47,7 +47,8 @@ class Report(ctypes.Structure):
                 ("status", c_i32), ("error_iteration", c_i64), ("wall_time", c_f64),
                 ("gpu_launches", c_i64), ("topk_fallbacks", c_i64), ("k1_ms", c_f64),
                 ("k2_ms", c_f64), ("k3_ms", c_f64), ("k1_count", c_i64), ("k2_count", c_i64),
-                ("k3_count", c_i64), ("prox_full_passes", c_i64)]
+                ("k3_count", c_i64), ("prox_full_passes", c_i64), ("single_pass", c_i32),
+                ("cluster_size", c_i32)]
 
 
 class TraceRecord(ctypes.Structure):
