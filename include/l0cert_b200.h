@@ -179,6 +179,37 @@ int32_t l0_loss_conjugate(int32_t loss, const double* d_zeta, const double* d_y,
 int32_t l0_all_finite(const void* d_x, int32_t dtype, int64_t rows, int64_t cols, int64_t ld,
                       int32_t* h_ok, void* d_ws, uint64_t ws_bytes, void* stream);
 
+/* ---- batched node contraction (tcgen05 tensor cores) ----------------------
+ * The batched engine's GEMM, exposed for verification: C_s = A B^T over K
+ * split s (s = 0..S-1), A M x K (pitch lda), B N x K (pitch ldb), fp64 or fp32
+ * inputs, computed as 3xTF32 (hi/lo TF32 operand split, fp32 accumulation in
+ * TMEM).  C is S x N x ldc fp32 (ldc >= M; partial sums per split).  splits=0
+ * lets the engine choose S (returned in *h_splits).  Replaces the numpy
+ * X @ Gamma / X.T @ R products of a batch of node solves (fista.py:162, :165). */
+/* Batched node relaxations on one shared X (the BnB caller's node batches,
+ * SPEC.md:294-357; per node exactly l0_fista_solve / fista.py:76-222 with that
+ * node's NodeState, cold start).  The two X passes of an iteration are tcgen05
+ * contractions over all nodes in 3xTF32, so per-node results carry fp32-class
+ * rounding (tolerance 1e-5 relative) whatever the problem's dtype.
+ * l0_batch_set_workspace pre-splits X (and X^T) into TF32 hi/lo operands, so
+ * X must not change while the batch exists.  Nodes advance in lockstep; a
+ * finished node is frozen.  d_beta_out is n_nodes x p (row per node); reps
+ * has n_nodes entries.  Trace callbacks are not available in batched mode. */
+typedef struct l0_batch l0_batch;
+int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out);
+int32_t l0_batch_workspace_bytes(const l0_batch* batch, uint64_t* bytes);
+int32_t l0_batch_set_workspace(l0_batch* batch, void* d_ws, uint64_t bytes);
+int32_t l0_batch_solve(l0_batch* batch, int64_t k, double M, double lambda2,
+                       const l0_fista_opts* opts, const l0_node* nodes /* n_nodes, nullable */,
+                       double* d_beta_out, l0_report* reps, void* stream);
+int32_t l0_batch_destroy(l0_batch* batch);
+
+uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                          const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
+                          int64_t ldc, int32_t splits, int32_t* h_splits, void* d_ws,
+                          uint64_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,413 @@
+// Batched node engine kernels: B branch-and-bound node relaxations on one
+// shared X (north star item 4).  The per-node arithmetic
+// is the single-solve engine's (fista.py:159-212 per node, with that node's
+// fixed-one / fixed-zero sets); the two X passes of every iteration become
+// tensor-core contractions (tc_gemm.cu) over all nodes at once:
+//
+//   kb_rhs   : R = grad F(U + c (U - U_prev)) per node (and Z = -grad F(U) on
+//              bound checks), split hi/lo for 3xTF32; F* partials
+//   kb_plan  : which node rows the transpose contraction needs
+//   GEMM_T   : Ct = X^T [R | Z]             (p x 2B, split-K partials)
+//   kb_prox  : per node (one CTA): gradient step, bound check, prox, g(beta+),
+//              beta+ split hi/lo for the forward contraction
+//   GEMM_F   : Cf = X beta+                 (n x B, split-K partials)
+//   kb_obj   : per node: u = sum of partials, F(u), objective / restart
+//
+// Node-major layouts everywhere ([node][coordinate], [node][row]) so that one
+// node's vectors are contiguous and the contractions' B operands are K-major.
+#include <cub/block/block_radix_sort.cuh>
+
+#include "batch_ops.cuh"
+#include "control.cuh"
+#include "engine.cuh"
+#include "prox.cuh"
+
+namespace l0 {
+
+struct BatchArgs {
+  int64_t n, p, B;
+  int64_t pv;       // stride of per-node fp64 p-vectors
+  int64_t pp;       // pitch of the fp32 split p-vectors (K of GEMM_F)
+  int64_t nn;       // pitch of per-node row vectors (K of GEMM_T)
+  int loss;
+  const double* y;
+  State* st;        // [B]
+  Params* prm;      // [B]
+  double* beta;     // [B][3][pv] ring per node
+  double* gam;      // [B][pv]
+  double* key;      // [B][pv]
+  double* xs;       // [B][pv]
+  double* tail;     // [B][pv]
+  double* scratch;  // [B][pv]
+  int* perm;        // [B][pv]
+  double* gv;       // [B][3 pv + 8]
+  uint8_t* mask;    // [B][pv]
+  int* fone;        // [B][fone_stride]
+  int64_t fone_stride;
+  float* bh;        // [B][pp]  beta+ split (GEMM_F B operand)
+  float* bl;
+  float* rh;        // [2B][nn] R | Z split (GEMM_T B operand)
+  float* rl;
+  float* cf;        // [sf][B][nn]
+  int sf;
+  float* ct;        // [st][2B][pp]
+  int sct;
+  double* u;        // [3][B][nn]
+  double* fpart;    // [B][rblocks][4]
+  double* lpart;    // [B][rblocks][2]
+  unsigned* cnt;    // [B] (zero between launches)
+  int* flags;       // [0] alive, [1] any zeta, [2] GEMM_T rows, [3] GEMM_F rows, [4] done count
+  int rblocks;      // row blocks of kb_rhs / kb_obj
+};
+
+constexpr int kRowThreads = 256;
+constexpr int kRowsPerBlock = 2048;
+// u_{t} = u_{t-1} + X (beta_t - beta_{t-1}) between re-syncs u_t = X beta_t:
+// the contraction's fp32-class error then scales with the step, not with u,
+// so the restart test F(u_t) + ... >= previous (fista.py:168) sees accurate
+// differences; every kResync iterations u is recomputed from beta_t.
+constexpr int64_t kResync = 40;
+__device__ __forceinline__ bool resync_at(int64_t t) { return t % kResync == 0; }
+
+__device__ __forceinline__ int64_t gvs(const BatchArgs& g) { return 3 * g.pv + 8; }
+
+__global__ void kb_state_init(BatchArgs g) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.B) return;
+  State* st = g.st + b;
+  st->t = 0;
+  st->restarts = 0;
+  st->err_iter = 0;
+  st->trace_count = 0;
+  st->phi = 1;
+  st->done = 0;
+  st->termination = TERM_ITERATION_LIMIT;
+  st->err = ST_OK;
+  st->dual_pending = 0;
+  st->check_pending = 0;
+  st->dual_only = 0;
+  st->stop_term = -1;
+  st->last_restarted = 0;
+  st->topk_fallbacks = 0;
+  st->obj = 0.0;
+  st->g_next = 0.0;
+  st->best_dual = g.prm[b].parent_bound;
+  st->gap = CUDART_NAN;
+  st->last_dual = CUDART_NAN;
+  st->loss_cur = 0.0;
+  st->theta = 0.0;
+  st->slow_prox = 0;
+}
+
+// R / Z rows of node blockIdx.y for rows [blockIdx.x * kRowsPerBlock, ...)
+__global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
+  __shared__ double red[32];
+  const int64_t b = blockIdx.y;
+  State* st = g.st + b;
+  if (st->done) return;
+  const bool wz = st->dual_pending != 0;
+  const bool wg = st->dual_only == 0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (wg || wz) atomicOr(g.flags + 0, 1);
+    if (wz) atomicOr(g.flags + 1, 1);
+  }
+  const int64_t t = st->t + 1;
+  const double c = momentum(st->phi);
+  const int64_t n = g.n, nn = g.nn, B = g.B;
+  const double* ucur = g.u + (ring(t - 1) * B + b) * nn;
+  const double* uprev = g.u + (ring(t - 2) * B + b) * nn;
+  double facc[3] = {0.0, 0.0, 0.0};
+  int bad = 0;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int64_t r1 = min(n, r0 + kRowsPerBlock);
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
+    const double uc = ucur[i];
+    const double yi = g.y[i];
+    if (wg) {
+      // X gamma = u_t + c (u_t - u_{t-1})   (linearity; fista.py:161-162)
+      const double ug = dadd(uc, dmul(c, dsub(uc, uprev[i])));
+      if (!isfinite(ug)) bad = 1;
+      float h, l;
+      tf32_split(loss_grad(g.loss, ug, yi), h, l);
+      g.rh[b * nn + i] = h;
+      g.rl[b * nn + i] = l;
+    }
+    if (wz) {
+      const double z = -loss_grad(g.loss, uc, yi);  // zeta = -grad F(u) (fista.py:152)
+      float h, l;
+      tf32_split(z, h, l);
+      g.rh[(B + b) * nn + i] = h;
+      g.rl[(B + b) * nn + i] = l;
+      conj_accumulate(g.loss, z, yi, facc);
+    }
+  }
+  if (wz) {
+    const double f0 = block_sum(facc[0], red);
+    const double f1 = block_sum(facc[1], red);
+    const double f2 = block_sum(facc[2], red);
+    if (threadIdx.x == 0) {
+      double* fp = g.fpart + (b * g.rblocks + blockIdx.x) * 4;
+      fp[0] = f0;
+      fp[1] = f1;
+      fp[2] = f2;
+    }
+  }
+  if (wg && bad) {
+    // loss_gradient on non-finite predictions: model.py:215 -> InvalidInputError
+    atomicExch(&st->err, (int)ST_INVALID);
+    st->err_iter = t;
+    st->done = 1;
+  }
+}
+
+__global__ void kb_plan(BatchArgs g) {
+  const int alive = g.flags[0], anyz = g.flags[1];
+  g.flags[2] = alive ? (int)(anyz ? 2 * g.B : g.B) : 0;
+  g.flags[3] = alive ? (int)g.B : 0;
+  g.flags[0] = 0;
+  g.flags[1] = 0;
+}
+
+__device__ __forceinline__ EngineArgs node_view(const BatchArgs& g, int64_t b) {
+  EngineArgs a{};
+  a.n = g.n;
+  a.p = g.p;
+  a.pv = g.pv;
+  a.loss = g.loss;
+  a.st = g.st + b;
+  a.prm = g.prm + b;
+  a.beta = g.beta + b * 3 * g.pv;
+  a.gam = g.gam + b * g.pv;
+  a.key = g.key + b * g.pv;
+  a.xs = g.xs + b * g.pv;
+  a.tail = g.tail + b * g.pv;
+  a.scratch = g.scratch + b * g.pv;
+  a.perm = g.perm + b * g.pv;
+  a.gv = g.gv + b * gvs(g);
+  a.mask = g.mask + b * g.pv;
+  a.fone = g.fone + b * g.fone_stride;
+  return a;
+}
+
+// one CTA per node: gradient step, bound check, prox (full sort of the free
+// keys, PAVA), g(beta+), split of beta+ for GEMM_F
+template <int T, int IPT>
+__global__ void __launch_bounds__(T, 1) kb_prox(BatchArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Sort = cub::BlockRadixSort<double, T, IPT, int, 6>;
+  ProxSmem& sm = *reinterpret_cast<ProxSmem*>(smem_raw);
+  typename Sort::TempStorage& tmp =
+      *reinterpret_cast<typename Sort::TempStorage*>(smem_raw + sizeof(ProxSmem));
+  const int64_t b = blockIdx.x;
+  const EngineArgs a = node_view(g, b);
+  State* st = a.st;
+  if (st->done) return;
+  const Params* P = a.prm;
+  const bool wz = st->dual_pending != 0;
+  const bool wg = st->dual_only == 0;
+  const int64_t t = st->t + 1;
+  const double c = momentum(st->phi);
+  const int64_t p = g.p, pv = g.pv, B = g.B;
+  const int tid = threadIdx.x;
+  if (wz) {
+    // v = X^T zeta (split-K partials, fixed order) and the F* sums over row blocks
+    for (int64_t j = tid; j < p; j += T) {
+      double v = 0.0;
+      for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(g.ct + s * (2 * B * g.pp) + (B + b) * g.pp + j);
+      a.gv[pv + j] = v;
+    }
+    if (tid == 0) {
+      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      for (int r = 0; r < g.rblocks; ++r) {
+        const double* fp = g.fpart + (b * g.rblocks + r) * 4;
+        f0 += fp[0];
+        f1 += fp[1];
+        f2 += fp[2];
+      }
+      a.gv[2 * pv + 0] = f0;
+      a.gv[2 * pv + 1] = f1;
+      a.gv[2 * pv + 2] = f2;
+    }
+  }
+  double keys[IPT];
+  int ids[IPT];
+  if (wg) {
+    // gradient step (fista.py:161-163) and sort keys |rho gamma| (prox.py:106-111)
+    const double* b1 = a.beta + ring(t - 1) * pv;
+    const double* b2 = a.beta + ring(t - 2) * pv;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t j = (int64_t)tid * IPT + i;
+      ids[i] = (int)j;
+      keys[i] = -CUDART_INF;
+      if (j < p) {
+        double gsum = 0.0;
+        for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(g.ct + s * (2 * B * g.pp) + b * g.pp + j);
+        double gam = dadd(b1[j], dmul(c, dsub(b1[j], b2[j])));
+        gam = dsub(gam, ddiv(gsum, P->L));
+        a.gam[j] = gam;
+        const int cls = P->node_mode ? a.mask[j] : FREE;
+        keys[i] = (cls == FREE) ? fabs(dmul(P->rho, gam)) : -1.0;
+      }
+    }
+  }
+  __syncthreads();
+  if (wz) {
+    if (dual_step(a, sm)) return;
+  }
+  if (st->dual_only) return;
+  Sort(tmp).SortDescending(keys, ids);  // stable: ties keep ascending ids (prox.py:111)
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t pos = (int64_t)tid * IPT + i;
+    if (pos < p) {
+      a.xs[pos] = keys[i];
+      a.perm[pos] = ids[i];
+    }
+  }
+  __syncthreads();
+  PostArgs q;
+  q.p = p;
+  q.nf = P->node_mode ? P->n_free : p;
+  q.kk = P->node_mode ? P->k_rem : P->k;
+  q.kg = P->node_mode ? P->k_g : P->k;
+  q.rho = P->rho;
+  q.M = P->M;
+  q.xs = a.xs;
+  q.perm = a.perm;
+  q.tail = a.tail;
+  q.in = a.gam;
+  q.out = a.beta + ring(t) * pv;
+  q.absb = a.scratch;
+  q.mask = P->node_mode ? a.mask : nullptr;
+  q.fone = P->node_mode ? a.fone : nullptr;
+  q.n_fone = P->n_fone;
+  q.gmode = 1;
+  q.want_g = 1;
+  q.g_out = &st->g_next;
+  q.st = st;
+  prox_post_sort<T>(q, sm);
+  __syncthreads();
+  // beta+ (re-sync) or beta+ - beta_t -> hi/lo operand rows of the forward contraction
+  const bool full = resync_at(t);
+  const double* bprev = a.beta + ring(t - 1) * pv;
+  for (int64_t j = tid; j < g.pp; j += T) {
+    float h = 0.f, l = 0.f;
+    if (j < p) tf32_split(full ? q.out[j] : dsub(q.out[j], bprev[j]), h, l);
+    g.bh[b * g.pp + j] = h;
+    g.bl[b * g.pp + j] = l;
+  }
+}
+
+// u = X beta+ (sum of split-K partials, fixed order), F(u), objective
+__global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
+  __shared__ double red[32];
+  __shared__ int s_last;
+  const int64_t b = blockIdx.y;
+  State* st = g.st + b;
+  if (mode == MODE_ITER && (st->done || st->dual_only)) return;
+  if (mode == MODE_INIT && st->done) return;
+  const int64_t t = mode == MODE_ITER ? st->t + 1 : 0;
+  const int64_t n = g.n, nn = g.nn, B = g.B;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int64_t r1 = min(n, r0 + kRowsPerBlock);
+  double lsum = 0.0;
+  int bad = 0;
+  const bool delta = mode == MODE_ITER && !resync_at(t);
+  const double* uprev = g.u + (ring(t - 1) * B + b) * nn;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
+    double u = 0.0;
+    for (int s = 0; s < g.sf; ++s) u += (double)g.cf[s * (B * nn) + b * nn + i];
+    if (delta) u = dadd(uprev[i], u);
+    if (mode == MODE_ITER) {
+      g.u[(ring(t) * B + b) * nn + i] = u;
+    } else {
+      g.u[(0 * B + b) * nn + i] = u;
+      g.u[(2 * B + b) * nn + i] = u;
+    }
+    if (!isfinite(u)) bad = 1;
+    lsum += loss_term(g.loss, u, g.y[i]);
+  }
+  const double csum = block_sum(lsum, red);
+  const int anybad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    double* lp = g.lpart + (b * g.rblocks + blockIdx.x) * 2;
+    lp[0] = csum;
+    lp[1] = anybad ? 1.0 : 0.0;
+    __threadfence();
+    s_last = atomicAdd(g.cnt + b, 1u) == (unsigned)(gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  g.cnt[b] = 0u;
+  double tot = 0.0, nb = 0.0;
+  for (int r = 0; r < (int)gridDim.x; ++r) {
+    const double* lp = g.lpart + (b * g.rblocks + r) * 2;
+    tot += __ldcg(lp);
+    nb += __ldcg(lp + 1);
+  }
+  const Params* P = g.prm + b;
+  if (nb > 0.0) {  // loss_value on non-finite predictions (model.py:152-161)
+    st->err = ST_INVALID;
+    st->err_iter = t;
+    if (mode == MODE_ITER) st->t = t;
+    st->done = 1;
+  } else if (mode == MODE_ITER) {
+    objective_update(st, P, tot);
+  } else {
+    st->loss_cur = tot;
+    st->obj = dadd(tot, dmul(P->two_l2, st->g_next));  // fista.py:143
+  }
+}
+
+// nodes finished -> flags[4]
+__global__ void kb_count(BatchArgs g) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int local = 0;
+  for (int64_t b = threadIdx.x; b < g.B; b += blockDim.x) local += g.st[b].done ? 1 : 0;
+  atomicAdd(&cnt, local);
+  __syncthreads();
+  if (threadIdx.x == 0) g.flags[4] = cnt;
+}
+
+__global__ void kb_request_stop(BatchArgs g, int term) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.B) return;
+  State* st = g.st + b;
+  const Params* P = g.prm + b;
+  if (st->done) return;
+  if (st->check_pending) {
+    if (st->stop_term < 0) st->stop_term = term;
+    st->dual_only = 1;
+  } else {
+    request_stop(st, P, term);
+  }
+}
+
+template <int T, int IPT>
+static size_t kb_prox_smem() {
+  return sizeof(ProxSmem) + sizeof(typename cub::BlockRadixSort<double, T, IPT, int, 6>::TempStorage);
+}
+
+template <int T, int IPT>
+static cudaError_t kb_prox_launch_t(const BatchArgs& g, cudaStream_t s) {
+  const size_t smem = kb_prox_smem<T, IPT>();
+  cudaError_t e = cudaFuncSetAttribute(kb_prox<T, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kb_prox<T, IPT><<<(unsigned)g.B, T, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+// p capacity of the per-node sort
+inline int64_t kb_prox_capacity() { return 1024 * 16; }
+
+cudaError_t kb_prox_launch(const BatchArgs& g, cudaStream_t s) {
+  if (g.p <= 2048) return kb_prox_launch_t<256, 8>(g, s);
+  if (g.p <= 8192) return kb_prox_launch_t<512, 16>(g, s);
+  return kb_prox_launch_t<1024, 16>(g, s);
+}
+
+}  // namespace l0

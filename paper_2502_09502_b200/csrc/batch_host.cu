@@ -1,0 +1,484 @@
+// Host side of the batched node engine (SURVEY.md §8(a) a6 batched, north
+// star item 4): many branch-and-bound node relaxations on one shared X,
+// advanced in lockstep by CUDA graphs of G iterations; the two X passes of an
+// iteration are tcgen05 contractions over all nodes (tc_gemm.cu).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "batch_ops.cuh"
+#include "tc_gemm.cuh"
+#include "l0cert_b200.h"
+
+namespace l0 {
+
+struct Batch {
+  const l0_problem* prob = nullptr;
+  BatchArgs g{};
+  int64_t n = 0, p = 0, B = 0;
+  int sms = 148;
+  uint64_t ws_bytes = 0;
+  void* ws = nullptr;
+  float *xh = nullptr, *xl = nullptr, *xth = nullptr, *xtl = nullptr;
+  TcGemmArgs gf{}, gt{};
+  CUtensorMap m_xh{}, m_xl{}, m_xth{}, m_xtl{}, m_bh{}, m_bl{}, m_rh{}, m_rl{};
+  int* h_flags = nullptr;   // pinned mirror of flags[0..8)
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_chunk = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int G = 0;
+  int64_t graph_kernels = 0;
+};
+
+static uint64_t batch_carve(Batch& Bt, char* base) {
+  BatchArgs& g = Bt.g;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) -> char* {
+    off = (off + 1023) & ~uint64_t(1023);
+    char* r = base ? base + off : nullptr;
+    off += bytes;
+    return r;
+  };
+  const int64_t n = g.n, p = g.p, B = g.B, pv = g.pv, pp = g.pp, nn = g.nn;
+  Bt.xh = (float*)take(4ull * n * pp);
+  Bt.xl = (float*)take(4ull * n * pp);
+  Bt.xth = (float*)take(4ull * p * nn);
+  Bt.xtl = (float*)take(4ull * p * nn);
+  g.bh = (float*)take(4ull * B * pp);
+  g.bl = (float*)take(4ull * B * pp);
+  g.rh = (float*)take(4ull * 2 * B * nn);
+  g.rl = (float*)take(4ull * 2 * B * nn);
+  g.cf = (float*)take(4ull * g.sf * B * nn);
+  g.ct = (float*)take(4ull * g.sct * 2 * B * pp);
+  g.u = (double*)take(8ull * 3 * B * nn);
+  g.st = (State*)take(sizeof(State) * B);
+  g.prm = (Params*)take(sizeof(Params) * B);
+  g.beta = (double*)take(8ull * 3 * B * pv);
+  g.gam = (double*)take(8ull * B * pv);
+  g.key = (double*)take(8ull * B * pv);
+  g.xs = (double*)take(8ull * B * pv);
+  g.tail = (double*)take(8ull * B * pv);
+  g.scratch = (double*)take(8ull * B * pv);
+  g.perm = (int*)take(4ull * B * pv);
+  g.gv = (double*)take(8ull * B * (3 * pv + 8));
+  g.mask = (uint8_t*)take(1ull * B * pv);
+  g.fone = (int*)take(4ull * B * g.fone_stride);
+  g.fpart = (double*)take(8ull * 4 * B * g.rblocks);
+  g.lpart = (double*)take(8ull * 2 * B * g.rblocks);
+  g.cnt = (unsigned*)take(4ull * B);
+  g.flags = (int*)take(4ull * 8);
+  return off + 1024;
+}
+
+static void batch_destroy_graph(Batch& Bt) {
+  if (Bt.exec) cudaGraphExecDestroy(Bt.exec);
+  Bt.exec = nullptr;
+  Bt.G = 0;
+}
+
+#define L0_B_TRY(expr)                                                                \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return set_error(ST_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+static int batch_iteration(Batch& Bt, cudaStream_t s) {
+  BatchArgs& g = Bt.g;
+  const dim3 rgrid((unsigned)g.rblocks, (unsigned)g.B);
+  kb_rhs<<<rgrid, kRowThreads, 0, s>>>(g);
+  kb_plan<<<1, 1, 0, s>>>(g);
+  L0_B_TRY(cudaGetLastError());
+  L0_B_TRY(tc_gemm_launch(Bt.m_xth, Bt.m_xtl, Bt.m_rh, Bt.m_rl, Bt.gt, std::min(Bt.gt.units, Bt.sms), s));
+  L0_B_TRY(kb_prox_launch(g, s));
+  L0_B_TRY(tc_gemm_launch(Bt.m_xh, Bt.m_xl, Bt.m_bh, Bt.m_bl, Bt.gf, std::min(Bt.gf.units, Bt.sms), s));
+  kb_obj<<<rgrid, kRowThreads, 0, s>>>(g, MODE_ITER);
+  L0_B_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+static int batch_build_graph(Batch& Bt, int G) {
+  if (Bt.exec && Bt.G == G) return ST_OK;
+  batch_destroy_graph(Bt);
+  cudaStream_t s = Bt.stream;
+  L0_B_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = ST_OK;
+  for (int i = 0; i < G && rc == ST_OK; ++i) rc = batch_iteration(Bt, s);
+  if (rc == ST_OK) {
+    kb_count<<<1, 256, 0, s>>>(Bt.g);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(Bt.h_flags, Bt.g.flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = set_error(ST_CUDA, cudaGetErrorString(e));
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (rc != ST_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return set_error(ST_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+  size_t nn = 0;
+  L0_B_TRY(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  L0_B_TRY(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  e = cudaGraphInstantiate(&Bt.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_error(ST_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+  Bt.G = G;
+  Bt.graph_kernels = kernels;
+  return ST_OK;
+}
+
+__global__ void kb_gather_beta(BatchArgs g, double* out) {
+  const int64_t b = blockIdx.y;
+  const int64_t slot = ring(g.st[b].t);
+  const double* src = g.beta + (b * 3 + slot) * g.pv;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.p; j += (int64_t)gridDim.x * blockDim.x)
+    out[b * g.p + j] = src[j];
+}
+
+}  // namespace l0
+
+struct l0_batch : l0::Batch {};
+
+using namespace l0;
+
+extern "C" {
+
+uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  const int64_t ldk = (K + 31) / 32 * 32;
+  return (uint64_t)(2 * (M + N) * ldk) * 4 + 1024;
+}
+
+int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                          const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
+                          int64_t ldc, int32_t splits, int32_t* h_splits_out, void* d_ws,
+                          uint64_t ws_bytes, void* stream) {
+  if (!d_A || !d_B || !d_C || !d_ws) return set_error(L0_INVALID, "null argument");
+  if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < M)
+    return set_error(L0_INVALID, "bad GEMM shape");
+  if (ws_bytes < l0_tc_gemm_workspace_bytes(M, N, K)) return set_error(L0_INVALID, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ldk = (K + 31) / 32 * 32;
+  char* base = (char*)(((uintptr_t)d_ws + 255) & ~uintptr_t(255));
+  float* ah = (float*)base;
+  float* al = ah + M * ldk;
+  float* bh = al + M * ldk;
+  float* bl = bh + N * ldk;
+  auto split = [&](const void* src, int dt, int64_t rows, int64_t ld, float* h, float* l) {
+    const int blocks = (int)std::min<int64_t>((rows * ldk + 255) / 256, 148 * 16);
+    if (dt == L0_F64)
+      k_split_rows<double><<<blocks, 256, 0, s>>>((const double*)src, rows, K, ld, h, l, ldk);
+    else
+      k_split_rows<float><<<blocks, 256, 0, s>>>((const float*)src, rows, K, ld, h, l, ldk);
+  };
+  split(d_A, a_dtype, M, lda, ah, al);
+  split(d_B, b_dtype, N, ldb, bh, bl);
+  if (cudaGetLastError() != cudaSuccess) return set_error(L0_CUDA, "split kernel launch failed");
+  CUtensorMap m_ah, m_al, m_bh, m_bl;
+  if (tc_make_map(&m_ah, ah, M, K, ldk, kTcBM) || tc_make_map(&m_al, al, M, K, ldk, kTcBM) ||
+      tc_make_map(&m_bh, bh, N, K, ldk, kTcBN) || tc_make_map(&m_bl, bl, N, K, ldk, kTcBN))
+    return set_error(L0_CUDA, "cuTensorMapEncodeTiled failed");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  TcGemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldc = ldc;
+  g.c_split = N * ldc;
+  g.C = d_C;
+  g.n_active = nullptr;
+  tc_gemm_plan(g, sms, splits > 0 ? splits : 32);
+  if (splits > 0) {
+    g.S = splits;
+    g.units = g.S * g.m_tiles * g.n_tiles;
+  }
+  if (h_splits_out) *h_splits_out = g.S;
+  const int grid = std::min(g.units, sms);
+  cudaError_t e = tc_gemm_launch(m_ah, m_al, m_bh, m_bl, g, grid, s);
+  if (e != cudaSuccess) return set_error(L0_CUDA, std::string("tc_gemm: ") + cudaGetErrorString(e));
+  return L0_OK;
+}
+
+int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out) {
+  if (!out || !prob) return set_error(L0_INVALID, "null argument");
+  *out = nullptr;
+  if (n_nodes < 1 || n_nodes > 65535) return set_error(L0_INVALID, "n_nodes must be in [1, 65535]");
+  const EngineArgs& a = prob->a;
+  if (a.p > kb_prox_capacity())
+    return set_error(L0_UNSUPPORTED, "batched nodes support p <= 16384 (per-node on-chip sort)");
+  if (a.n >= (int64_t)INT32_MAX || a.p >= (int64_t)INT32_MAX)
+    return set_error(L0_INVALID, "n and p must fit the tensor-map coordinates");
+  l0_batch* Bt = new l0_batch();
+  Bt->prob = prob;
+  Bt->n = a.n;
+  Bt->p = a.p;
+  Bt->B = n_nodes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&Bt->sms, cudaDevAttrMultiProcessorCount, dev);
+  BatchArgs& g = Bt->g;
+  g.n = a.n;
+  g.p = a.p;
+  g.B = n_nodes;
+  g.pv = (a.p + 31) / 32 * 32;
+  g.pp = g.pv;
+  g.nn = (a.n + 31) / 32 * 32;
+  g.loss = a.loss;
+  g.y = a.y;
+  g.fone_stride = g.pv;
+  g.rblocks = (int)((a.n + kRowsPerBlock - 1) / kRowsPerBlock);
+  // contraction plans: forward M = n, N = B, K = p; transpose M = p, N = 2B
+  // (the zeta rows only on bound checks), K = n, split count planned for N = B
+  TcGemmArgs& gf = Bt->gf;
+  gf.M = a.n; gf.N = n_nodes; gf.K = a.p;
+  tc_gemm_plan(gf, Bt->sms, 32);
+  TcGemmArgs& gt = Bt->gt;
+  gt.M = a.p; gt.N = n_nodes; gt.K = a.n;
+  tc_gemm_plan(gt, Bt->sms, 32);
+  gt.N = 2 * n_nodes;
+  gt.n_tiles = (int)((gt.N + kTcBN - 1) / kTcBN);
+  gt.units = gt.S * gt.m_tiles * gt.n_tiles;
+  g.sf = gf.S;
+  g.sct = gt.S;
+  Bt->ws_bytes = batch_carve(*Bt, nullptr);
+  cudaError_t e = cudaStreamCreateWithFlags(&Bt->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&Bt->ev_in, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&Bt->ev_chunk, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&Bt->h_flags, 8 * sizeof(int));
+  if (e != cudaSuccess) {
+    l0_batch_destroy(Bt);
+    return set_error(L0_CUDA, cudaGetErrorString(e));
+  }
+  *out = Bt;
+  return L0_OK;
+}
+
+int32_t l0_batch_workspace_bytes(const l0_batch* Bt, uint64_t* bytes) {
+  if (!Bt || !bytes) return set_error(L0_INVALID, "null argument");
+  *bytes = Bt->ws_bytes;
+  return L0_OK;
+}
+
+int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
+  if (!Bt || !d_ws) return set_error(L0_INVALID, "null argument");
+  if (bytes < Bt->ws_bytes) return set_error(L0_INVALID, "workspace too small");
+  batch_destroy_graph(*Bt);
+  Bt->ws = d_ws;
+  char* base = (char*)(((uintptr_t)d_ws + 1023) & ~uintptr_t(1023));
+  batch_carve(*Bt, base);
+  BatchArgs& g = Bt->g;
+  const EngineArgs& a = Bt->prob->a;
+  cudaStream_t s = Bt->stream;
+  const int64_t n = g.n, p = g.p;
+  // X -> hi/lo TF32 operands, row-major (forward) and transposed (transpose pass)
+  const int blocks = (int)std::min<int64_t>((n * g.pp + 255) / 256, (int64_t)Bt->sms * 16);
+  const dim3 tgrid((unsigned)((p + 31) / 32), (unsigned)((g.nn + 31) / 32));
+  if (a.dtype == F64) {
+    k_split_rows<double><<<blocks, 256, 0, s>>>((const double*)a.X, n, p, a.ld, Bt->xh, Bt->xl, g.pp);
+    k_split_transpose<double><<<tgrid, dim3(32, 8), 0, s>>>((const double*)a.X, n, p, a.ld, Bt->xth, Bt->xtl, g.nn);
+  } else {
+    k_split_rows<float><<<blocks, 256, 0, s>>>((const float*)a.X, n, p, a.ld, Bt->xh, Bt->xl, g.pp);
+    k_split_transpose<float><<<tgrid, dim3(32, 8), 0, s>>>((const float*)a.X, n, p, a.ld, Bt->xth, Bt->xtl, g.nn);
+  }
+  L0_B_TRY(cudaGetLastError());
+  L0_B_TRY(cudaMemsetAsync(g.rh, 0, 4ull * 2 * g.B * g.nn, s));
+  L0_B_TRY(cudaMemsetAsync(g.rl, 0, 4ull * 2 * g.B * g.nn, s));
+  L0_B_TRY(cudaMemsetAsync(g.cnt, 0, 4ull * g.B, s));
+  L0_B_TRY(cudaMemsetAsync(g.flags, 0, 4ull * 8, s));
+  int rc = 0;
+  rc |= tc_make_map(&Bt->m_xh, Bt->xh, n, p, g.pp, kTcBM);
+  rc |= tc_make_map(&Bt->m_xl, Bt->xl, n, p, g.pp, kTcBM);
+  rc |= tc_make_map(&Bt->m_xth, Bt->xth, p, n, g.nn, kTcBM);
+  rc |= tc_make_map(&Bt->m_xtl, Bt->xtl, p, n, g.nn, kTcBM);
+  rc |= tc_make_map(&Bt->m_bh, g.bh, g.B, p, g.pp, kTcBN);
+  rc |= tc_make_map(&Bt->m_bl, g.bl, g.B, p, g.pp, kTcBN);
+  rc |= tc_make_map(&Bt->m_rh, g.rh, 2 * g.B, n, g.nn, kTcBN);
+  rc |= tc_make_map(&Bt->m_rl, g.rl, 2 * g.B, n, g.nn, kTcBN);
+  if (rc) return set_error(L0_CUDA, "cuTensorMapEncodeTiled failed");
+  TcGemmArgs& gf = Bt->gf;
+  gf.ldc = g.nn;
+  gf.c_split = g.B * g.nn;
+  gf.C = g.cf;
+  gf.n_active = g.flags + 3;
+  TcGemmArgs& gt = Bt->gt;
+  gt.ldc = g.pp;
+  gt.c_split = 2 * g.B * g.pp;
+  gt.C = g.ct;
+  gt.n_active = g.flags + 2;
+  L0_B_TRY(cudaStreamSynchronize(s));
+  return L0_OK;
+}
+
+int32_t l0_batch_destroy(l0_batch* Bt) {
+  if (!Bt) return L0_OK;
+  batch_destroy_graph(*Bt);
+  if (Bt->h_flags) cudaFreeHost(Bt->h_flags);
+  if (Bt->ev_in) cudaEventDestroy(Bt->ev_in);
+  if (Bt->ev_chunk) cudaEventDestroy(Bt->ev_chunk);
+  if (Bt->stream) cudaStreamDestroy(Bt->stream);
+  delete Bt;
+  return L0_OK;
+}
+
+int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const l0_fista_opts* o,
+                       const l0_node* nodes, double* d_beta_out, l0_report* reps, void* stream) {
+  if (!Bt || !o || !reps || !d_beta_out) return set_error(L0_INVALID, "null argument");
+  if (!Bt->ws) return set_error(L0_INVALID, "batch has no workspace (l0_batch_set_workspace)");
+  BatchArgs& g = Bt->g;
+  const int64_t p = g.p, B = g.B, pv = g.pv;
+  std::memset(reps, 0, sizeof(l0_report) * (size_t)B);
+  if (!(k >= 1 && k <= p)) return set_error(L0_INVALID, "k must satisfy 1 <= k <= p");
+  if (!(M > 0 && std::isfinite(M))) return set_error(L0_INVALID, "M must be a positive finite real");
+  if (!(lambda2 > 0 && std::isfinite(lambda2))) return set_error(L0_INVALID, "lambda2 must be a positive finite real");
+  if (!(o->gap_tolerance > 0)) return set_error(L0_INVALID, "gap_tolerance must be positive");
+  if (o->bound_check_interval < 1) return set_error(L0_INVALID, "bound_check_interval must be >= 1");
+  if (o->max_iterations < 1) return set_error(L0_INVALID, "max_iterations must be >= 1");
+  if (!(o->lipschitz > 0) || std::isnan(o->lipschitz))
+    return set_error(L0_INVALID, "lipschitz constant must be provided and positive");
+  // ---- per-node classes and parameters (model.py:119-149, perspective.py:36-73) ----
+  std::vector<uint8_t> mask((size_t)(B * pv), (uint8_t)FREE);
+  std::vector<int> fone((size_t)(B * g.fone_stride), 0);
+  std::vector<Params> prm((size_t)B);
+  for (int64_t b = 0; b < B; ++b) {
+    const l0_node* nd = nodes ? &nodes[b] : nullptr;
+    int64_t n1 = 0, n0 = 0;
+    double parent = -INFINITY;
+    uint8_t* mk = mask.data() + b * pv;
+    std::vector<int> f1;
+    if (nd) {
+      parent = nd->parent_bound;
+      n1 = nd->n_fixed_one;
+      n0 = nd->n_fixed_zero;
+      for (int64_t i = 0; i < n1; ++i) {
+        const int64_t j = nd->h_fixed_one[i];
+        if (j < 0 || j >= p) return set_error(L0_INVALID, "fixed_one index out of range");
+        if (mk[j] != FREE) return set_error(L0_INVALID, "duplicate fixed index");
+        mk[j] = FIXED_ONE;
+        f1.push_back((int)j);
+      }
+      for (int64_t i = 0; i < n0; ++i) {
+        const int64_t j = nd->h_fixed_zero[i];
+        if (j < 0 || j >= p) return set_error(L0_INVALID, "fixed_zero index out of range");
+        if (mk[j] != FREE) return set_error(L0_INVALID, "fixed_one and fixed_zero must be disjoint");
+        mk[j] = FIXED_ZERO;
+      }
+    }
+    if (n1 > k) return set_error(L0_INFEASIBLE, "|fixed_one| exceeds the budget k (node " + std::to_string(b) + ")");
+    std::sort(f1.begin(), f1.end());
+    std::copy(f1.begin(), f1.end(), fone.begin() + b * g.fone_stride);
+    const int64_t nfree = p - n1 - n0;
+    Params& hp = prm[(size_t)b];
+    hp = Params{};
+    hp.L = std::max(o->lipschitz, 1e-12);   // fista.py:101
+    hp.two_l2 = 2.0 * lambda2;              // fista.py:98
+    hp.rho = hp.L / hp.two_l2;              // fista.py:102
+    hp.M = M;
+    hp.gap_tol = o->gap_tolerance;
+    hp.gap_tol_rel = o->gap_tolerance_rel;
+    hp.early_primal = o->early_primal_cutoff;
+    hp.early_dual = o->early_dual_cutoff;
+    hp.parent_bound = parent;
+    hp.max_iter = o->max_iterations;
+    hp.k = k;
+    hp.k_g = k - n1;
+    hp.k_rem = std::min(k - n1, nfree);
+    hp.n_free = nfree;
+    hp.n_fone = n1;
+    hp.bci = o->bound_check_interval;
+    hp.restart = o->restart ? 1 : 0;
+    hp.stop_on_gap = o->stop_on_gap ? 1 : 0;
+    hp.node_mode = (n1 + n0) > 0 ? 1 : 0;
+    hp.loss = g.loss;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t user_s = (cudaStream_t)stream;
+  cudaStream_t s = Bt->stream;
+  L0_B_TRY(cudaEventRecord(Bt->ev_in, user_s));
+  L0_B_TRY(cudaStreamWaitEvent(s, Bt->ev_in, 0));
+  L0_B_TRY(cudaMemcpyAsync(g.prm, prm.data(), sizeof(Params) * B, cudaMemcpyHostToDevice, s));
+  L0_B_TRY(cudaMemcpyAsync(g.mask, mask.data(), (size_t)(B * pv), cudaMemcpyHostToDevice, s));
+  L0_B_TRY(cudaMemcpyAsync(g.fone, fone.data(), 4ull * B * g.fone_stride, cudaMemcpyHostToDevice, s));
+  int64_t launches = 0;
+  kb_state_init<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(g);
+  ++launches;
+  // cold start: beta_0 = 0 (fista.py:130-137); u_0 = X beta_0 through the forward contraction
+  L0_B_TRY(cudaMemsetAsync(g.beta, 0, 8ull * 3 * B * pv, s));
+  L0_B_TRY(cudaMemsetAsync(g.bh, 0, 4ull * B * g.pp, s));
+  L0_B_TRY(cudaMemsetAsync(g.bl, 0, 4ull * B * g.pp, s));
+  Bt->gf.n_active = nullptr;
+  L0_B_TRY(tc_gemm_launch(Bt->m_xh, Bt->m_xl, Bt->m_bh, Bt->m_bl, Bt->gf, std::min(Bt->gf.units, Bt->sms), s));
+  Bt->gf.n_active = g.flags + 3;
+  kb_obj<<<dim3((unsigned)g.rblocks, (unsigned)B), kRowThreads, 0, s>>>(g, MODE_INIT);
+  L0_B_TRY(cudaGetLastError());
+  launches += 2;
+  const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100) : 10;
+  int rc = batch_build_graph(*Bt, G);
+  if (rc) return rc;
+  int64_t chunks = 0;
+  bool stop_sent = false;
+  for (;;) {
+    L0_B_TRY(cudaGraphLaunch(Bt->exec, s));
+    L0_B_TRY(cudaEventRecord(Bt->ev_chunk, s));
+    L0_B_TRY(cudaEventSynchronize(Bt->ev_chunk));
+    ++chunks;
+    if (Bt->h_flags[4] >= B) break;
+    const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (!stop_sent && elapsed > o->time_limit) {  // fista.py:204-206 (checked per chunk)
+      kb_request_stop<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(g, TERM_TIME_LIMIT);
+      L0_B_TRY(cudaGetLastError());
+      ++launches;
+      stop_sent = true;
+    }
+  }
+  launches += chunks * Bt->graph_kernels;
+  // ---- reports and iterates ----------------------------------------------------
+  std::vector<State> hs((size_t)B);
+  L0_B_TRY(cudaMemcpyAsync(hs.data(), g.st, sizeof(State) * B, cudaMemcpyDeviceToHost, s));
+  kb_gather_beta<<<dim3((unsigned)std::min<int64_t>((p + 255) / 256, 64), (unsigned)B), 256, 0, s>>>(g, d_beta_out);
+  L0_B_TRY(cudaGetLastError());
+  ++launches;
+  cudaEvent_t ev_out;
+  L0_B_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+  cudaEventRecord(ev_out, s);
+  cudaStreamWaitEvent(user_s, ev_out, 0);
+  L0_B_TRY(cudaStreamSynchronize(s));
+  cudaEventDestroy(ev_out);
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  int first_err = ST_OK;
+  int64_t err_node = -1;
+  for (int64_t b = 0; b < B; ++b) {
+    const State& h = hs[(size_t)b];
+    l0_report& r = reps[b];
+    r.primal_value = h.obj;
+    r.dual_bound = h.best_dual;
+    r.gap = h.gap;
+    r.iterations = h.t;
+    r.restarts = h.restarts;
+    r.termination = h.termination;
+    r.status = h.err;
+    r.error_iteration = h.err_iter;
+    r.wall_time = wall;
+    r.gpu_launches = launches;
+    r.topk_fallbacks = h.topk_fallbacks;
+    if (h.err != ST_OK && first_err == ST_OK) { first_err = h.err; err_node = b; }
+  }
+  if (first_err != ST_OK)
+    return set_error(first_err, "node " + std::to_string(err_node) + " failed (status " +
+                                    std::to_string(first_err) + " at iteration " +
+                                    std::to_string(hs[(size_t)err_node].err_iter) + ")");
+  return L0_OK;
+}
+
+}  // extern "C"

@@ -7,3 +7,6 @@
 #include "ops.cu"
 #include "engine_host.cu"
 #include "abi_ops.cu"
+#include "tc_gemm.cu"
+#include "batch.cu"
+#include "batch_host.cu"

@@ -131,6 +131,26 @@ class DeviceProblem:
         self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
         native.check(lib.l0_problem_set_workspace(handle, self.ws.data_ptr(), nb.value))
 
+    def batch(self, n_nodes: int):
+        """Batched-node engine for ``n_nodes`` nodes on this X (cached; the
+        workspace holds X split into TF32 hi/lo operands, 4 x n x p fp32)."""
+        import torch
+        cache = self.__dict__.setdefault("_batches", {})
+        if n_nodes in cache:
+            return cache[n_nodes]
+        for old in list(cache):          # keep one batch engine resident
+            cache.pop(old)[2]()
+        lib = native.load()
+        handle = ctypes.c_void_p()
+        native.check(lib.l0_batch_create(self.handle, int(n_nodes), ctypes.byref(handle)))
+        fin = weakref.finalize(self, lib.l0_batch_destroy, handle)
+        nb = ctypes.c_uint64()
+        native.check(lib.l0_batch_workspace_bytes(handle, ctypes.byref(nb)))
+        ws = torch.empty(int(nb.value), dtype=torch.uint8, device=self.X.device)
+        native.check(lib.l0_batch_set_workspace(handle, ws.data_ptr(), nb.value))
+        cache[n_nodes] = (handle, ws, fin)
+        return cache[n_nodes]
+
     def matvec(self, v):
         import torch
         from . import _device

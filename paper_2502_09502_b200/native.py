@@ -92,6 +92,15 @@ _PROTOS = {
                                   c_vp]),
     "l0_all_finite": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, ctypes.POINTER(c_i32), c_vp,
                               c_u64, c_vp]),
+    "l0_batch_create": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "l0_batch_workspace_bytes": (c_i32, [c_vp, ctypes.POINTER(c_u64)]),
+    "l0_batch_set_workspace": (c_i32, [c_vp, c_vp, c_u64]),
+    "l0_batch_solve": (c_i32, [c_vp, c_i64, c_f64, c_f64, ctypes.POINTER(FistaOpts),
+                               c_vp, c_vp, c_vp, c_vp]),
+    "l0_batch_destroy": (c_i32, [c_vp]),
+    "l0_tc_gemm_workspace_bytes": (c_u64, [c_i64, c_i64, c_i64]),
+    "l0_tc_gemm_3xtf32": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i32, c_i64, c_i64,
+                                  c_vp, c_i64, c_i32, ctypes.POINTER(c_i32), c_vp, c_u64, c_vp]),
 }
 
 EXPORTED = tuple(_PROTOS)

@@ -1,0 +1,123 @@
+"""Batched node engine on the B200: the tcgen05 3xTF32 contraction and the
+batched FISTA solves against the oracle (fista.py:76-222 per node)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, splits=0):
+    from paper_2502_09502_b200 import native
+    lib = native.lib()
+    M, K = A.shape
+    N = B.shape[0]
+    ws = torch.empty(int(lib.l0_tc_gemm_workspace_bytes(M, N, K)), dtype=torch.uint8, device="cuda")
+    s_out = ctypes.c_int32(0)
+    # first call to learn S (auto), then allocate C
+    S_max = 64
+    C = torch.zeros((S_max, N, M), dtype=torch.float32, device="cuda")
+    dt = lambda t: native.F64 if t.dtype == torch.float64 else native.F32
+    native.check(lib.l0_tc_gemm_3xtf32(A.data_ptr(), dt(A), M, K, A.stride(0), B.data_ptr(), dt(B), N,
+                                       B.stride(0), C.data_ptr(), M, splits, ctypes.byref(s_out),
+                                       ws.data_ptr(), ws.numel(), None))
+    torch.cuda.synchronize()
+    S = s_out.value
+    return C[:S].double().sum(0), S
+
+
+@pytest.mark.parametrize("M,N,K,splits,dtype", [
+    (128, 256, 32, 1, torch.float32),
+    (300, 40, 100, 1, torch.float32),
+    (300, 40, 100, 3, torch.float64),
+    (1000, 512, 777, 0, torch.float32),
+    (4999, 300, 2048, 0, torch.float64),
+    (2000, 1024, 5000, 0, torch.float32),
+])
+def test_tc_gemm_3xtf32(M, N, K, splits, dtype):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, generator=g, device="cuda", dtype=torch.float64).to(dtype)
+    B = torch.randn(N, K, generator=g, device="cuda", dtype=torch.float64).to(dtype)
+    C, S = _gemm(A, B, splits)
+    ref = B.double() @ A.double().T                    # N x M
+    scale = B.double().abs() @ A.double().abs().T      # error scale of each dot product
+    err = ((C - ref).abs() / scale).max().item()
+    # tensor-core fp32 accumulation is not round-to-nearest: the error grows ~linearly in K
+    assert err < 4e-6, (err, S)
+    if splits:
+        assert S == splits
+
+
+# ---------------------------------------------------------------------------
+# batched node solves
+# ---------------------------------------------------------------------------
+def _c4_instance(scale, count):
+    from paper_2502_09502_b200 import LossKind, NodeState, ProblemInstance
+    from paper_2502_09502_b200.data import make_config
+    cfg = make_config("C4", scale=scale, nodes=count)
+    inst = ProblemInstance(cfg.X, cfg.y, LossKind(cfg.loss), cfg.k, cfg.M, cfg.lambda2, dtype="fp32")
+    nodes = [None] + [NodeState(fixed_one=f1, fixed_zero=f0) for f0, f1 in cfg.nodes[:count - 1]]
+    return inst, nodes
+
+
+def _rel(a, b):
+    return abs(a - b) / max(1.0, abs(b))
+
+
+@pytest.mark.parametrize("scale,count", [(0.1, 24), (0.08, 300)])
+def test_batched_matches_single_solves(scale, count):
+    from paper_2502_09502_b200 import FistaOptions, lipschitz_constant, solve_relaxation
+    from paper_2502_09502_b200 import solve_relaxation_batched
+    inst, nodes = _c4_instance(scale, count)
+    L = lipschitz_constant(inst)
+    opts = FistaOptions(max_iterations=120, stop_on_gap=False, lipschitz=L)
+    reps = solve_relaxation_batched(inst, nodes, opts=opts)
+    assert len(reps) == count
+    check = list(range(0, count, max(1, count // 12)))
+    for i in check:
+        ref = solve_relaxation(inst, nodes[i], opts=opts)
+        r = reps[i]
+        assert r.iterations == ref.iterations == 120
+        # the gap is a difference of two fp32-class quantities: compare it
+        # absolutely (the iteration-limit -> converged relabel at gap <= tol
+        # can differ when the gap sits at the tolerance)
+        assert abs(r.gap - ref.gap) < 1e-5 * max(1.0, abs(ref.primal_value)), (i, r.gap, ref.gap)
+        # fp32-class contraction: 1e-5 relative (north star, fp32 mode)
+        assert _rel(r.primal_value, ref.primal_value) < 1e-5, (i, r.primal_value, ref.primal_value)
+        assert _rel(r.dual_bound, ref.dual_bound) < 1e-5, (i, r.dual_bound, ref.dual_bound)
+        scale_b = max(1.0, float(np.abs(ref.beta).max()))
+        assert float(np.abs(r.beta - ref.beta).max()) / scale_b < 1e-4, i
+        # fixed coordinates respected exactly
+        nd = nodes[i]
+        if nd is not None and nd.fixed_zero:
+            assert np.all(r.beta[list(nd.fixed_zero)] == 0.0)
+
+
+def test_batched_default_options_converge_like_single():
+    from paper_2502_09502_b200 import FistaOptions, lipschitz_constant, solve_relaxation
+    from paper_2502_09502_b200 import solve_relaxation_batched
+    inst, nodes = _c4_instance(0.1, 8)
+    L = lipschitz_constant(inst)
+    opts = FistaOptions(max_iterations=3000, lipschitz=L, gap_tolerance=1e-4)
+    reps = solve_relaxation_batched(inst, nodes, opts=opts)
+    for i, nd in enumerate(nodes):
+        ref = solve_relaxation(inst, nd, opts=opts)
+        assert reps[i].termination == ref.termination
+        # restart decisions (obj_next >= obj) are discrete: a 1e-7 difference can
+        # move one, so the stopping check may land a few cadence points apart
+        assert abs(reps[i].iterations - ref.iterations) <= max(40, ref.iterations // 2)
+        assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5
+        assert reps[i].gap <= 1e-4 or reps[i].termination.value != "converged"
+
+
+def test_batched_infeasible_node_raises():
+    from paper_2502_09502_b200 import FistaOptions, NodeState, solve_relaxation_batched
+    from paper_2502_09502_b200.errors import InfeasibleNodeError
+    inst, nodes = _c4_instance(0.05, 3)
+    bad = NodeState(fixed_one=tuple(range(inst.k + 1)))
+    with pytest.raises(InfeasibleNodeError):
+        solve_relaxation_batched(inst, [None, bad], opts=FistaOptions(max_iterations=5, lipschitz=1e3))
