@@ -8,19 +8,19 @@
 //              bound checks), split hi/lo for 3xTF32; F* partials
 //   kb_plan  : which node rows the transpose contraction needs
 //   GEMM_T   : Ct = X^T [R | Z]             (p x 2B, split-K partials)
-//   kb_prox  : per node (one CTA): gradient step, bound check, prox, g(beta+),
-//              beta+ split hi/lo for the forward contraction
+//   kb_step  : per (slab, node): gradient step and the slab epilogue
+//   kb_window: per node (one CTA): bound check, windowed sort + PAVA, g(beta+),
+//              beta+ step split hi/lo for the forward contraction
 //   GEMM_F   : Cf = X beta+                 (n x B, split-K partials)
 //   kb_obj   : per node: u = sum of partials, F(u), objective / restart
 //
 // Node-major layouts everywhere ([node][coordinate], [node][row]) so that one
 // node's vectors are contiguous and the contractions' B operands are K-major.
-#include <cub/block/block_radix_sort.cuh>
-
 #include "batch_ops.cuh"
 #include "control.cuh"
 #include "engine.cuh"
 #include "prox.cuh"
+#include "slab_epilogue.cuh"
 
 namespace l0 {
 
@@ -58,6 +58,17 @@ struct BatchArgs {
   unsigned* cnt;    // [B] (zero between launches)
   int* flags;       // [0] alive, [1] any zeta, [2] GEMM_T rows, [3] GEMM_F rows, [4] done count
   int rblocks;      // row blocks of kb_rhs / kb_obj
+  // per-node slab epilogue products (slab_epilogue.cuh), S slabs of kK2Slab columns
+  int S;
+  double* hval;       // [B][pv]
+  double* cand_key;   // [B][pv]
+  int* cand_idx;      // [B][pv]
+  int* slab_cnt;      // [B][S]
+  double* slab_sum;   // [B][S]
+  double* slab_max;
+  double* slab_below;
+  double* slab_hfone;
+  double* slab_htop;  // [B][S][kHTop]
 };
 
 constexpr int kRowThreads = 256;
@@ -186,114 +197,80 @@ __device__ __forceinline__ EngineArgs node_view(const BatchArgs& g, int64_t b) {
   a.gv = g.gv + b * gvs(g);
   a.mask = g.mask + b * g.pv;
   a.fone = g.fone + b * g.fone_stride;
+  a.k2_slabs = g.S;
+  a.hval = g.hval + b * g.pv;
+  a.cand_key = g.cand_key + b * g.pv;
+  a.cand_idx = g.cand_idx + b * g.pv;
+  a.slab_cnt = g.slab_cnt + b * g.S;
+  a.slab_sum = g.slab_sum + b * g.S;
+  a.slab_max = g.slab_max + b * g.S;
+  a.slab_below = g.slab_below + b * g.S;
+  a.slab_hfone = g.slab_hfone + b * g.S;
+  a.slab_htop = g.slab_htop + b * g.S * kHTop;
   return a;
 }
 
-// one CTA per node: gradient step, bound check, prox (full sort of the free
-// keys, PAVA), g(beta+), split of beta+ for GEMM_F
-template <int T, int IPT>
-__global__ void __launch_bounds__(T, 1) kb_prox(BatchArgs g) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  using Sort = cub::BlockRadixSort<double, T, IPT, int, 6>;
-  ProxSmem& sm = *reinterpret_cast<ProxSmem*>(smem_raw);
-  typename Sort::TempStorage& tmp =
-      *reinterpret_cast<typename Sort::TempStorage*>(smem_raw + sizeof(ProxSmem));
-  const int64_t b = blockIdx.x;
+// (slab, node): reduce the transpose contraction's split-K partials for 256
+// columns of one node, then the single engine's slab epilogue (gradient step,
+// keys, speculative outputs, window candidates, Huber values)
+__global__ void __launch_bounds__(kK2Slab) kb_step(BatchArgs g) {
+  __shared__ EpiSmem sm;
+  const int64_t b = blockIdx.y;
+  const int slab = blockIdx.x;
   const EngineArgs a = node_view(g, b);
-  State* st = a.st;
+  const State* st = a.st;
   if (st->done) return;
-  const Params* P = a.prm;
   const bool wz = st->dual_pending != 0;
   const bool wg = st->dual_only == 0;
+  if (!wg && !wz) return;
   const int64_t t = st->t + 1;
   const double c = momentum(st->phi);
-  const int64_t p = g.p, pv = g.pv, B = g.B;
-  const int tid = threadIdx.x;
-  if (wz) {
-    // v = X^T zeta (split-K partials, fixed order) and the F* sums over row blocks
-    for (int64_t j = tid; j < p; j += T) {
-      double v = 0.0;
-      for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(g.ct + s * (2 * B * g.pp) + (B + b) * g.pp + j);
-      a.gv[pv + j] = v;
-    }
-    if (tid == 0) {
-      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-      for (int r = 0; r < g.rblocks; ++r) {
-        const double* fp = g.fpart + (b * g.rblocks + r) * 4;
-        f0 += fp[0];
-        f1 += fp[1];
-        f2 += fp[2];
-      }
-      a.gv[2 * pv + 0] = f0;
-      a.gv[2 * pv + 1] = f1;
-      a.gv[2 * pv + 2] = f2;
-    }
+  const int64_t B = g.B, pv = g.pv;
+  const int64_t j = (int64_t)slab * kK2Slab + threadIdx.x;
+  double gsum = 0.0, v = 0.0;
+  if (j < g.p) {
+    const float* ct = g.ct;
+    const int64_t split = 2 * B * g.pp;
+    if (wg)
+      for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(ct + s * split + b * g.pp + j);
+    if (wz)
+      for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(ct + s * split + (B + b) * g.pp + j);
   }
-  double keys[IPT];
-  int ids[IPT];
-  if (wg) {
-    // gradient step (fista.py:161-163) and sort keys |rho gamma| (prox.py:106-111)
-    const double* b1 = a.beta + ring(t - 1) * pv;
-    const double* b2 = a.beta + ring(t - 2) * pv;
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int64_t j = (int64_t)tid * IPT + i;
-      ids[i] = (int)j;
-      keys[i] = -CUDART_INF;
-      if (j < p) {
-        double gsum = 0.0;
-        for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(g.ct + s * (2 * B * g.pp) + b * g.pp + j);
-        double gam = dadd(b1[j], dmul(c, dsub(b1[j], b2[j])));
-        gam = dsub(gam, ddiv(gsum, P->L));
-        a.gam[j] = gam;
-        const int cls = P->node_mode ? a.mask[j] : FREE;
-        keys[i] = (cls == FREE) ? fabs(dmul(P->rho, gam)) : -1.0;
-      }
+  if (wz && slab == 0 && threadIdx.x == 0) {
+    // F*(-zeta) accumulators over the row blocks (fixed order)
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    for (int r = 0; r < g.rblocks; ++r) {
+      const double* fp = g.fpart + (b * g.rblocks + r) * 4;
+      f0 += fp[0];
+      f1 += fp[1];
+      f2 += fp[2];
     }
+    a.gv[2 * pv + 0] = f0;
+    a.gv[2 * pv + 1] = f1;
+    a.gv[2 * pv + 2] = f2;
   }
-  __syncthreads();
-  if (wz) {
-    if (dual_step(a, sm)) return;
-  }
-  if (st->dual_only) return;
-  Sort(tmp).SortDescending(keys, ids);  // stable: ties keep ascending ids (prox.py:111)
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int64_t pos = (int64_t)tid * IPT + i;
-    if (pos < p) {
-      a.xs[pos] = keys[i];
-      a.perm[pos] = ids[i];
-    }
-  }
-  __syncthreads();
-  PostArgs q;
-  q.p = p;
-  q.nf = P->node_mode ? P->n_free : p;
-  q.kk = P->node_mode ? P->k_rem : P->k;
-  q.kg = P->node_mode ? P->k_g : P->k;
-  q.rho = P->rho;
-  q.M = P->M;
-  q.xs = a.xs;
-  q.perm = a.perm;
-  q.tail = a.tail;
-  q.in = a.gam;
-  q.out = a.beta + ring(t) * pv;
-  q.absb = a.scratch;
-  q.mask = P->node_mode ? a.mask : nullptr;
-  q.fone = P->node_mode ? a.fone : nullptr;
-  q.n_fone = P->n_fone;
-  q.gmode = 1;
-  q.want_g = 1;
-  q.g_out = &st->g_next;
-  q.st = st;
-  prox_post_sort<T>(q, sm);
+  slab_epilogue(a, slab, t, c, wg, wz, gsum, v, sm);
+}
+
+// one CTA per node: bound check, windowed sort + PAVA, g(beta+) (the single
+// engine's K3), then beta+ (or its step) split hi/lo for GEMM_F
+__global__ void __launch_bounds__(kWinThreads, 1) kb_window(BatchArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
+  WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
+  const int64_t b = blockIdx.x;
+  const EngineArgs a = node_view(g, b);
+  if (a.st->done) return;
+  const int64_t t = a.st->t + 1;
+  if (!prox_window_body(a, ps, sm)) return;
   __syncthreads();
   // beta+ (re-sync) or beta+ - beta_t -> hi/lo operand rows of the forward contraction
   const bool full = resync_at(t);
-  const double* bprev = a.beta + ring(t - 1) * pv;
-  for (int64_t j = tid; j < g.pp; j += T) {
+  const double* out = a.beta + ring(t) * g.pv;
+  const double* bprev = a.beta + ring(t - 1) * g.pv;
+  for (int64_t j = threadIdx.x; j < g.pp; j += kWinThreads) {
     float h = 0.f, l = 0.f;
-    if (j < p) tf32_split(full ? q.out[j] : dsub(q.out[j], bprev[j]), h, l);
+    if (j < g.p) tf32_split(full ? out[j] : dsub(out[j], bprev[j]), h, l);
     g.bh[b * g.pp + j] = h;
     g.bl[b * g.pp + j] = l;
   }
@@ -387,27 +364,17 @@ __global__ void kb_request_stop(BatchArgs g, int term) {
   }
 }
 
-template <int T, int IPT>
-static size_t kb_prox_smem() {
-  return sizeof(ProxSmem) + sizeof(typename cub::BlockRadixSort<double, T, IPT, int, 6>::TempStorage);
-}
-
-template <int T, int IPT>
-static cudaError_t kb_prox_launch_t(const BatchArgs& g, cudaStream_t s) {
-  const size_t smem = kb_prox_smem<T, IPT>();
-  cudaError_t e = cudaFuncSetAttribute(kb_prox<T, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kb_prox<T, IPT><<<(unsigned)g.B, T, smem, s>>>(g);
-  return cudaGetLastError();
-}
-
-// p capacity of the per-node sort
-inline int64_t kb_prox_capacity() { return 1024 * 16; }
+inline int64_t kb_prox_capacity() { return (int64_t)kWinThreads * kK2Slab; }
 
 cudaError_t kb_prox_launch(const BatchArgs& g, cudaStream_t s) {
-  if (g.p <= 2048) return kb_prox_launch_t<256, 8>(g, s);
-  if (g.p <= 8192) return kb_prox_launch_t<512, 16>(g, s);
-  return kb_prox_launch_t<1024, 16>(g, s);
+  kb_step<<<dim3((unsigned)g.S, (unsigned)g.B), kK2Slab, 0, s>>>(g);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = prox_window_smem();
+  e = cudaFuncSetAttribute(kb_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kb_window<<<(unsigned)g.B, kWinThreads, smem, s>>>(g);
+  return cudaGetLastError();
 }
 
 }  // namespace l0

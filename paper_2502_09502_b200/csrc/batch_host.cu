@@ -69,6 +69,15 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
   g.fpart = (double*)take(8ull * 4 * B * g.rblocks);
   g.lpart = (double*)take(8ull * 2 * B * g.rblocks);
   g.cnt = (unsigned*)take(4ull * B);
+  g.hval = (double*)take(8ull * B * pv);
+  g.cand_key = (double*)take(8ull * B * pv);
+  g.cand_idx = (int*)take(4ull * B * pv);
+  g.slab_cnt = (int*)take(4ull * B * g.S);
+  g.slab_sum = (double*)take(8ull * B * g.S);
+  g.slab_max = (double*)take(8ull * B * g.S);
+  g.slab_below = (double*)take(8ull * B * g.S);
+  g.slab_hfone = (double*)take(8ull * B * g.S);
+  g.slab_htop = (double*)take(8ull * B * g.S * kHTop);
   g.flags = (int*)take(4ull * 8);
   return off + 1024;
 }
@@ -217,7 +226,7 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   if (n_nodes < 1 || n_nodes > 65535) return set_error(L0_INVALID, "n_nodes must be in [1, 65535]");
   const EngineArgs& a = prob->a;
   if (a.p > kb_prox_capacity())
-    return set_error(L0_UNSUPPORTED, "batched nodes support p <= 16384 (per-node on-chip sort)");
+    return set_error(L0_UNSUPPORTED, "batched nodes support p <= 131072 (per-node window kernel)");
   if (a.n >= (int64_t)INT32_MAX || a.p >= (int64_t)INT32_MAX)
     return set_error(L0_INVALID, "n and p must fit the tensor-map coordinates");
   l0_batch* Bt = new l0_batch();
@@ -232,13 +241,14 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   g.n = a.n;
   g.p = a.p;
   g.B = n_nodes;
-  g.pv = (a.p + 31) / 32 * 32;
+  g.pv = (a.p + kK2Slab - 1) / kK2Slab * kK2Slab;   // slab arrays index slab * 256 + pos
   g.pp = g.pv;
   g.nn = (a.n + 31) / 32 * 32;
   g.loss = a.loss;
   g.y = a.y;
   g.fone_stride = g.pv;
   g.rblocks = (int)((a.n + kRowsPerBlock - 1) / kRowsPerBlock);
+  g.S = (int)((a.p + kK2Slab - 1) / kK2Slab);
   // contraction plans: forward M = n, N = B, K = p; transpose M = p, N = 2B
   // (the zeta rows only on bound checks), K = n, split count planned for N = B
   TcGemmArgs& gf = Bt->gf;

@@ -401,17 +401,16 @@ __device__ int dual_step_slabs(const EngineArgs& a, ProxSmem& ps, WinSmem& ws) {
   return ps.done;
 }
 
-__global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
-  WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
+// K3 body for one solve (the single engine's CTA, or one node's CTA of the
+// batched engine).  Returns 1 when beta+ was produced (0: finished / bound only).
+__device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) {
   const State* st0 = a.st;
-  if (st0->done) return;
+  if (st0->done) return 0;
   L0_STAMP(a.st, 0);
   if (st0->dual_pending) {
-    if (dual_step_slabs(a, ps, sm)) return;
+    if (dual_step_slabs(a, ps, sm)) return 0;
   }
-  if (a.st->dual_only) return;
+  if (a.st->dual_only) return 0;
   const Params* P = a.prm;
   State* st = a.st;
   const int tid = threadIdx.x;
@@ -483,7 +482,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
       select_window(a.key, p, ub, kWinCap, sm);
       if (sm.sel_state == 2) {
         if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
-        return;
+        return 0;
       }
       const unsigned long long lb = sm.sel_lb;
       const int cnt = sm.sel_count;
@@ -603,7 +602,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
     }
     if (path == 1 && kkg > kCandCap) {
       if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
-      return;
+      return 0;
     }
     if (path == 1) {
       __syncthreads();
@@ -648,6 +647,14 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
     }
   }
   L0_STAMP(st, 8);
+  return 1;
+}
+
+__global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
+  WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
+  prox_window_body(a, ps, sm);
 }
 
 size_t prox_window_smem() {
