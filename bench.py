@@ -39,6 +39,7 @@ WORKLOAD = "C2"
 # Lanczos 2.99073e5), rounded up so it stays a valid Lipschitz bound
 L_C2 = 2.9908e5
 REL_GAP = 1e-6
+TF32_DENSE_PEAK = 1100.0   # TFLOP/s, B200 dense TF32 (B200_PROFILING.md)
 
 
 def log(*a):
@@ -181,6 +182,119 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# batched nodes (C4): tensor-core roofline
+# ---------------------------------------------------------------------------
+def tf32_peak(seconds=1.5):
+    """cuBLAS TF32 dense throughput on this GPU (torch.matmul 8192^3, fp32 inputs,
+    TF32 math): burst (best) and sustained (back to back) TFLOP/s."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(3):
+            a @ b
+        torch.cuda.synchronize()
+        best = 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(10):
+            e0.record(); a @ b; e1.record(); torch.cuda.synchronize()
+            best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+        t0 = time.perf_counter(); cnt = 0
+        e0.record()
+        while time.perf_counter() - t0 < seconds:
+            a @ b; cnt += 1
+            if cnt % 8 == 0:
+                torch.cuda.synchronize()
+        e1.record(); torch.cuda.synchronize()
+        sustained = 2 * n ** 3 * cnt / (e0.elapsed_time(e1) / 1e3) / 1e12
+        return best, sustained
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def run_batched(args):
+    """C4: 512 node relaxations (n=20000, p=5000 fp32) advanced together; the two
+    X passes per iteration are tcgen05 3xTF32 contractions."""
+    import torch
+    import paper_2502_09502_b200 as eng
+    from paper_2502_09502_b200 import data
+    t0 = time.time()
+    cd = data.make_config("C4", scale=args.c4_scale, nodes=args.c4_nodes)
+    inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2,
+                               dtype="fp32")
+    nodes = [None] + [eng.NodeState(fixed_one=f1, fixed_zero=f0)
+                      for f0, f1 in cd.nodes[:args.c4_nodes - 1]]
+    L = eng.lipschitz_constant(inst)
+    log(f"[bench] C4 generated + L in {time.time() - t0:.1f}s")
+    B, n, p, K = len(nodes), cd.n, cd.p, args.c4_steps
+    opts = lambda it, prof: eng.FistaOptions(lipschitz=L, max_iterations=it, stop_on_gap=False,
+                                             profile=prof)
+    eng.solve_relaxation_batched(inst, nodes, opts=opts(3, False))
+    eng.solve_relaxation_batched(inst, nodes, opts=opts(3, True))
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = eng.solve_relaxation_batched(inst, nodes, opts=opts(K, False), return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    assert all(r.iterations == K for r in reps)
+    prof = eng.solve_relaxation_batched(inst, nodes, opts=opts(K, True), return_device=True)[0].stats
+    it = prof["profiled_iterations"]
+    gt, gf, px = prof["gemm_t_ms"] / it, prof["gemm_f_ms"] / it, prof["prox_ms"] / it
+    checks = sum(1 for t in range(1, K + 1) if t == 1 or t % 10 == 0) / K
+    useful_f = 2.0 * n * p * B
+    useful_t = 2.0 * n * p * B * (1.0 + checks)
+    burst, sustained = tf32_peak()
+    tensor_f = 3 * useful_f / (gf / 1e3) / 1e12
+    tensor_t = 3 * useful_t / (gt / 1e3) / 1e12
+    cpu = None
+    if not args.no_cpu:
+        import threadpoolctl
+        from oracle import l0_oracle
+        X64 = cd.X.astype(np.float64)
+        cores = os.cpu_count()
+        nd = nodes[1]
+        with threadpoolctl.threadpool_limits(cores):
+            l0_oracle.fista(X64, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=1,
+                            fixed_one=nd.fixed_one, fixed_zero=nd.fixed_zero, stop_on_gap=False)
+            t0 = time.perf_counter()
+            l0_oracle.fista(X64, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=5,
+                            fixed_one=nd.fixed_one, fixed_zero=nd.fixed_zero, stop_on_gap=False)
+            dt = time.perf_counter() - t0
+        cpu = {"value": 5 / dt, "unit": "node-iters/s", "cores": cores, "kind": "port",
+               "sample": f"5 FISTA iterations of one C4 node (oracle port, {cores} threads)"}
+    del inst
+    torch.cuda.empty_cache()
+    return {"workload": f"C4: {B} node relaxations, n={n}, p={p}, fp32 X, SE, k=10, M=2, "
+                        f"lambda2=0.5, cold start, {K} iterations each (lockstep)",
+            "metric": "node FISTA iterations/s", "value": B * K / (ms / 1e3),
+            "ms_per_batched_iteration": ms / K, "clocks": clk,
+            "contraction": "tcgen05 kind::tf32, 3xTF32 (hi/lo split), fp32 TMEM accumulation",
+            "roofline": {"bound": "tensor", "unit": "TFLOP/s",
+                         "kernel": "tc_gemm_kernel (forward X.Beta step)",
+                         "achieved": tensor_f, "peak": TF32_DENSE_PEAK,
+                         "frac": tensor_f / TF32_DENSE_PEAK,
+                         "peak_source": "B200_PROFILING.md dense TF32 (MEASURED_PEAKS.json has no "
+                                        "TF32 entry); measured cuBLAS TF32 8192^3 here: burst "
+                                        f"{burst:.0f}, sustained {sustained:.0f}",
+                         "cublas_tf32_burst": burst, "cublas_tf32_sustained": sustained,
+                         "transpose_achieved": tensor_t, "transpose_frac": tensor_t / TF32_DENSE_PEAK,
+                         "useful_tflops_forward": useful_f / (gf / 1e3) / 1e12,
+                         "flops_per_forward_launch": 3 * useful_f,
+                         "note": "tensor FLOPs count the 3 TF32 products of the hi/lo split"},
+            "ms_per_iteration_split": {"gemm_transpose": gt, "prox": px, "gemm_forward": gf},
+            "cpu_baseline": cpu}
+
+
+# ---------------------------------------------------------------------------
 # ours
 # ---------------------------------------------------------------------------
 def run_ours(args):
@@ -279,6 +393,15 @@ def run_ours(args):
     log(f"[bench] e2e {e2e['value']} it/s {e2e_reps}")
 
     cb = cpu_baseline(cd, args.cpu_iters) if not args.no_cpu else None
+    del inst
+    torch.cuda.empty_cache()
+    batched = None
+    if args.c4_nodes > 0:
+        try:
+            batched = run_batched(args)
+            log(f"[bench] C4 {batched['value']:.0f} node-it/s {batched['ms_per_iteration_split']}")
+        except Exception as exc:   # reported, never silently dropped
+            batched = {"error": repr(exc)}
     line = {"metric": "FISTA iters/sec (C2 root relaxation, HBM-bound GEMV passes)",
             "value": value, "unit": "iters/s", "n_gpus": 1, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
@@ -286,7 +409,8 @@ def run_ours(args):
             "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
             "restarts": rep.restarts, "final_gap": rep.gap,
-            "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks")}
+            "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks"),
+            "batched_nodes": batched}
     print(json.dumps(line), flush=True)
 
 
@@ -340,6 +464,9 @@ def main():
     ap.add_argument("--e2e-solves", type=int, default=2)
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
+    ap.add_argument("--c4-steps", type=int, default=50)
+    ap.add_argument("--c4-scale", type=float, default=1.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -30,6 +30,8 @@ struct Batch {
   cudaEvent_t ev_in = nullptr, ev_chunk = nullptr;
   cudaGraphExec_t exec = nullptr;
   int G = 0;
+  int profile = 0;
+  std::vector<cudaEvent_t> ev;   // profile: [iter][gemm_t b,e | step+window b,e | gemm_f b,e]
   int64_t graph_kernels = 0;
 };
 
@@ -84,8 +86,11 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
 
 static void batch_destroy_graph(Batch& Bt) {
   if (Bt.exec) cudaGraphExecDestroy(Bt.exec);
+  for (auto e : Bt.ev) cudaEventDestroy(e);
+  Bt.ev.clear();
   Bt.exec = nullptr;
   Bt.G = 0;
+  Bt.profile = 0;
 }
 
 #define L0_B_TRY(expr)                                                                \
@@ -95,27 +100,40 @@ static void batch_destroy_graph(Batch& Bt) {
       return set_error(ST_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-static int batch_iteration(Batch& Bt, cudaStream_t s) {
+static int batch_iteration(Batch& Bt, cudaStream_t s, cudaEvent_t* ev) {
   BatchArgs& g = Bt.g;
   const dim3 rgrid((unsigned)g.rblocks, (unsigned)g.B);
+  auto rec = [&](int i) -> cudaError_t {
+    return ev ? cudaEventRecordWithFlags(ev[i], s, cudaEventRecordExternal) : cudaSuccess;
+  };
   kb_rhs<<<rgrid, kRowThreads, 0, s>>>(g);
   kb_plan<<<1, 1, 0, s>>>(g);
   L0_B_TRY(cudaGetLastError());
+  L0_B_TRY(rec(0));
   L0_B_TRY(tc_gemm_launch(Bt.m_xth, Bt.m_xtl, Bt.m_rh, Bt.m_rl, Bt.gt, std::min(Bt.gt.units, Bt.sms), s));
+  L0_B_TRY(rec(1));
+  L0_B_TRY(rec(2));
   L0_B_TRY(kb_prox_launch(g, s));
+  L0_B_TRY(rec(3));
+  L0_B_TRY(rec(4));
   L0_B_TRY(tc_gemm_launch(Bt.m_xh, Bt.m_xl, Bt.m_bh, Bt.m_bl, Bt.gf, std::min(Bt.gf.units, Bt.sms), s));
+  L0_B_TRY(rec(5));
   kb_obj<<<rgrid, kRowThreads, 0, s>>>(g, MODE_ITER);
   L0_B_TRY(cudaGetLastError());
   return ST_OK;
 }
 
-static int batch_build_graph(Batch& Bt, int G) {
-  if (Bt.exec && Bt.G == G) return ST_OK;
+static int batch_build_graph(Batch& Bt, int G, int profile) {
+  if (Bt.exec && Bt.G == G && Bt.profile == profile) return ST_OK;
   batch_destroy_graph(Bt);
+  if (profile) {
+    Bt.ev.resize((size_t)G * 6);
+    for (auto& e : Bt.ev) L0_B_TRY(cudaEventCreate(&e));
+  }
   cudaStream_t s = Bt.stream;
   L0_B_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = ST_OK;
-  for (int i = 0; i < G && rc == ST_OK; ++i) rc = batch_iteration(Bt, s);
+  for (int i = 0; i < G && rc == ST_OK; ++i) rc = batch_iteration(Bt, s, profile ? &Bt.ev[(size_t)i * 6] : nullptr);
   if (rc == ST_OK) {
     kb_count<<<1, 256, 0, s>>>(Bt.g);
     cudaError_t e = cudaGetLastError();
@@ -143,6 +161,7 @@ static int batch_build_graph(Batch& Bt, int G) {
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return set_error(ST_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
   Bt.G = G;
+  Bt.profile = profile;
   Bt.graph_kernels = kernels;
   return ST_OK;
 }
@@ -434,15 +453,26 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   L0_B_TRY(cudaGetLastError());
   launches += 2;
   const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100) : 10;
-  int rc = batch_build_graph(*Bt, G);
+  int rc = batch_build_graph(*Bt, G, o->profile ? 1 : 0);
   if (rc) return rc;
   int64_t chunks = 0;
   bool stop_sent = false;
+  double prof_ms[3] = {0.0, 0.0, 0.0};
+  int64_t prof_n = 0;
   for (;;) {
     L0_B_TRY(cudaGraphLaunch(Bt->exec, s));
     L0_B_TRY(cudaEventRecord(Bt->ev_chunk, s));
     L0_B_TRY(cudaEventSynchronize(Bt->ev_chunk));
     ++chunks;
+    if (o->profile) {
+      for (int i = 0; i < G; ++i) {
+        float ms;
+        for (int k2 = 0; k2 < 3; ++k2)
+          if (cudaEventElapsedTime(&ms, Bt->ev[(size_t)i * 6 + 2 * k2], Bt->ev[(size_t)i * 6 + 2 * k2 + 1]) == cudaSuccess)
+            prof_ms[k2] += ms;
+        ++prof_n;
+      }
+    }
     if (Bt->h_flags[4] >= B) break;
     const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (!stop_sent && elapsed > o->time_limit) {  // fista.py:204-206 (checked per chunk)
@@ -482,6 +512,12 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
     r.wall_time = wall;
     r.gpu_launches = launches;
     r.topk_fallbacks = h.topk_fallbacks;
+    r.prox_full_passes = h.slow_prox;
+    // profile: contraction / prox times summed over the executed chunk iterations
+    r.k2_ms = prof_ms[0];   // transpose contraction X^T [R | Z]
+    r.k3_ms = prof_ms[1];   // slab epilogue + windowed prox
+    r.k1_ms = prof_ms[2];   // forward contraction X (beta step)
+    r.k1_count = r.k2_count = r.k3_count = prof_n;
     if (h.err != ST_OK && first_err == ST_OK) { first_err = h.err; err_node = b; }
   }
   if (first_err != ST_OK)

@@ -177,7 +177,9 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
             gap=float(r.gap), iterations=int(r.iterations), restarts=int(r.restarts),
             termination=_TERM[int(r.termination)], wall_time=float(r.wall_time),
             stats={"gpu_launches": int(r.gpu_launches), "batched": len(nodes),
-                   "lipschitz": float(L)}))
+                   "lipschitz": float(L), "prox_full_passes": int(r.prox_full_passes),
+                   **({"gemm_t_ms": r.k2_ms, "prox_ms": r.k3_ms, "gemm_f_ms": r.k1_ms,
+                       "profiled_iterations": int(r.k1_count)} if opts.profile else {})}))
     return out
 
 
