@@ -315,7 +315,7 @@ def run_ours(args):
 
     def fixed(iters, profile):
         return eng.FistaOptions(lipschitz=L_C2, max_iterations=iters, gap_tolerance=1e-300,
-                                stop_on_gap=False, profile=profile)
+                                stop_on_gap=False, profile=profile, engine_path=args.engine)
 
     # warm-up: W iterations (graph capture, caches)
     eng.solve_relaxation(inst, opts=fixed(W, True), return_device=True)
@@ -376,7 +376,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = eng.solve_relaxation(inst_h, opts=eng.FistaOptions(
-            lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP))
+            lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP, engine_path=args.engine))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         e2e_iters += r.iterations
@@ -464,6 +464,7 @@ def main():
     ap.add_argument("--e2e-solves", type=int, default=2)
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine", default="auto", choices=["auto", "two_pass", "single_pass"])
     ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
     ap.add_argument("--c4-steps", type=int, default=50)
     ap.add_argument("--c4-scale", type=float, default=1.0)

@@ -75,7 +75,8 @@ typedef struct l0_fista_opts {
   int32_t stop_on_gap;          /* 0: fixed-iteration mode (no gap stop) */
   int32_t chunk_iterations;     /* iterations per captured CUDA graph (0: auto) */
   int32_t profile;              /* 1: time the kernels with CUDA events (report fields) */
-  int32_t engine_path;          /* 0 auto (single pass when it fits), 1 two-pass, 2 single pass */
+  int32_t engine_path;          /* 0 auto (single pass for fp64 X when it fits a <= 8-CTA cluster
+                                   plan, else two-pass), 1 two-pass, 2 single pass */
 } l0_fista_opts;
 
 /* NodeState (model.py:119-149): host index arrays, sorted unique, disjoint. */
@@ -136,6 +137,9 @@ int32_t l0_nccl_unique_id(void* h_out128);
 
 /* diagnostics: clock64 phase stamps of the last prox kernel (L0_PROBE builds) */
 int32_t l0_debug_probe(l0_problem* prob, int64_t* h_out16);
+/* diagnostics: copy the engine's p-length scratch vector (per-tile timestamps of
+ * the single-pass kernel in L0_PROBE builds) */
+int32_t l0_debug_scratch(l0_problem* prob, double* h_out, int64_t count);
 
 /* ---- hot path ----------------------------------------------------------------- */
 int32_t l0_fista_solve(l0_problem* prob, int64_t k, double M, double lambda2,

@@ -433,6 +433,14 @@ int32_t l0_debug_probe(l0_problem* P, int64_t* out16) {
   return ST_OK;
 }
 
+int32_t l0_debug_scratch(l0_problem* P, double* h_out, int64_t count) {
+  if (!P || !h_out || !P->ws) return set_error(ST_INVALID, "null argument");
+  count = std::min<int64_t>(count, P->a.pv);
+  L0_CUDA_TRY(cudaStreamSynchronize(P->stream));
+  L0_CUDA_TRY(cudaMemcpy(h_out, P->a.scratch, 8 * (size_t)count, cudaMemcpyDeviceToHost));
+  return ST_OK;
+}
+
 int32_t l0_problem_set_comm(l0_problem* P, const void* h_id, int32_t nranks, int32_t rank) {
   if (!P) return set_error(ST_INVALID, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(ST_INVALID, "bad rank");
@@ -553,9 +561,12 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   hp.stop_on_gap = o->stop_on_gap ? 1 : 0;
   hp.node_mode = node_mode ? 1 : 0;
   hp.loss = a.loss;
-  // engine path: auto = two-pass (measured faster on B200); the
-  // single physical pass (fused) is opt-in while it is being tuned
-  const int want_fused = (o->engine_path == 2) ? P->fused_planned : 0;
+  // engine path: auto = the single physical pass where it is measured faster
+  // (fp64 X with a cluster of <= 8 CTAs per row block: C2 1847 vs 1419 it/s),
+  // the two-pass engine otherwise (fp32 X: the transposes dominate)
+  const int auto_fused = P->fused_planned && a.dtype == F64 && a.fz_cs <= 8;
+  const int want_fused = (o->engine_path == 2) ? P->fused_planned
+                         : (o->engine_path == 1) ? 0 : auto_fused;
   if (o->engine_path == 2 && !P->fused_planned)
     return set_error(ST_UNSUPPORTED, "the single-pass kernel does not fit this problem");
   if (want_fused != a.fused) destroy_graphs(*P);

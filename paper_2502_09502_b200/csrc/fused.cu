@@ -9,12 +9,15 @@
 //   * a thread-block cluster of fz_cs CTAs spans a full row block; CTA c owns
 //     columns [c W, (c+1) W) with its beta slice in shared memory;
 //   * row tiles (fz_rows rows x W columns) stream HBM -> shared memory with
-//     cp.async.bulk (TMA bulk copies, one mbarrier per double buffer);
-//   * forward: per-row partial dots, block-reduced, exchanged through
-//     distributed shared memory after one cluster barrier -> u_t for the tile,
-//     identical in every CTA (fixed order over the cluster);
-//   * transpose: the same shared-memory tile accumulates X^T [r_R | r_N | zeta]
-//     in registers (8..12 columns per thread);
+//     cp.async.bulk into a ring of fz_stages buffers (one mbarrier each);
+//   * forward: per-row partial dots of tile k+D (D tiles of lookahead),
+//     block-reduced in a fixed order and pushed to EVERY CTA of the cluster
+//     with st.async into a ring of kFzSlots partial slots, each completing a
+//     transaction-count mbarrier in the receiving CTA -- no cluster barrier
+//     on the per-tile path, the exchange latency hides behind D tiles;
+//   * transpose: when tile k's partials are complete, u for its rows is the
+//     fixed-order sum over the cluster (identical in every CTA), and the same
+//     shared-memory tile accumulates X^T [r_R | r_N | zeta] in registers;
 //   * the last CTA of the grid reduces the per-cluster loss (fixed order) and
 //     runs the objective / restart logic (control.cuh).
 //
@@ -22,8 +25,11 @@
 // the candidate matching the restart decision and runs the slab epilogue
 // (gradient step, keys, window candidates, Huber values).
 //
-// Arithmetic per row and column is the 2-pass engine's (gemv.cu), so results
-// agree with it to summation-order rounding.
+// Flow control: a CTA's forward group works on tile j only once its
+// transpose group freed stage j - S, which needed every peer's partials of
+// j - S; a peer that published those has its own transpose past j - 2S, so
+// partial slot j (mod kFzSlots) is never one the peer still has to read as
+// long as kFzSlots >= 2 S.
 
 #include <cstdio>
 #include <cstdlib>
@@ -34,8 +40,9 @@
 
 namespace l0 {
 
-constexpr int kFzThreads = 256;
 constexpr int kFzMaxRows = 8;
+constexpr int kFzMaxCs = 16;
+constexpr int kFzSlots = 8;    // partial-slot ring (2 x the forward lead, see flow control)
 // vectors (16 B) per thread per row: 8 fp64 or 12 fp32 columns per thread,
 // i.e. 24 / 36 fp64 accumulators for the three right-hand sides
 template <typename TX> constexpr int fz_maxv() { return sizeof(TX) == 8 ? 4 : 3; }
@@ -64,6 +71,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   }
 }
+// cluster-scope acquire of remote st.async data; backs off so waiting warps
+// leave the issue slots to the forward group
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(phase)
+        : "memory");
+    if (ok) break;
+    __nanosleep(100);
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -75,12 +97,6 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -91,12 +107,19 @@ __device__ __forceinline__ uint32_t cluster_id() {
   asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ double ld_dsmem(const double* local, uint32_t rank) {
+__device__ __forceinline__ uint32_t map_rank(const void* local, uint32_t rank) {
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr(local)), "r"(rank));
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-  return v;
+  return ra;
+}
+// v -> [remote] in CTA `rank`, completing 8 bytes on that CTA's mbarrier
+__device__ __forceinline__ void st_async_f64(const double* local_dst, const uint64_t* local_bar,
+                                             uint32_t rank, double v) {
+  const uint32_t ra = map_rank(local_dst, rank);
+  const uint32_t rb = map_rank(local_bar, rank);
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra),
+               "d"(v), "r"(rb)
+               : "memory");
 }
 
 template <typename TX> struct FzVec;
@@ -113,27 +136,78 @@ template <> struct FzVec<float> {
   }
 };
 
+constexpr int kFzFwdWarps = 4;                      // forward group
+constexpr int kFzTrWarps = 8;                       // transpose group
+constexpr int kFzFwd = kFzFwdWarps * 32;            // 128 threads
+constexpr int kFzTr = kFzTrWarps * 32;              // 256 threads
+constexpr int kFzBlock = kFzFwd + kFzTr;            // 384 threads
+constexpr int kFzMaxStages = 12;
+constexpr int kFzLead = kFzSlots / 2;   // forward may run at most this many tiles ahead
+
 struct FzShared {
-  uint64_t bar[3];
-  double xpart[2][kFzMaxRows];   // this CTA's row partials (tile parity)
-  double wpart[2][kFzThreads / 32][kFzMaxRows];
-  double rr[2][3][kFzMaxRows];   // r_R, r_N, zeta of the tile rows (tile parity)
+  uint64_t full[kFzMaxStages];              // tile ring (bulk-copy complete_tx)
+  uint64_t empty[kFzMaxStages];             // forward warps done reading a stage
+  uint64_t xb[kFzSlots];                    // partial slots (st.async complete_tx)
+  uint64_t tfree[kFzLead];                  // transpose group finished tile j (ring)
+  double part[kFzSlots][kFzMaxCs][kFzMaxRows];   // [slot][source rank][row]
+  double yv[kFzSlots][kFzMaxRows];          // y and u_{t-1} of the slot's rows (self st.async)
+  double up[kFzSlots][kFzMaxRows];
+  double sy[kFzMaxStages][kFzMaxRows];      // y / u_{t-1} of a stage's rows (bulk copies
+  double su[kFzMaxStages][kFzMaxRows];      // under the stage's barrier)
+  double rr[3][kFzMaxRows];                 // r_R, r_N, zeta of the transpose group's tile
   double red[32];
   int bad;
 };
 
-// shared memory: FzShared | beta slice (W doubles) | 3 tiles (rows x W x sizeof(TX))
-template <typename TX>
-__global__ void __launch_bounds__(kFzThreads, 2) kf_fused(EngineArgs a, int mode) {
+__device__ __forceinline__ double gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (double)t;
+}
+// L0_PROBE builds: per-tile timestamps of two CTAs into a.scratch
+//   [cta 0 | cta cs-1][tile][fwd start, fwd end, transpose start, transpose end, -, -]
+#ifdef L0_PROBE
+#define FZ_STAMP(a, slotk, which)                                                           \
+  do {                                                                                     \
+    const int _c = (blockIdx.x == 0) ? 0 : ((int)blockIdx.x == a.fz_cs - 1 ? 1 : -1);     \
+    if (_c >= 0 && (slotk) < 1000) a.scratch[(_c * 1000 + (slotk)) * 6 + (which)] = gtimer(); \
+  } while (0)
+#else
+#define FZ_STAMP(a, slotk, which) do { } while (0)
+#endif
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+
+// shared memory: FzShared | beta slice (W doubles) | stages x (R x W x sizeof(TX))
+//
+// Warps 0-3 (forward group) stream tiles through the bulk-copy ring; warp w
+// owns rows w, w+4, ... of a tile: its lanes dot the row with the beta slice,
+// one warp reduction per row, and lanes 0..cs-1 push the row's partial to
+// every CTA of the cluster with st.async (lane 0 also y / u_{t-1} to this
+// CTA).  The stage is refilled as soon as the four warps have read it, so all
+// but one stage are in flight.  Warps 4-11 (transpose group) consume tiles in
+// order: the tile's rows are re-read from L2 into registers first (the loads
+// do not depend on r), then u and r from the complete partials, then the
+// three accumulations.  HBM sees X once.
+//   R  rows per tile (multiple of 4)     NV 16-byte vectors per transpose thread
+template <typename TX, int R, int NV>
+__global__ void __launch_bounds__(kFzBlock, 1) kf_fused(EngineArgs a, int mode) {
   extern __shared__ __align__(128) unsigned char smem[];
   using V = FzVec<TX>;
   constexpr int VE = V::N;
-  constexpr int kFzMaxV = fz_maxv<TX>();
+  constexpr int W = NV * kFzTr * VE;          // columns per CTA
+  constexpr int FV = W / (32 * VE);            // vectors per forward lane per row
+  constexpr int RPW = R / kFzFwdWarps;         // rows per forward warp
+  static_assert(R % kFzFwdWarps == 0 && R <= kFzMaxRows, "rows per tile");
   FzShared& sh = *reinterpret_cast<FzShared*>(smem);
   double* sbeta = reinterpret_cast<double*>(smem + ((sizeof(FzShared) + 127) & ~size_t(127)));
-  const int64_t W = a.fz_w;
   TX* tiles = reinterpret_cast<TX*>(sbeta + W);
-  const int R = a.fz_rows;
+  const int S = a.fz_stages;
 
   State* st = a.st;
   int64_t t = 0;
@@ -156,200 +230,216 @@ __global__ void __launch_bounds__(kFzThreads, 2) kf_fused(EngineArgs a, int mode
   const int ncl = a.fz_ncl;
   const int64_t n = a.n, ld = a.ld;
   const int64_t c0 = (int64_t)crank * W;                      // first column of this CTA
-  const int64_t wvalid = max((int64_t)0, min(W, ld - c0));    // columns inside the row
-  const uint32_t row_bytes = (uint32_t)(wvalid * (int64_t)sizeof(TX));
+  const int wvalid = (int)max((int64_t)0, min((int64_t)W, ld - c0));   // columns inside the row
+  const uint32_t row_bytes = (uint32_t)wvalid * (uint32_t)sizeof(TX);
   const double* bsrc = (mode == MODE_ITER) ? a.beta + ring(t) * a.pv : a.beta;
+  const double* uprev = a.u + ((mode == MODE_ITER) ? ring(t - 1) * n : 0);
 
-  // beta slice (zero beyond p) and barriers
-  for (int64_t j = tid; j < W; j += kFzThreads) {
+  // static tile schedule of this cluster: cid, cid + ncl, ...
+  const int ntiles = (int)a.fz_tiles;
+  const int mytiles = cid < ntiles ? (ntiles - cid + ncl - 1) / ncl : 0;
+  auto tile_of = [&](int k) -> int64_t { return (int64_t)cid + (int64_t)k * ncl; };
+  auto tile_rows = [&](int k) -> int { return (int)min((int64_t)R, n - tile_of(k) * R); };
+  auto slot_bytes = [&](int k) -> uint32_t {
+    return (uint32_t)((cs + 2) * tile_rows(k) * (int)sizeof(double));
+  };
+
+  for (int j = tid; j < W; j += kFzBlock) {
     const int64_t col = c0 + j;
     sbeta[j] = col < a.p ? bsrc[col] : 0.0;
   }
   if (tid == 0) {
-    mbar_init(&sh.bar[0], 1);
-    mbar_init(&sh.bar[1], 1);
-    mbar_init(&sh.bar[2], 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kFzFwdWarps);
+    }
+    for (int i = 0; i < kFzSlots; ++i) mbar_init(&sh.xb[i], 1);
+    for (int i = 0; i < kFzLead; ++i) mbar_init(&sh.tfree[i], 1);
     sh.bad = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (cs > 1) cluster_barrier();
-
-  // static tile schedule of this cluster: cid, cid + ncl, ... ; tile k of this
-  // cluster lives in buffer k % 3
-  const int64_t ntiles = a.fz_tiles;
-  const int64_t mytiles = cid < ntiles ? (ntiles - cid + ncl - 1) / ncl : 0;
-  auto tile_of = [&](int64_t k) -> int64_t { return cid + k * ncl; };
-  auto tile_rows = [&](int64_t tile) -> int { return (int)min((int64_t)R, n - tile * R); };
-  auto issue = [&](int64_t k) {
-    const int64_t tile = tile_of(k);
-    const int buf = (int)(k % 3);
-    const int rows = tile_rows(tile);
-    TX* dst = tiles + (int64_t)buf * R * W;
-    if (row_bytes == 0) {
-      mbar_arrive_expect(&sh.bar[buf], 0);
-      return;
-    }
-    mbar_arrive_expect(&sh.bar[buf], row_bytes * rows);
-    for (int r = 0; r < rows; ++r)
-      bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
-               row_bytes, &sh.bar[buf]);
-  };
   if (tid == 0)
-    for (int64_t k = 0; k < 3 && k < mytiles; ++k) issue(k);
+    for (int k = 0; k < kFzSlots && k < mytiles; ++k) mbar_arrive_expect(&sh.xb[k], slot_bytes(k));
+  // every CTA's barriers are initialised and armed before anyone sends
+  if (cs > 1) cluster_barrier();
+  else __syncthreads();
 
-  // per-thread vectors: v-th vector covers columns v*256*VE + tid*VE .. +VE
-  const int nv = a.fz_nv;
-  double accR[kFzMaxV * VE], accN[kFzMaxV * VE], accZ[kFzMaxV * VE];
-#pragma unroll
-  for (int i = 0; i < kFzMaxV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
+  // y / u_{t-1} ride along with a tile when their segments are 16-byte bulk
+  // copies (even row counts and offsets); otherwise the forward group loads them
+  const bool side_ok = (n % 2 == 0);
+  auto side = [&](int k) { return side_ok && (tile_rows(k) % 2 == 0); };
+  auto issue = [&](int k, int buf) {
+    const int64_t tile = tile_of(k);
+    const int rows = tile_rows(k);
+    TX* dst = tiles + (int64_t)buf * R * W;
+    const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
+    mbar_arrive_expect(&sh.full[buf], row_bytes * rows + sb);
+    if (row_bytes > 0)
+      for (int r = 0; r < rows; ++r)
+        bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
+                 row_bytes, &sh.full[buf]);
+    if (sb) {
+      bulk_g2s(&sh.sy[buf][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[buf]);
+      if (mode == MODE_ITER) bulk_g2s(&sh.su[buf][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[buf]);
+    }
+  };
+
+  double accR[NV * VE], accN[NV * VE], accZ[NV * VE];
   double loss_acc = 0.0, f_acc[3] = {0.0, 0.0, 0.0};
   int bad = 0, gbad_R = 0, gbad_N = 0;
-  uint32_t phase[3] = {0u, 0u, 0u};
 
-  // forward partial dots of tile k into xpart[k & 1] (block-reduced, fixed order)
-  auto forward = [&](int64_t k) {
-    const int buf = (int)(k % 3);
-    const int rows = tile_rows(tile_of(k));
-    mbar_wait(&sh.bar[buf], phase[buf]);
-    phase[buf] ^= 1u;
-    const TX* tl = tiles + (int64_t)buf * R * W;
-    double dot[kFzMaxRows];
+  if (warp < kFzFwdWarps) {
+    // ===================== forward group =====================
+    if (tid == 0)
+      for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
+    int buf = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < mytiles; ++k) {
+      const int rows = tile_rows(k);
+      const int q = k % kFzSlots;
+      if (tid == 0) FZ_STAMP(a, k, 0);
+      // flow control: at most kFzLead tiles ahead of this CTA's transpose group
+      if (k >= kFzLead) mbar_wait(&sh.tfree[(k - kFzLead) % kFzLead], (uint32_t)(((k - kFzLead) / kFzLead) & 1));
+      mbar_wait(&sh.full[buf], ph);
+      const TX* tl = tiles + (int64_t)buf * R * W;
 #pragma unroll
-    for (int r = 0; r < kFzMaxRows; ++r) dot[r] = 0.0;
+      for (int i = 0; i < RPW; ++i) {
+        const int r = warp + i * kFzFwdWarps;
+        if (r < rows) {
+          double d0 = 0.0, d1 = 0.0;      // two chains for ILP
 #pragma unroll
-    for (int v = 0; v < kFzMaxV; ++v) {
-      if (v < nv) {
-        const int64_t col = (int64_t)v * kFzThreads * VE + tid * VE;
-        if (col < wvalid) {
-          double b[VE];
-#pragma unroll
-          for (int e = 0; e < VE; ++e) b[e] = sbeta[col + e];
-#pragma unroll
-          for (int r = 0; r < kFzMaxRows; ++r) {
-            if (r < rows) {
-              double x[VE];
-              V::widen(*reinterpret_cast<const typename V::T*>(tl + (int64_t)r * W + col), x);
-#pragma unroll
-              for (int e = 0; e < VE; ++e) dot[r] = fma(x[e], b[e], dot[r]);
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kFzMaxRows; ++r) {
-      if (r < rows) {
-        const double w = warp_sum(dot[r]);
-        if (lane == 0) sh.wpart[k & 1][warp][r] = w;
-      }
-    }
-    __syncthreads();
-    if (tid < rows) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kFzThreads / 32; ++w) s += sh.wpart[k & 1][w][tid];
-      sh.xpart[k & 1][tid] = s;
-    }
-  };
-  // u for the rows of tile k from the cluster's partials; r_R, r_N, zeta
-  auto gather = [&](int64_t k) {
-    const int64_t tile = tile_of(k);
-    const int rows = tile_rows(tile);
-    const int par = (int)(k & 1);
-    if (tid < rows) {
-      double u = 0.0;
-      for (int c = 0; c < cs; ++c)
-        u += (cs > 1) ? ld_dsmem(&sh.xpart[par][tid], (uint32_t)c) : sh.xpart[par][tid];
-      const int64_t row = tile * R + tid;
-      const double yi = a.y[row];
-      const double up = (mode == MODE_ITER) ? a.u[ring(t - 1) * n + row] : u;
-      const double dlt = dsub(u, up);
-      const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
-      const double ugN = dadd(u, dmul(cN, dlt));
-      if (!isfinite(ugR)) gbad_R = 1;
-      if (!isfinite(ugN)) gbad_N = 1;
-      sh.rr[par][0][tid] = loss_grad(a.loss, ugR, yi);
-      sh.rr[par][1][tid] = loss_grad(a.loss, ugN, yi);
-      const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
-      sh.rr[par][2][tid] = z;
-      if (crank == 0) {
-        if (mode == MODE_ITER) {
-          a.u[ring(t) * n + row] = u;
-        } else {
-          a.u[row] = u;
-          a.u[2 * n + row] = u;
-        }
-        if (!isfinite(u)) bad = 1;
-        loss_acc += loss_term(a.loss, u, yi);
-        if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
-      }
-    }
-    __syncthreads();
-  };
-  // transpose accumulation of tile k (rows' r from rr[k & 1])
-  auto transpose = [&](int64_t k) {
-    const int buf = (int)(k % 3);
-    const int rows = tile_rows(tile_of(k));
-    const int par = (int)(k & 1);
-    const TX* tl = tiles + (int64_t)buf * R * W;
-#pragma unroll
-    for (int r = 0; r < kFzMaxRows; ++r) {
-      if (r < rows) {
-        const double rR = sh.rr[par][0][r], rN = sh.rr[par][1][r], rZ = sh.rr[par][2][r];
-#pragma unroll
-        for (int v = 0; v < kFzMaxV; ++v) {
-          if (v < nv) {
-            const int64_t col = (int64_t)v * kFzThreads * VE + tid * VE;
+          for (int j = 0; j < FV; ++j) {
+            const int col = (j * 32 + lane) * VE;
             if (col < wvalid) {
               double x[VE];
-              V::widen(*reinterpret_cast<const typename V::T*>(tl + (int64_t)r * W + col), x);
+              V::widen(*reinterpret_cast<const typename V::T*>(tl + r * W + col), x);
 #pragma unroll
               for (int e = 0; e < VE; ++e) {
-                accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-                accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
-                if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+                if (((j * VE + e) & 1) == 0) d0 = fma(x[e], sbeta[col + e], d0);
+                else d1 = fma(x[e], sbeta[col + e], d1);
               }
             }
           }
+          const double dsum = warp_sum(d0 + d1);
+          if (lane < cs) st_async_f64(&sh.part[q][crank][r], &sh.xb[q], (uint32_t)lane, dsum);
+          if (lane == 0) {
+            double yv, uv;
+            if (side(k)) {
+              yv = sh.sy[buf][r];
+              uv = (mode == MODE_ITER) ? sh.su[buf][r] : 0.0;
+            } else {
+              const int64_t row = tile_of(k) * R + r;
+              yv = a.y[row];
+              uv = (mode == MODE_ITER) ? uprev[row] : 0.0;
+            }
+            st_async_f64(&sh.yv[q][r], &sh.xb[q], crank, yv);
+            st_async_f64(&sh.up[q][r], &sh.xb[q], crank, uv);
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[buf]);
+      if (tid == 0) {
+        FZ_STAMP(a, k, 1);
+        if (k + S < mytiles) {
+          mbar_wait(&sh.empty[buf], ph);           // all four warps read the stage
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(k + S, buf);
+        }
+      }
+      if (++buf == S) { buf = 0; ph ^= 1u; }
     }
-  };
-
-  // software pipeline: the cluster exchange of tile k+1 overlaps the
-  // transpose of tile k (split arrive / wait of the cluster barrier)
-  if (mytiles > 0) {
-    forward(0);
-    if (cs > 1) cluster_barrier();
-    else __syncthreads();
-    gather(0);
-  }
-  for (int64_t k = 0; k < mytiles; ++k) {
-    const bool more = k + 1 < mytiles;
-    if (more) {
-      forward(k + 1);
-      if (cs > 1) cluster_arrive();
-    }
-    transpose(k);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();                              // tile k's buffer is free
-    if (tid == 0 && k + 3 < mytiles) issue(k + 3);
-    if (more) {
-      if (cs > 1) cluster_wait();
-      else __syncthreads();
-      gather(k + 1);
-    }
-  }
-
-  // ---- publish per-cluster partials -------------------------------------------
-  const int64_t pv = a.pv;
+  } else {
+    // ===================== transpose group =====================
+    const int lt = tid - kFzFwd;
 #pragma unroll
-  for (int v = 0; v < kFzMaxV; ++v) {
-    if (v < nv) {
+    for (int i = 0; i < NV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
+    const TX* xcols = static_cast<const TX*>(a.X) + c0;
+    // the tile's rows from L2 into registers first (independent of r)
+    typename V::T xv[R][NV];
+    for (int k = 0; k < mytiles; ++k) {
+      const int64_t tile = tile_of(k);
+      const int rows = tile_rows(k);
+      const int q = k % kFzSlots;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int col = v * kFzTr * VE + lt * VE;
+          if (r < rows && col < wvalid)
+            xv[r][v] = __ldg(reinterpret_cast<const typename V::T*>(xcols + (tile * R + r) * ld + col));
+          else
+            xv[r][v] = typename V::T{};
+        }
+      }
+      mbar_wait_cluster(&sh.xb[q], (uint32_t)((k / kFzSlots) & 1));
+      if (lt == 0) FZ_STAMP(a, k, 2);
+      if (lt < rows) {
+        double u = 0.0;
+        for (int c = 0; c < cs; ++c) u += sh.part[q][c][lt];
+        const int64_t row = tile * R + lt;
+        const double yi = sh.yv[q][lt];
+        const double up = (mode == MODE_ITER) ? sh.up[q][lt] : u;
+        const double dlt = dsub(u, up);
+        const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
+        const double ugN = dadd(u, dmul(cN, dlt));
+        if (!isfinite(ugR)) gbad_R = 1;
+        if (!isfinite(ugN)) gbad_N = 1;
+        sh.rr[0][lt] = loss_grad(a.loss, ugR, yi);
+        sh.rr[1][lt] = loss_grad(a.loss, ugN, yi);
+        const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
+        sh.rr[2][lt] = z;
+        if (crank == 0) {
+          if (mode == MODE_ITER) {
+            a.u[ring(t) * n + row] = u;
+          } else {
+            a.u[row] = u;
+            a.u[2 * n + row] = u;
+          }
+          if (!isfinite(u)) bad = 1;
+          loss_acc += loss_term(a.loss, u, yi);
+          if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
+        }
+      }
+      named_sync(2, kFzTr);
+      // slot q consumed: arm it for tile k + kFzSlots
+      if (lt == 0 && k + kFzSlots < mytiles) mbar_arrive_expect(&sh.xb[q], slot_bytes(k + kFzSlots));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double rR = sh.rr[0][r], rN = sh.rr[1][r], rZ = sh.rr[2][r];
+        if (r < rows) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double x[VE];
+            V::widen(xv[r][v], x);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+              accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
+              accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+              if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+            }
+          }
+        }
+      }
+      named_sync(2, kFzTr);      // rr reusable
+      if (lt == 0) {
+        FZ_STAMP(a, k, 3);
+        mbar_arrive(&sh.tfree[k % kFzLead]);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- publish per-cluster partials (transpose group) ---------------------------
+  const int64_t pv = a.pv;
+  if (warp >= kFzFwdWarps) {
+    const int lt = tid - kFzFwd;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
 #pragma unroll
       for (int e = 0; e < VE; ++e) {
-        const int64_t col = c0 + (int64_t)v * kFzThreads * VE + tid * VE + e;
+        const int64_t col = c0 + (int64_t)v * kFzTr * VE + lt * VE + e;
         if (col < pv) {
           a.fz_part[(0 * (int64_t)ncl + cid) * pv + col] = accR[v * VE + e];
           a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
@@ -373,7 +463,7 @@ __global__ void __launch_bounds__(kFzThreads, 2) kf_fused(EngineArgs a, int mode
     cp[3] = f1;
     cp[4] = f2;
   }
-  if (cs > 1) cluster_barrier();  // DSMEM reads of this CTA's xpart are over
+  if (cs > 1) cluster_barrier();  // no st.async into this CTA is still in flight
   __threadfence();
   __syncthreads();
   __shared__ int s_last;
@@ -491,21 +581,43 @@ __global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a) {
 static size_t fused_smem(const EngineArgs& a) {
   const size_t es = a.dtype == F64 ? 8 : 4;
   return ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)a.fz_w +
-         3 * (size_t)a.fz_rows * (size_t)a.fz_w * es;
+         (size_t)a.fz_stages * (size_t)a.fz_rows * (size_t)a.fz_w * es;
 }
 
-template <typename TX>
-static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at) {
+using KfFn = void (*)(EngineArgs, int);
+
+template <typename TX, int R>
+static KfFn kf_pick_nv(int nv) {
+  switch (nv) {
+    case 1: return kf_fused<TX, R, 1>;
+    case 2: return kf_fused<TX, R, 2>;
+    case 3: return kf_fused<TX, R, 3>;
+    case 4: return sizeof(TX) == 8 ? (KfFn)kf_fused<TX, R, 4> : nullptr;
+    default: return nullptr;
+  }
+}
+
+static KfFn kf_pick(const EngineArgs& a) {
+  const bool f64 = a.dtype == F64;
+  if (a.fz_rows == 4) return f64 ? kf_pick_nv<double, 4>(a.fz_nv) : kf_pick_nv<float, 4>(a.fz_nv);
+  if (a.fz_rows == 8) return f64 ? kf_pick_nv<double, 8>(a.fz_nv) : kf_pick_nv<float, 8>(a.fz_nv);
+  return nullptr;
+}
+
+static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at,
+                                KfFn* fn) {
+  *fn = kf_pick(a);
+  if (!*fn) return cudaErrorInvalidValue;
   const size_t smem = fused_smem(a);
-  cudaError_t e = cudaFuncSetAttribute(kf_fused<TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (a.fz_cs > 8) {
-    e = cudaFuncSetAttribute(kf_fused<TX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(*fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3((unsigned)(a.fz_cs * a.fz_ncl));
-  cfg.blockDim = dim3(kFzThreads);
+  cfg.blockDim = dim3(kFzBlock);
   cfg.dynamicSmemBytes = smem;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.fz_cs;
@@ -516,40 +628,53 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   return cudaSuccess;
 }
 
+// Choose cluster size, rows per tile and ring depth: the smallest cluster
+// (override: L0_FZ_CS) whose column slice fits the per-thread registers,
+// R = 8 rows per tile (L0_FZ_R: 4 or 8), as many stages as ~200 KB of shared
+// memory holds (<= kFzMaxStages).
 int fused_plan(EngineArgs& a, int sms) {
   (void)sms;
   const int VE = a.dtype == F64 ? 2 : 4;
-  const int64_t unit = (int64_t)kFzThreads * VE;   // columns per vector sweep
+  const int64_t unit = (int64_t)kFzTr * VE;   // columns per transpose-thread vector sweep
   const size_t es = a.dtype == F64 ? 8 : 4;
-  for (int cs : {1, 2, 4, 8}) {
+  const int maxv = a.dtype == F64 ? 4 : 3;
+  const char* env = getenv("L0_FZ_CS");
+  const int want_cs = env ? atoi(env) : 0;
+  const char* renv = getenv("L0_FZ_R");
+  const int R = (renv && atoi(renv) == 8) ? 8 : 4;
+  const size_t budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) : 170) * 1024;
+  for (int cs : {1, 2, 4, 8, 16}) {
+    if (want_cs > 0 && cs != want_cs) continue;
     const int64_t need = (a.p + cs - 1) / cs;
     const int64_t W = ((need + unit - 1) / unit) * unit;
     const int nv = (int)(W / unit);
-    if (nv > (a.dtype == F64 ? fz_maxv<double>() : fz_maxv<float>())) continue;
-    // rows per tile: three tiles + beta slice within 113 KB (2 CTAs per SM)
-    int R = (int)((113 * 1024 - 8 * W - 1536) / (3 * W * (int64_t)es));
-    R = std::min(R, kFzMaxRows);
-    if (R < 1) continue;
+    if (nv > maxv) continue;
+    const size_t fixed = ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)W;
+    if (fixed >= budget) continue;
+    int S = (int)((budget - fixed) / ((size_t)R * (size_t)W * es));
+    S = std::min(S, kFzMaxStages);
+    if (S < 2) continue;
     a.fz_cs = cs;
     a.fz_w = W;
     a.fz_nv = nv;
     a.fz_rows = R;
+    a.fz_stages = S;
     a.fz_tiles = (a.n + R - 1) / R;
     a.fz_ncl = 1;   // grid of one cluster for the occupancy query
     int ncl = 0;
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
-    cudaError_t e = (a.dtype == F64) ? fused_config<double>(a, cfg, at) : fused_config<float>(a, cfg, at);
+    KfFn fn = nullptr;
+    cudaError_t e = fused_config(a, cfg, at, &fn);
     if (e != cudaSuccess) {
       if (getenv("L0_DEBUG")) fprintf(stderr, "fused_plan: config %s\n", cudaGetErrorString(e));
       cudaGetLastError();
       return 0;
     }
-    e = (a.dtype == F64) ? cudaOccupancyMaxActiveClusters(&ncl, kf_fused<double>, &cfg)
-                         : cudaOccupancyMaxActiveClusters(&ncl, kf_fused<float>, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
     if (getenv("L0_DEBUG"))
-      fprintf(stderr, "fused_plan: cs=%d W=%lld nv=%d R=%d smem=%zu ncl=%d (%s)\n", cs,
-              (long long)W, nv, R, fused_smem(a), ncl, cudaGetErrorString(e));
+      fprintf(stderr, "fused_plan: cs=%d W=%lld nv=%d R=%d S=%d smem=%zu ncl=%d (%s)\n", cs,
+              (long long)W, nv, R, S, fused_smem(a), ncl, cudaGetErrorString(e));
     if (e != cudaSuccess || ncl < 1) {
       cudaGetLastError();
       return 0;
@@ -563,11 +688,11 @@ int fused_plan(EngineArgs& a, int sms) {
 cudaError_t launch_fused(const EngineArgs& a, int mode, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute at[1];
-  cudaError_t e = (a.dtype == F64) ? fused_config<double>(a, cfg, at) : fused_config<float>(a, cfg, at);
+  KfFn fn = nullptr;
+  cudaError_t e = fused_config(a, cfg, at, &fn);
   if (e != cudaSuccess) return e;
   cfg.stream = s;
-  if (a.dtype == F64) e = cudaLaunchKernelEx(&cfg, kf_fused<double>, a, mode);
-  else e = cudaLaunchKernelEx(&cfg, kf_fused<float>, a, mode);
+  e = cudaLaunchKernelEx(&cfg, fn, a, mode);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

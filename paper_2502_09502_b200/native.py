@@ -72,6 +72,7 @@ _PROTOS = {
                                ctypes.POINTER(Node), c_vp, c_vp, ctypes.POINTER(Report), TRACE_CB,
                                c_vp, c_vp]),
     "l0_debug_probe": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
+    "l0_debug_scratch": (c_i32, [c_vp, c_vp, c_i64]),
     "l0_matvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "l0_rmatvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "l0_power_iteration": (c_i32, [c_vp, c_vp, c_f64, c_i64, ctypes.POINTER(c_f64),
