@@ -135,14 +135,15 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    """dram bytes (read + write) per launch of each kernel, from the committed ncu
+    --set full captures (profiles/ncu_summary.json)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("k2_dram_bytes_per_launch"), d.get("k1_dram_bytes_per_launch")
+        return {k: v.get("dram_bytes_per_launch") for k, v in d.get("kernels", {}).items()}
     except Exception:
-        return None, None
+        return {}
 
 
 # ---------------------------------------------------------------------------
@@ -342,36 +343,45 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     s = 8
     n, p = cd.n, cd.p
-    k2_bytes = n * p * s + 8 * (3 * n + 5 * p)     # X, u_t, u_t-1, y, beta_t, beta_t-1, gamma, key
-    k1_bytes = n * p * s + 8 * (p + 2 * n)          # X, beta, y, u
     k1_avg = st["k1_ms"] / max(1, st["k1_count"])
     k2_avg = st["k2_ms"] / max(1, st["k2_count"])
     k3_avg = st["k3_ms"] / max(1, st["k3_count"])
-    dom = "k2_transpose" if st["k2_ms"] >= st["k1_ms"] else "k1_forward"
-    dom_bytes, dom_ms = (k2_bytes, k2_avg) if dom == "k2_transpose" else (k1_bytes, k1_avg)
+    single = bool(st.get("single_pass"))
+    traffic = ncu_traffic()
+    if single:
+        # KF reads X once: both gradient candidates, X^T zeta and u_t from one pass
+        kf_bytes = n * p * s + 8 * (4 * n + p)        # X, y, u_{t-1}, u_t (write), beta slice
+        dom, dom_bytes, dom_ms = "kf_fused", kf_bytes, k2_avg
+        others = {"kr_reduce_epilogue": {"launch_ms": k1_avg},
+                  "k3_prox_window": {"launch_ms": k3_avg}}
+    else:
+        k2_bytes = n * p * s + 8 * (3 * n + 5 * p)     # X, u_t, u_t-1, y, beta_t, beta_t-1, gamma, key
+        k1_bytes = n * p * s + 8 * (p + 2 * n)          # X, beta, y, u
+        dom = "k2_transpose" if st["k2_ms"] >= st["k1_ms"] else "k1_forward"
+        dom_bytes, dom_ms = (k2_bytes, k2_avg) if dom == "k2_transpose" else (k1_bytes, k1_avg)
+        others = {"k1_forward": {"launch_ms": k1_avg, "achieved_gbs": k1_bytes / (k1_avg / 1e3) / 1e9,
+                                 "frac": k1_bytes / (k1_avg / 1e3) / 1e9 / peak},
+                  "k2_transpose": {"launch_ms": k2_avg, "achieved_gbs": k2_bytes / (k2_avg / 1e3) / 1e9,
+                                   "frac": k2_bytes / (k2_avg / 1e3) / 1e9 / peak},
+                  "k3_prox_pava_envelope": {"launch_ms": k3_avg}}
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    t2, t1 = ncu_traffic()
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": (t2 if dom == "k2_transpose" else t1),
-                "algorithmic_bytes_per_launch": dom_bytes,
-                "launch_ms": dom_ms,
-                "other_kernels": {
-                    "k1_forward": {"launch_ms": k1_avg, "achieved_gbs": k1_bytes / (k1_avg / 1e3) / 1e9,
-                                   "frac": k1_bytes / (k1_avg / 1e3) / 1e9 / peak},
-                    "k2_transpose": {"launch_ms": k2_avg, "achieved_gbs": k2_bytes / (k2_avg / 1e3) / 1e9,
-                                     "frac": k2_bytes / (k2_avg / 1e3) / 1e9 / peak},
-                    "k3_prox_pava_envelope": {"launch_ms": k3_avg}},
+                "traffic": traffic.get(dom), "algorithmic_bytes_per_launch": dom_bytes,
+                "launch_ms": dom_ms, "engine": "single pass (X read once per iteration)" if single
+                else "two pass", "other_kernels": others,
                 "iteration_bytes_2pass": 2 * n * p * s,
-                "iteration_frac_of_hbm": (2 * n * p * s) / (ms / 1e3 / K) / 1e9 / peak}
-
+                "iteration_rate_vs_2pass_roofline": (2 * n * p * s) / (ms / 1e3 / K) / 1e9 / peak,
+                "note": "iteration_rate_vs_2pass_roofline > 1 is possible only because the "
+                        "single-pass engine reads X once per iteration" if single else ""}
     # end to end through the public API with host-resident X (pinned)
     Xpin = torch.from_numpy(cd.X).pin_memory()
     e2e_iters, e2e_time = 0, 0.0
     h2d = cd.X.nbytes + cd.y.nbytes
     d2h = cd.p * 8
     e2e_reps = []
-    for _ in range(args.e2e_solves):
+    for i in range(args.e2e_solves + (1 if args.e2e_solves > 0 else 0)):
+        warm = i == 0          # one untimed warm-up call (process-level one-time costs)
         inst_h = eng.ProblemInstance(Xpin, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -379,10 +389,11 @@ def run_ours(args):
             lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP, engine_path=args.engine))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        e2e_iters += r.iterations
-        e2e_time += dt
+        if not warm:
+            e2e_iters += r.iterations
+            e2e_time += dt
         e2e_reps.append({"iterations": r.iterations, "seconds": dt, "rel_gap": r.gap / abs(r.primal_value),
-                         "termination": r.termination.value})
+                         "termination": r.termination.value, "warmup": warm})
         inst_h.release_device()
         del inst_h
     e2e = {"value": e2e_iters / e2e_time if e2e_time > 0 else None, "unit": "iters/s",
@@ -408,6 +419,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
             "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
+            "engine_path": "single_pass" if single else "two_pass",
             "restarts": rep.restarts, "final_gap": rep.gap,
             "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks"),
             "batched_nodes": batched}

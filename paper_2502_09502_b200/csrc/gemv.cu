@@ -238,45 +238,32 @@ __device__ __forceinline__ void k2_accumulate(const EngineArgs& a, const double 
   bool vok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) vok[v] = (v * 32 * VE + lane * VE) < width;
-  // warp w takes rows w, w+8, ...; 2 rows per step for memory parallelism
-  for (int rr = warp; rr < rows; rr += 16) {
-    const int rr2 = rr + 8;
-    typename V::T b0[NV], b1[NV];
-    const bool has2 = rr2 < rows;
+  // warp w takes rows w, w+8, ...; RS rows per step for memory parallelism
+  // (the same bytes in flight per lane for fp64 and fp32)
+  constexpr int RS = sizeof(TX) == 8 ? 2 : 4;
+  for (int rr = warp; rr < rows; rr += 8 * RS) {
+    typename V::T b[RS][NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (vok[v]) {
-        b0[v] = ld_stream(reinterpret_cast<const typename V::T*>(xbase + (int64_t)rr * a.ld + v * 32 * VE));
-        if (has2)
-          b1[v] = ld_stream(reinterpret_cast<const typename V::T*>(xbase + (int64_t)rr2 * a.ld + v * 32 * VE));
+    for (int i = 0; i < RS; ++i) {
+      const int ri = rr + 8 * i;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (vok[v] && ri < rows)
+          b[i][v] = ld_stream(reinterpret_cast<const typename V::T*>(xbase + (int64_t)ri * a.ld + v * 32 * VE));
         else
-          b1[v] = typename V::T{};
-      } else {
-        b0[v] = typename V::T{};
-        b1[v] = typename V::T{};
+          b[i][v] = typename V::T{};
       }
     }
-    {
-      const double rg = WG ? sr[0][rr] : 0.0;
-      const double rz = WZ ? sr[1][rr] : 0.0;
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const int ri = rr + 8 * i;
+      if (ri >= rows) break;
+      const double rg = WG ? sr[0][ri] : 0.0;
+      const double rz = WZ ? sr[1][ri] : 0.0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double x[VE];
-        V::widen(b0[v], x);
-#pragma unroll
-        for (int e = 0; e < VE; ++e) {
-          if (WG) accg[v * VE + e] = fma(x[e], rg, accg[v * VE + e]);
-          if (WZ) accz[v * VE + e] = fma(x[e], rz, accz[v * VE + e]);
-        }
-      }
-    }
-    if (has2) {
-      const double rg = WG ? sr[0][rr2] : 0.0;
-      const double rz = WZ ? sr[1][rr2] : 0.0;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double x[VE];
-        V::widen(b1[v], x);
+        V::widen(b[i][v], x);
 #pragma unroll
         for (int e = 0; e < VE; ++e) {
           if (WG) accg[v * VE + e] = fma(x[e], rg, accg[v * VE + e]);

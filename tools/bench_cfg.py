@@ -42,7 +42,7 @@ for path in ("two_pass", "single_pass"):
     res[path] = r
     print(f"{path}: {iters/(ms/1e3):.1f} it/s ({ms/iters:.3f} ms/it) k1 {st['k1_ms']/max(1,st['k1_count']):.4f} "
           f"k2 {st['k2_ms']/max(1,st['k2_count']):.4f} k3 {st['k3_ms']/max(1,st['k3_count']):.4f} "
-          f"obj {r.primal_value:.12g} dual {r.dual_bound:.12g} cs {st['cluster_size']}", flush=True)
+          f"obj {r.primal_value:.12g} dual {r.dual_bound:.12g} cs {st["cluster_size"]} full_prox {st["prox_full_passes"]} topk_fb {st["topk_fallbacks"]} restarts {r.restarts}", flush=True)
 if len(res) == 2:
     a, b = res["two_pass"], res["single_pass"]
     print("rel obj diff", abs(a.primal_value - b.primal_value) / abs(a.primal_value),
