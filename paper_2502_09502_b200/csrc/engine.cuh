@@ -16,6 +16,9 @@ constexpr int kK1Slab = 2048;
 constexpr int kK2Threads = 256;
 constexpr int kK2Slab = 256;
 constexpr int kK2StageRows = 256;                       // rows of r staged per pass
+// 256-column slabs per K2 work item: fp32 items span two slabs so each row
+// segment a CTA streams is 2 KB, as for fp64
+template <typename TX> constexpr int kK2Cw = sizeof(TX) == 4 ? 2 : 1;
 constexpr int kPvAlign = 2048;                          // p-vector stride alignment
 constexpr int kTargetCtas = 148 * 4;
 constexpr int kHTop = 32;   // per-slab Huber top list (bound checks with k <= 32)

@@ -127,12 +127,13 @@ static int compute_layout(Problem& P) {
   a.k1_grid = (int)std::min<int64_t>(k1_res, (int64_t)a.k1_slabs * a.k1_chunks);
   // K2: 256-column slabs
   a.k2_slabs = (int)ceil_div(p, kK2Slab);
+  const int64_t k2_groups = ceil_div(a.k2_slabs, a.dtype == F32 ? kK2Cw<float> : kK2Cw<double>);
   int64_t k2_res = (int64_t)sms * k2_blocks_per_sm(a.dtype);
-  chunks = std::max<int64_t>(1, ceil_div(k2_res * 8, a.k2_slabs));
+  chunks = std::max<int64_t>(1, ceil_div(k2_res * 8, k2_groups));
   chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, 16)));
   a.k2_rows = ceil_div(n, chunks);
   a.k2_chunks = (int)ceil_div(n, a.k2_rows);
-  a.k2_grid = (int)std::min<int64_t>(k2_res, (int64_t)a.k2_slabs * a.k2_chunks);
+  a.k2_grid = (int)std::min<int64_t>(k2_res, k2_groups * a.k2_chunks);
   a.fused = fused_plan(a, sms) ? 1 : 0;
   P.fused_planned = a.fused;
   if (!a.fused) { a.fz_ncl = 1; a.fz_cs = 1; }
@@ -562,9 +563,12 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   hp.node_mode = node_mode ? 1 : 0;
   hp.loss = a.loss;
   // engine path: auto = the single physical pass where it is measured faster
-  // (fp64 X with a cluster of <= 8 CTAs per row block: C2 1847 vs 1419 it/s),
-  // the two-pass engine otherwise (fp32 X: the transposes dominate)
-  const int auto_fused = P->fused_planned && a.dtype == F64 && a.fz_cs <= 8;
+  // (fp64 X far beyond L2 with a 4..8-CTA cluster per row block: C2 1847 vs
+  // 1419 it/s), the two-pass engine otherwise (fp32 X: the transposes
+  // dominate; small X: L2 serves the second pass)
+  const double x_bytes = (double)a.n * (double)a.ld * 8.0;
+  const int auto_fused = P->fused_planned && a.dtype == F64 && a.fz_cs >= 4 && a.fz_cs <= 8 &&
+                         x_bytes > 512e6;   // L2-resident X (C1): the second pass hits L2
   const int want_fused = (o->engine_path == 2) ? P->fused_planned
                          : (o->engine_path == 1) ? 0 : auto_fused;
   if (o->engine_path == 2 && !P->fused_planned)

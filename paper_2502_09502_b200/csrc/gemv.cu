@@ -221,9 +221,10 @@ __global__ void k_objective(EngineArgs a, int mode) {
 
 // ===========================================================================
 // K2: transpose pass g = X^T r (and v = X^T zeta on bound checks).
-// Persistent CTAs pull (chunk, slab) items; an item is `k2_rows` rows x 256
-// columns.  Each lane owns 8 columns; the 8 warps split the rows and are
-// combined in a fixed order through shared memory.
+// Persistent CTAs pull (chunk, slab group) items; an item is `k2_rows` rows x
+// kK2Cw<TX> slabs of 256 columns (2 for fp32, so every row segment a CTA
+// streams is 2 KB as for fp64).  Each lane owns 8 columns per slab; the 8
+// warps split the rows and are combined in a fixed order through shared memory.
 // ===========================================================================
 template <typename TX, bool WG, bool WZ>
 __device__ __forceinline__ void k2_accumulate(const EngineArgs& a, const double (*sr)[kK2StageRows],
@@ -231,16 +232,16 @@ __device__ __forceinline__ void k2_accumulate(const EngineArgs& a, const double 
                                               int warp, double* accg, double* accz) {
   using V = Vec16<TX>;
   constexpr int VE = V::N;
-  constexpr int NV = 8 / VE;  // vectors per lane per row (8 columns per lane)
+  constexpr int CW = kK2Cw<TX>;
+  constexpr int NV = 8 * CW / VE;  // vectors per lane per row (8 columns per lane per slab)
   const TX* xbase = static_cast<const TX*>(a.X) + s0 * a.ld + col0 + lane * VE;
   // vectors of this lane that lie inside the row (ld is a multiple of VE)
-  const int64_t width = min((int64_t)kK2Slab, a.ld - col0);
+  const int64_t width = min((int64_t)(kK2Slab * CW), a.ld - col0);
   bool vok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) vok[v] = (v * 32 * VE + lane * VE) < width;
   // warp w takes rows w, w+8, ...; RS rows per step for memory parallelism
-  // (the same bytes in flight per lane for fp64 and fp32)
-  constexpr int RS = sizeof(TX) == 8 ? 2 : 4;
+  constexpr int RS = 2;
   for (int rr = warp; rr < rows; rr += 8 * RS) {
     typename V::T b[RS][NV];
 #pragma unroll
@@ -290,10 +291,12 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
                                         K2Smem& sm) {
   using V = Vec16<TX>;
   constexpr int VE = V::N;
-  constexpr int NV = 8 / VE;
+  constexpr int CW = kK2Cw<TX>;
+  constexpr int NV = 8 * CW / VE;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n = a.n;
-  const unsigned items = (unsigned)a.k2_slabs * (unsigned)a.k2_chunks;
+  const int groups = (a.k2_slabs + CW - 1) / CW;
+  const unsigned items = (unsigned)groups * (unsigned)a.k2_chunks;
   int bad = 0;
   for (;;) {
     __syncthreads();
@@ -301,15 +304,15 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
     __syncthreads();
     const unsigned item = sm.item;
     if (item >= items) break;
-    const int chunk = (int)(item / a.k2_slabs), slab = (int)(item % a.k2_slabs);
-    const int64_t col0 = (int64_t)slab * kK2Slab;
+    const int chunk = (int)(item / groups), grp = (int)(item % groups);
+    const int64_t col0 = (int64_t)grp * CW * kK2Slab;
     const int64_t r0 = (int64_t)chunk * a.k2_rows;
     const int64_t r1 = min(n, r0 + a.k2_rows);
-    const bool fst = WZ && mode == MODE_ITER && slab == 0;  // this item owns the F* partial
+    const bool fst = WZ && mode == MODE_ITER && grp == 0;  // this item owns the F* partial
 
-    double accg[8], accz[8];
+    double accg[8 * CW], accz[8 * CW];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { accg[i] = 0.0; accz[i] = 0.0; }
+    for (int i = 0; i < 8 * CW; ++i) { accg[i] = 0.0; accz[i] = 0.0; }
     double facc[3] = {0.0, 0.0, 0.0};
 
     for (int64_t s0 = r0; s0 < r1; s0 += kK2StageRows) {
@@ -343,29 +346,32 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
     }
 
     // ---- combine the 8 warps (fixed order) and publish the item partial -----
+    // (one 256-column slab of the group at a time: lane vectors 2h.. belong to slab h)
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
+    for (int h = 0; h < CW; ++h) {
+      __syncthreads();
 #pragma unroll
-      for (int e = 0; e < VE; ++e) {
-        const int col = v * 32 * VE + lane * VE + e;
-        if (WG) sm.sacc[warp][0][col] = accg[v * VE + e];
-        if (WZ) sm.sacc[warp][1][col] = accz[v * VE + e];
+      for (int v = h * (NV / CW); v < (h + 1) * (NV / CW); ++v) {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          const int col = (v - h * (NV / CW)) * 32 * VE + lane * VE + e;
+          if (WG) sm.sacc[warp][0][col] = accg[v * VE + e];
+          if (WZ) sm.sacc[warp][1][col] = accz[v * VE + e];
+        }
       }
-    }
-    __syncthreads();
-    {
+      __syncthreads();
       const int col = tid;  // 256 threads <-> 256 columns
       if (WG) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += sm.sacc[w][0][col];
-        a.k2_part[(int64_t)chunk * a.pv + col0 + col] = s;
+        a.k2_part[(int64_t)chunk * a.pv + col0 + h * kK2Slab + col] = s;
       }
       if (WZ) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += sm.sacc[w][1][col];
-        a.k2_part[((int64_t)a.k2_chunks + chunk) * a.pv + col0 + col] = s;
+        a.k2_part[((int64_t)a.k2_chunks + chunk) * a.pv + col0 + h * kK2Slab + col] = s;
       }
     }
     if (fst) {
@@ -379,15 +385,18 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
       }
     }
 
-    // ---- last chunk of this slab: reduce over chunks, gradient step ---------
+    // ---- last chunk of this slab group: reduce over chunks, gradient step -----
     __threadfence();
     __syncthreads();
-    if (tid == 0) sm.last = (atomicAdd(cnt_k2_slab(a) + slab, 1u) == (unsigned)(a.k2_chunks - 1));
+    if (tid == 0) sm.last = (atomicAdd(cnt_k2_slab(a) + grp, 1u) == (unsigned)(a.k2_chunks - 1));
     __syncthreads();
     if (!sm.last) continue;
     __threadfence();
-    {
-      const int64_t col = col0 + tid;
+#pragma unroll
+    for (int h = 0; h < CW; ++h) {
+      const int slab = grp * CW + h;
+      if (slab >= a.k2_slabs) break;
+      const int64_t col = (int64_t)slab * kK2Slab + tid;
       double g = 0.0, v = 0.0;
       if (col < a.p) {
         if (WG) {
@@ -403,14 +412,17 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
         }
       }
       // single GPU: the prox's elementwise work for these 256 columns
-      if (mode == MODE_ITER && !a.multi) slab_epilogue(a, slab, t, c, WG, WZ, g, v, sm.epi);
+      if (mode == MODE_ITER && !a.multi) {
+        __syncthreads();
+        slab_epilogue(a, slab, t, c, WG, WZ, g, v, sm.epi);
+      }
     }
-    if (tid == 0) cnt_k2_slab(a)[slab] = 0u;
+    if (tid == 0) cnt_k2_slab(a)[grp] = 0u;
     if (!(WZ && mode == MODE_ITER)) continue;
     // ---- very last slab: F*(-zeta) accumulators over chunks (fixed order) ---
     __threadfence();
     __syncthreads();
-    if (tid == 0) sm.last = (atomicAdd(cnt_k2_all(a), 1u) == (unsigned)(a.k2_slabs - 1));
+    if (tid == 0) sm.last = (atomicAdd(cnt_k2_all(a), 1u) == (unsigned)(groups - 1));
     __syncthreads();
     if (!sm.last) continue;
     __threadfence();
@@ -444,7 +456,7 @@ __device__ __forceinline__ void k2_body(const EngineArgs& a, int mode, int64_t t
 }
 
 template <typename TX>
-__global__ void __launch_bounds__(kK2Threads) k2_transpose(EngineArgs a, int mode) {
+__global__ void __launch_bounds__(kK2Threads, 2) k2_transpose(EngineArgs a, int mode) {
   __shared__ K2Smem sm;
   bool wg = true, wz = false;
   int64_t t = 0;
