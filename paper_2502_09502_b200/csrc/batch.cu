@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
   int bad = 0;
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
   const int64_t r1 = min(n, r0 + kRowsPerBlock);
+  #pragma unroll 4
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
     const double uc = ucur[i];
     const double yi = g.y[i];
@@ -231,10 +232,14 @@ __global__ void __launch_bounds__(kK2Slab) kb_step(BatchArgs g) {
   if (j < g.p) {
     const float* ct = g.ct;
     const int64_t split = 2 * B * g.pp;
-    if (wg)
+    if (wg) {
+#pragma unroll 4
       for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(ct + s * split + b * g.pp + j);
-    if (wz)
+    }
+    if (wz) {
+#pragma unroll 4
       for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(ct + s * split + (B + b) * g.pp + j);
+    }
   }
   if (wz && slab == 0 && threadIdx.x == 0) {
     // F*(-zeta) accumulators over the row blocks (fixed order)
@@ -292,8 +297,10 @@ __global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
   int bad = 0;
   const bool delta = mode == MODE_ITER && !resync_at(t);
   const double* uprev = g.u + (ring(t - 1) * B + b) * nn;
+  #pragma unroll 4
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
     double u = 0.0;
+#pragma unroll 4
     for (int s = 0; s < g.sf; ++s) u += (double)g.cf[s * (B * nn) + b * nn + i];
     if (delta) u = dadd(uprev[i], u);
     if (mode == MODE_ITER) {

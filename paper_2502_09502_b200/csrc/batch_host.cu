@@ -3,6 +3,7 @@
 // advanced in lockstep by CUDA graphs of G iterations; the two X passes of an
 // iteration are tcgen05 contractions over all nodes (tc_gemm.cu).
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -273,9 +274,14 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   TcGemmArgs& gf = Bt->gf;
   gf.M = a.n; gf.N = n_nodes; gf.K = a.p;
   tc_gemm_plan(gf, Bt->sms, 32);
+  if (const char* e = getenv("L0_TC_SF")) {   // tuning override
+    gf.S = std::max(1, atoi(e));
+    gf.units = gf.S * gf.m_tiles * gf.n_tiles;
+  }
   TcGemmArgs& gt = Bt->gt;
   gt.M = a.p; gt.N = n_nodes; gt.K = a.n;
   tc_gemm_plan(gt, Bt->sms, 32);
+  if (const char* e = getenv("L0_TC_ST")) gt.S = std::max(1, atoi(e));
   gt.N = 2 * n_nodes;
   gt.n_tiles = (int)((gt.N + kTcBN - 1) / kTcBN);
   gt.units = gt.S * gt.m_tiles * gt.n_tiles;

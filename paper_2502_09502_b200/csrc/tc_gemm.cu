@@ -86,10 +86,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 struct Unit {
   int s, mt, nt;
 };
-__device__ __forceinline__ Unit decode(const TcGemmArgs& g, int u) {
+// units are numbered over the LIVE n-tiles only (rows of B actually needed,
+// read on the device), so a launch with fewer live rows stays balanced
+__device__ __forceinline__ Unit decode(const TcGemmArgs& g, int nt_live, int u) {
   Unit r;
-  r.nt = u % g.n_tiles;
-  const int rest = u / g.n_tiles;
+  r.nt = u % nt_live;
+  const int rest = u / nt_live;
   r.mt = rest % g.m_tiles;
   r.s = rest / g.m_tiles;
   return r;
@@ -115,6 +117,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_act = g.n_active ? (int64_t)*g.n_active : g.N;
+  const int nt_live = (int)min((int64_t)g.n_tiles, (n_act + kTcBN - 1) / kTcBN);
+  const int units = g.S * g.m_tiles * nt_live;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_ah) : "memory");
@@ -142,7 +146,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto unit_live = [&](const Unit& w) { return (int64_t)w.nt * kTcBN < n_act; };
   auto kb_range = [&](int s, int& kb0, int& kb1) {
     kb0 = (int)(((int64_t)g.kb_total * s) / g.S);
     kb1 = (int)(((int64_t)g.kb_total * (s + 1)) / g.S);
@@ -153,9 +156,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        const Unit w = decode(g, u);
-        if (!unit_live(w)) continue;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = decode(g, nt_live, u);
         int kb0, kb1;
         kb_range(w.s, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -177,9 +179,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int li = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        const Unit w = decode(g, u);
-        if (!unit_live(w)) continue;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = decode(g, nt_live, u);
         const int acc = li & 1;
         bar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1u);
         tc_fence_after();
@@ -211,9 +212,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ===== epilogue: TMEM -> registers -> C (transposed, coalesced along m) =====
     const int q = warp & 3;
     int li = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const Unit w = decode(g, u);
-      if (!unit_live(w)) continue;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = decode(g, nt_live, u);
       const int acc = li & 1;
       bar_wait(&tfull[acc], (li >> 1) & 1);
       tc_fence_after();

@@ -121,3 +121,44 @@ def test_batched_infeasible_node_raises():
     bad = NodeState(fixed_one=tuple(range(inst.k + 1)))
     with pytest.raises(InfeasibleNodeError):
         solve_relaxation_batched(inst, [None, bad], opts=FistaOptions(max_iterations=5, lipschitz=1e3))
+
+
+def test_batched_logistic_fp64_matches_single_solves():
+    """Logistic loss, fp64 X (the contraction is still 3xTF32): per-node
+    results vs the fp64 single solve at the batched tolerance."""
+    from paper_2502_09502_b200 import (FistaOptions, LossKind, NodeState, ProblemInstance,
+                                       lipschitz_constant, solve_relaxation, solve_relaxation_batched)
+    from paper_2502_09502_b200.data import make_config, random_nodes
+    cfg = make_config("C3", scale=0.04)
+    inst = ProblemInstance(cfg.X.astype(np.float64), cfg.y, LossKind.LOGISTIC, cfg.k, cfg.M, cfg.lambda2)
+    nodes = [None] + [NodeState(fixed_one=f1, fixed_zero=f0) for f0, f1 in random_nodes(inst.p, 5, seed=3)]
+    L = lipschitz_constant(inst)
+    opts = FistaOptions(max_iterations=80, stop_on_gap=False, lipschitz=L)
+    reps = solve_relaxation_batched(inst, nodes, opts=opts)
+    for i, nd in enumerate(nodes):
+        ref = solve_relaxation(inst, nd, opts=opts)
+        assert reps[i].iterations == ref.iterations
+        assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5, i
+        assert _rel(reps[i].dual_bound, ref.dual_bound) < 1e-5, i
+
+
+def test_batched_single_node_and_trivial_root():
+    """A batch of one (the root) reproduces the single solve; early primal
+    cutoffs apply per node."""
+    from paper_2502_09502_b200 import (FistaOptions, lipschitz_constant, solve_relaxation,
+                                       solve_relaxation_batched)
+    inst, nodes = _c4_instance(0.05, 4)
+    L = lipschitz_constant(inst)
+    opts = FistaOptions(max_iterations=60, stop_on_gap=False, lipschitz=L)
+    r1 = solve_relaxation_batched(inst, [None], opts=opts)[0]
+    ref = solve_relaxation(inst, None, opts=opts)
+    assert _rel(r1.primal_value, ref.primal_value) < 1e-5
+    # an incumbent cutoff between the nodes' objectives stops some nodes early
+    full = solve_relaxation_batched(inst, nodes, opts=opts)
+    cut = float(np.median([r.primal_value for r in full]))
+    reps = solve_relaxation_batched(inst, nodes, opts=FistaOptions(
+        max_iterations=60, stop_on_gap=False, lipschitz=L, early_primal_cutoff=cut))
+    for r, f in zip(reps, full):
+        if f.primal_value < cut * (1 - 1e-6):
+            assert r.termination.value == "primal_below_incumbent"
+            assert r.iterations <= f.iterations
