@@ -15,8 +15,9 @@ ours       value  = K iterations / device time of a K-iteration solve with X res
                     in pinned host memory (H2D of X and y + D2H of beta inside)
 reference  the CPU oracle port of the reference solver (oracle/l0_oracle.py, numpy +
            C PAVA, all host threads), K iterations of the same workload
-N > 1      rows of X sharded over the ranks (NCCL all-reduce of the gradient); the
-           global problem is fixed, so scaling is "strong".
+N > 1      node sharding (default): each GPU runs its own branch-and-bound node of C2
+           (independent units, no collective, "weak"); --shard rows splits C2's rows
+           over the ranks with the engine's NCCL all-reduce each iteration ("strong").
 """
 
 import argparse
@@ -40,6 +41,7 @@ WORKLOAD = "C2"
 L_C2 = 2.9908e5
 REL_GAP = 1e-6
 TF32_DENSE_PEAK = 1100.0   # TFLOP/s, B200 dense TF32 (B200_PROFILING.md)
+METRIC = "FISTA iters/sec (C2 perspective relaxation; N>1: one branch-and-bound node per GPU)"
 
 
 def log(*a):
@@ -172,9 +174,9 @@ def run_reference(args):
         return
     cd = make_inputs(args.scale)
     cb = cpu_baseline(cd, args.steps, warm=args.warmup)
-    line = {"metric": "FISTA iters/sec (C2, CPU reference solver)", "value": cb["value"],
+    line = {"metric": METRIC, "value": cb["value"],
             "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
             "config": base_config(cd, 1), "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
@@ -301,7 +303,7 @@ def run_batched(args):
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_ours_sharded(args, world, rank, local)
     torch.cuda.set_device(0)
     import paper_2502_09502_b200 as eng
@@ -413,9 +415,10 @@ def run_ours(args):
             log(f"[bench] C4 {batched['value']:.0f} node-it/s {batched['ms_per_iteration_split']}")
         except Exception as exc:   # reported, never silently dropped
             batched = {"error": repr(exc)}
-    line = {"metric": "FISTA iters/sec (C2 root relaxation, HBM-bound GEMV passes)",
+    line = {"metric": METRIC,
             "value": value, "unit": "iters/s", "n_gpus": 1, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "strong" if args.shard == "rows" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
             "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
@@ -427,27 +430,44 @@ def run_ours(args):
 
 
 def run_ours_sharded(args, world, rank, local):
+    """N > 1.  Default (--shard nodes): node sharding, the path's independent
+    units: every rank holds C2's X and runs K iterations of
+    its own branch-and-bound node (rank 0 the root, the others seeded
+    fixed-zero/fixed-one sets), no data-path collective; value = node
+    iterations of all ranks / max-over-ranks device time ("weak").
+    --shard rows: C2's rows split over the ranks with the engine's NCCL
+    all-reduce of the gradient each iteration ("strong")."""
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2502_09502_b200 import distributed as shard
     import paper_2502_09502_b200 as eng
+    from paper_2502_09502_b200 import data
     eng.native.load()
     cd = make_inputs(args.scale)
-    r0, r1 = shard.row_range(cd.n, world, rank)
-    inst = shard.ShardedProblem(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
-                                cd.M, cd.lambda2, n_global=cd.n)
     K, W = args.steps, args.warmup
     opts = lambda it: eng.FistaOptions(lipschitz=L_C2, max_iterations=it, gap_tolerance=1e-300,
-                                       stop_on_gap=False)
-    shard.solve_relaxation_sharded(inst, opts=opts(W))
+                                       stop_on_gap=False, engine_path=args.engine)
+    if args.shard == "rows":
+        r0, r1 = shard.row_range(cd.n, world, rank)
+        inst = shard.ShardedProblem(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
+                                    cd.M, cd.lambda2, n_global=cd.n)
+        solve = lambda it: shard.solve_relaxation_sharded(inst, opts=opts(it))
+        scaling, units_per_step, par = "strong", 1, "rows%d" % world
+    else:
+        inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+        sets = data.random_nodes(cd.p, world, seed=1)
+        node = None if rank == 0 else eng.NodeState(fixed_one=sets[rank][1], fixed_zero=sets[rank][0])
+        solve = lambda it: eng.solve_relaxation(inst, node, opts=opts(it), return_device=True)
+        scaling, units_per_step, par = "weak", world, "nodes%d" % world
+    solve(W)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
-    rep = shard.solve_relaxation_sharded(inst, opts=opts(K))
+    rep = solve(K)
     end.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -455,13 +475,18 @@ def run_ours_sharded(args, world, rank, local):
     ms = torch.tensor([start.elapsed_time(end)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    launches = torch.tensor([float(rep.stats["gpu_launches"])], device="cuda")
+    dist.all_reduce(launches)
     if rank == 0:
-        line = {"metric": "FISTA iters/sec (C2 root relaxation, rows sharded)",
-                "value": K / (ms / 1e3), "unit": "iters/s", "n_gpus": world, "steps": K,
-                "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (reference generator, seed 0)",
-                "config": base_config(cd, world), "gpu_launches": int(rep.stats["gpu_launches"])}
+        cfg = base_config(cd, world)
+        cfg["parallelism"] = par
+        line = {"metric": METRIC,
+                "value": units_per_step * K / (ms / 1e3), "unit": "iters/s", "n_gpus": world,
+                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference generator, seed 0)", "config": cfg,
+                "gpu_launches": int(launches.item()),
+                "engine_path": "single_pass" if rep.stats.get("single_pass") else "two_pass"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -477,6 +502,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", default="auto", choices=["auto", "two_pass", "single_pass"])
+    ap.add_argument("--force-dist", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--shard", default="nodes", choices=["nodes", "rows"],
+                    help="N > 1: independent node relaxations per GPU (weak) or C2's rows (strong)")
     ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
     ap.add_argument("--c4-steps", type=int, default=50)
     ap.add_argument("--c4-scale", type=float, default=1.0)
