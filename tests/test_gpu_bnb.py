@@ -1,0 +1,72 @@
+"""Branch-and-bound on the batched engine vs the spec's examples and an
+enumeration oracle (oracle/bnb_oracle.py)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _inst(X, y, k, M, lam2):
+    from paper_2502_09502_b200 import LossKind, ProblemInstance
+    return ProblemInstance(np.asarray(X, dtype=np.float64), np.asarray(y, dtype=np.float64),
+                           LossKind.SQUARED_ERROR, k, M, lam2)
+
+
+def test_beam_search_spec_example():
+    # X = I2, y = (3, 1), lambda2 = 1, M = 10, k = 1 -> support {first}, 1.5, 5.5
+    from paper_2502_09502_b200.bnb import beam_search_incumbent
+    beta, obj = beam_search_incumbent(_inst(np.eye(2), [3.0, 1.0], 1, 10.0, 1.0), beam_width=2)
+    assert np.flatnonzero(beta).tolist() == [0]
+    assert beta[0] == pytest.approx(1.5, rel=1e-9)
+    assert obj == pytest.approx(5.5, rel=1e-9)
+
+
+def test_branching_spec_example():
+    # incumbent (1.5, 0.5), k = 2 -> the first coordinate
+    from paper_2502_09502_b200.bnb import select_branching_variable
+    from paper_2502_09502_b200 import NodeState
+    inst = _inst(np.eye(2), [3.0, 1.0], 2, 10.0, 1.0)
+    assert select_branching_variable(inst, None, np.array([1.5, 0.5])) == 0
+    assert select_branching_variable(inst, NodeState(fixed_one=(0, 1)), np.array([1.5, 0.5])) is None
+
+
+def test_certify_one_dimensional():
+    # X = [[1]], y = (1), k = 1, M = 2, lambda2 = 1 -> optimal 0.5, one node
+    from paper_2502_09502_b200.bnb import CertificateStatus, certify
+    cert = certify(_inst([[1.0]], [1.0], 1, 2.0, 1.0))
+    assert cert.status is CertificateStatus.OPTIMAL
+    assert cert.incumbent_objective == pytest.approx(0.5, rel=1e-9)
+    assert cert.nodes_explored == 1
+    assert cert.global_lower_bound <= cert.incumbent_objective + 1e-9
+
+
+def test_certify_k_equals_p_is_one_node():
+    # k = p, M large -> the root relaxation is integral
+    from paper_2502_09502_b200.bnb import CertificateStatus, certify
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((30, 6))
+    y = X @ rng.standard_normal(6) + 0.1 * rng.standard_normal(30)
+    cert = certify(_inst(X, y, 6, 100.0, 0.5))
+    assert cert.status is CertificateStatus.OPTIMAL
+    assert cert.nodes_explored == 1
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_certify_matches_enumeration(seed):
+    # 20 random instances p=8, n=20, k=2 -> enumeration optimum, Optimal
+    from oracle.bnb_oracle import best_subset
+    from paper_2502_09502_b200.bnb import BnBOptions, CertificateStatus, certify
+    rng = np.random.default_rng(100 + seed)
+    X = rng.standard_normal((20, 8))
+    bt = np.zeros(8)
+    bt[rng.choice(8, 2, replace=False)] = rng.choice([-1.0, 1.0], 2) * rng.uniform(0.5, 1.5, 2)
+    y = X @ bt + 0.3 * rng.standard_normal(20)
+    k, M, lam2 = 2, 20.0, 0.3
+    obj, beta, S = best_subset(X, y, k, lam2, M)
+    cert = certify(_inst(X, y, k, M, lam2), BnBOptions(gap_tolerance=1e-7, batch_size=8))
+    assert cert.status is CertificateStatus.OPTIMAL
+    assert cert.incumbent_objective == pytest.approx(obj, rel=1e-7, abs=1e-9)
+    assert tuple(np.flatnonzero(np.abs(cert.incumbent_beta) > 1e-9)) == S
+    # soundness: the certified bound never exceeds the true optimum
+    assert cert.global_lower_bound <= obj + 1e-7 * abs(obj)
