@@ -343,7 +343,10 @@ __device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t k
 }
 
 // Fenchel bound from the slab epilogue's products (fista.py:150-157).  With
-// k <= 32 the top-k Huber values are among the per-slab top-32 lists.
+// k <= 32 the top-k Huber values are among the per-slab top-32 lists; their
+// top-k sum is a radix selection over those lists (the bitonic sort of all of
+// them is kept behind a constant for comparison).
+constexpr bool kSortHtopLists = false;
 __device__ int dual_step_slabs(const EngineArgs& a, ProxSmem& ps, WinSmem& ws) {
   const Params* P = a.prm;
   State* st = a.st;
@@ -362,7 +365,7 @@ __device__ int dual_step_slabs(const EngineArgs& a, ProxSmem& ps, WinSmem& ws) {
     const int64_t nfree = node ? P->n_free : p;
     double top;
     const int64_t m = (int64_t)S * kHTop;
-    if (kg <= kHTop && m <= kWinCap) {
+    if (kg <= kHTop && m <= kWinCap && kSortHtopLists) {
       // the global top-kg is among the per-slab top-32 lists: sort them
       const int n = pow2_at_least(m > 2 ? (int)m : 2);
       for (int i = threadIdx.x; i < n; i += blockDim.x) {

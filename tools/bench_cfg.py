@@ -13,8 +13,9 @@ iters = int(sys.argv[3]) if len(sys.argv) > 3 else 100
 t0 = time.time()
 cd = data.make_config(name, scale=scale)
 inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype=cd.dtype)
-Xd = torch.from_numpy(cd.X).cuda().double()
-v = torch.randn(Xd.shape[1], device="cuda", dtype=torch.float64)
+Xd = torch.from_numpy(cd.X).cuda()
+Xd = Xd.double() if Xd.numel() < 2e9 else Xd          # fp32 power iteration for huge X
+v = torch.randn(Xd.shape[1], device="cuda", dtype=Xd.dtype)
 for _ in range(300):                    # power iteration (the reference's 500-it cap fails here)
     w = Xd.T @ (Xd @ v)
     lam = float(w.norm())
@@ -24,7 +25,8 @@ torch.cuda.empty_cache()
 L = {"squared_error": 2.0, "logistic": 0.25}[cd.loss] * lam * 1.05
 print(f"{name} n={cd.n} p={cd.p} {cd.dtype} {cd.loss} gen+L {time.time()-t0:.1f}s L={L:.6g}", flush=True)
 res = {}
-for path in ("two_pass", "single_pass"):
+paths = sys.argv[4].split(",") if len(sys.argv) > 4 else ["two_pass", "single_pass"]
+for path in paths:
     o = lambda k: eng.FistaOptions(lipschitz=L, max_iterations=k, stop_on_gap=False, gap_tolerance=1e-300,
                                    engine_path=path, profile=True)
     try:

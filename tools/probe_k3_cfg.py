@@ -1,6 +1,6 @@
 """K3 phase timing for any config (build with L0_PROBE=1):
 python tools/probe_k3_cfg.py C3 [scale]"""
-import ctypes, sys
+import ctypes, os, sys
 sys.path.insert(0, ".")
 import torch
 import paper_2502_09502_b200 as eng
@@ -17,7 +17,7 @@ del Xd
 L = {"squared_error": 2.0, "logistic": 0.25}[cd.loss] * lam * 1.05
 names = ["start", "dual", "gather+offs", "merge", "append", "search", "->scatter", "scatter", "g+theta"]
 for its in (2, 5, 11, 23, 40, 80):
-    rep = eng.solve_relaxation(inst, opts=eng.FistaOptions(lipschitz=L, max_iterations=its, engine_path="two_pass",
+    rep = eng.solve_relaxation(inst, opts=eng.FistaOptions(lipschitz=L, max_iterations=its, engine_path=os.environ.get("ENGINE", "two_pass"),
                                gap_tolerance=1e-300, stop_on_gap=False, chunk_iterations=1))
     buf = (ctypes.c_int64 * 16)()
     eng.native.lib().l0_debug_probe(inst.device_problem().handle, buf)
