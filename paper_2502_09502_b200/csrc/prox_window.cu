@@ -302,6 +302,43 @@ __device__ void sort_window_regs(WinSmem& sm, int cnt) {
   __syncthreads();
 }
 
+// Large windows: each warp sorts a run of 32 * E pairs in registers (shuffles
+// only), then the kWinThreads / 32 sorted runs are merged by co-ranking
+// (sortnet.cuh merge_runs) -- far fewer block barriers than a block bitonic.
+template <int E>
+__device__ void sort_window_runs(WinSmem& sm, int cnt) {
+  constexpr int RUN = 32 * E;
+  constexpr int NW = kWinThreads / 32;
+  static_assert(RUN * NW == kWinCap, "runs cover the window");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double k[E];
+  int id[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int s = warp * RUN + e * 32 + lane;
+    k[e] = s < cnt ? sm.wkey[s] : -CUDART_INF;
+    id[e] = s < cnt ? sm.widx[s] : INT_MAX - s;   // distinct: the co-rank merge needs a strict order
+  }
+  __syncthreads();
+  bitonic_warp<E>(k, id, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int s = warp * RUN + e * 32 + lane;
+    sm.wkey[s] = k[e];
+    sm.widx[s] = id[e];
+  }
+  if (threadIdx.x <= NW) sm.u.hist[threadIdx.x] = (unsigned)(threadIdx.x * RUN);
+  __syncthreads();
+  const int res = merge_runs(sm.wkey, sm.widx, sm.mkey, sm.midx, sm.u.hist, NW, kWinCap);
+  if (res) {
+    for (int s = threadIdx.x; s < cnt; s += kWinThreads) {
+      sm.wkey[s] = sm.mkey[s];
+      sm.widx[s] = sm.midx[s];
+    }
+  }
+  __syncthreads();
+}
+
 __device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t kk, double* carry,
                             WinSmem& sm, bool presorted = false) {
   const int tid = threadIdx.x;
@@ -309,7 +346,7 @@ __device__ void sort_append(const EngineArgs& a, int cnt, int64_t len, int64_t k
     if (cnt <= kWinThreads) sort_window_regs<1>(sm, cnt);
     else if (cnt <= 2 * kWinThreads) sort_window_regs<2>(sm, cnt);
     else if (cnt <= 4 * kWinThreads) sort_window_regs<4>(sm, cnt);
-    else sort_window_regs<8>(sm, cnt);
+    else sort_window_runs<8>(sm, cnt);
   }
   // tail prefix sums: blocked ranges of kWinIpt positions per thread
   double loc = 0.0;

@@ -102,6 +102,48 @@ __device__ void bitonic_regs(double (&k)[E], int (&id)[E], double* sk, int* si) 
   }
 }
 
+// Warp-level bitonic sort of 32 * E pairs held E per lane (element e of lane
+// l is run position e * 32 + l): strides < 32 through shuffles, strides >= 32
+// inside the lane; no shared memory, no block barriers.
+template <int E>
+__device__ __forceinline__ void bitonic_warp(double (&k)[E], int (&id)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll 1
+  for (int kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int je = j >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+#pragma unroll
+          for (int e2 = e + 1; e2 < E; ++e2) {
+            if ((e ^ e2) == je) {
+              const int i = e * 32 + lane;
+              const bool dir = (i & kk) == 0;
+              const bool ord = precedes(k[e], id[e], k[e2], id[e2]);
+              if (dir != ord) {
+                const double tk = k[e]; k[e] = k[e2]; k[e2] = tk;
+                const int ti = id[e]; id[e] = id[e2]; id[e2] = ti;
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = e * 32 + lane;
+          const double pk = __shfl_xor_sync(0xffffffffu, k[e], j);
+          const int pi = __shfl_xor_sync(0xffffffffu, id[e], j);
+          const bool first = precedes(k[e], id[e], pk, pi);
+          const bool lo = (i & j) == 0, dir = (i & kk) == 0;
+          if ((lo == dir) != first) { k[e] = pk; id[e] = pi; }
+        }
+      }
+    }
+  }
+}
+
 // Number of elements of the sorted run [lo, hi) that precede (k, i).
 __device__ __forceinline__ int count_preceding(const double* key, const int* idx, int lo, int hi,
                                                double k, int i) {
