@@ -127,32 +127,62 @@ __global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
   const int64_t n = g.n, nn = g.nn, B = g.B;
   const double* ucur = g.u + (ring(t - 1) * B + b) * nn;
   const double* uprev = g.u + (ring(t - 2) * B + b) * nn;
+  float* rh = g.rh + b * nn;
+  float* rl = g.rl + b * nn;
+  float* zh = g.rh + (B + b) * nn;
+  float* zl = g.rl + (B + b) * nn;
   double facc[3] = {0.0, 0.0, 0.0};
   int bad = 0;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
-  const int64_t r1 = min(n, r0 + kRowsPerBlock);
-  #pragma unroll 4
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
-    const double uc = ucur[i];
-    const double yi = g.y[i];
-    if (wg) {
-      // X gamma = u_t + c (u_t - u_{t-1})   (linearity; fista.py:161-162)
-      const double ug = dadd(uc, dmul(c, dsub(uc, uprev[i])));
-      if (!isfinite(ug)) bad = 1;
-      float h, l;
-      tf32_split(loss_grad(g.loss, ug, yi), h, l);
-      g.rh[b * nn + i] = h;
-      g.rl[b * nn + i] = l;
+  const int r0 = blockIdx.x * kRowsPerBlock;
+  const int r1 = (int)min(n, (int64_t)r0 + kRowsPerBlock);
+  // two rows per thread per step (16-byte loads; nn and r0 are even)
+  auto row = [&](double uc, double up, double yi, double& gr, double& zv) {
+    // X gamma = u_t + c (u_t - u_{t-1})   (linearity; fista.py:161-162)
+    const double ug = dadd(uc, dmul(c, dsub(uc, up)));
+    if (!isfinite(ug)) bad = 1;
+    gr = loss_grad(g.loss, ug, yi);
+    zv = -loss_grad(g.loss, uc, yi);              // zeta = -grad F(u) (fista.py:152)
+  };
+#pragma unroll 2
+  for (int i = r0 + 2 * (int)threadIdx.x; i < r1; i += 2 * kRowThreads) {
+    const bool two = i + 1 < r1;
+    double uc[2], up[2], yi[2];
+    if (two) {
+      const double2 a2 = *reinterpret_cast<const double2*>(ucur + i);
+      const double2 b2 = *reinterpret_cast<const double2*>(uprev + i);
+      const double2 y2 = *reinterpret_cast<const double2*>(g.y + i);
+      uc[0] = a2.x; uc[1] = a2.y; up[0] = b2.x; up[1] = b2.y; yi[0] = y2.x; yi[1] = y2.y;
+    } else {
+      uc[0] = ucur[i]; up[0] = uprev[i]; yi[0] = g.y[i];
+      uc[1] = 0.0; up[1] = 0.0; yi[1] = 0.0;
     }
-    if (wz) {
-      const double z = -loss_grad(g.loss, uc, yi);  // zeta = -grad F(u) (fista.py:152)
-      float h, l;
-      tf32_split(z, h, l);
-      g.rh[(B + b) * nn + i] = h;
-      g.rl[(B + b) * nn + i] = l;
-      conj_accumulate(g.loss, z, yi, facc);
+    float gh[2], gl[2], zh2[2], zl2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+      double gr = 0.0, zv = 0.0;
+      row(uc[h], up[h], yi[h], gr, zv);
+      tf32_split(gr, gh[h], gl[h]);
+      if (wz) {
+        tf32_split(zv, zh2[h], zl2[h]);
+        conj_accumulate(g.loss, zv, yi[h], facc);
+      }
+    }
+    if (two) {
+      if (wg) {
+        *reinterpret_cast<float2*>(rh + i) = make_float2(gh[0], gh[1]);
+        *reinterpret_cast<float2*>(rl + i) = make_float2(gl[0], gl[1]);
+      }
+      if (wz) {
+        *reinterpret_cast<float2*>(zh + i) = make_float2(zh2[0], zh2[1]);
+        *reinterpret_cast<float2*>(zl + i) = make_float2(zl2[0], zl2[1]);
+      }
+    } else {
+      if (wg) { rh[i] = gh[0]; rl[i] = gl[0]; }
+      if (wz) { zh[i] = zh2[0]; zl[i] = zl2[0]; }
     }
   }
+  if (!wg) bad = 0;
   if (wz) {
     const double f0 = block_sum(facc[0], red);
     const double f1 = block_sum(facc[1], red);
@@ -297,20 +327,49 @@ __global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
   int bad = 0;
   const bool delta = mode == MODE_ITER && !resync_at(t);
   const double* uprev = g.u + (ring(t - 1) * B + b) * nn;
-  #pragma unroll 4
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kRowThreads) {
-    double u = 0.0;
-#pragma unroll 4
-    for (int s = 0; s < g.sf; ++s) u += (double)g.cf[s * (B * nn) + b * nn + i];
-    if (delta) u = dadd(uprev[i], u);
-    if (mode == MODE_ITER) {
-      g.u[(ring(t) * B + b) * nn + i] = u;
+  double* uo = g.u + ((mode == MODE_ITER ? ring(t) : 0) * B + b) * nn;
+  double* uo2 = g.u + (2 * B + b) * nn;           // MODE_INIT: u_{-1} = u_0
+  const float* cfb = g.cf + b * nn;
+  const int64_t cstride = B * nn;
+  const int sf = g.sf;
+  const int i0 = (int)r0, i1 = (int)r1;
+  // two rows per thread per step (16-byte loads; nn and r0 are even)
+#pragma unroll 1
+  for (int i = i0 + 2 * (int)threadIdx.x; i < i1; i += 2 * kRowThreads) {
+    const bool two = i + 1 < i1;
+    double u[2] = {0.0, 0.0}, yv[2], upv[2] = {0.0, 0.0};
+    if (two) {
+      for (int s = 0; s < sf; ++s) {
+        const float2 c2 = *reinterpret_cast<const float2*>(cfb + s * cstride + i);
+        u[0] += (double)c2.x;
+        u[1] += (double)c2.y;
+      }
+      const double2 y2 = *reinterpret_cast<const double2*>(g.y + i);
+      yv[0] = y2.x; yv[1] = y2.y;
+      if (delta) {
+        const double2 p2 = *reinterpret_cast<const double2*>(uprev + i);
+        upv[0] = p2.x; upv[1] = p2.y;
+      }
     } else {
-      g.u[(0 * B + b) * nn + i] = u;
-      g.u[(2 * B + b) * nn + i] = u;
+      for (int s = 0; s < sf; ++s) u[0] += (double)cfb[s * cstride + i];
+      yv[0] = g.y[i];
+      yv[1] = 0.0;
+      if (delta) upv[0] = uprev[i];
     }
-    if (!isfinite(u)) bad = 1;
-    lsum += loss_term(g.loss, u, g.y[i]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+      if (delta) u[h] = dadd(upv[h], u[h]);
+      if (!isfinite(u[h])) bad = 1;
+      lsum += loss_term(g.loss, u[h], yv[h]);
+    }
+    if (two) {
+      *reinterpret_cast<double2*>(uo + i) = make_double2(u[0], u[1]);
+      if (mode != MODE_ITER) *reinterpret_cast<double2*>(uo2 + i) = make_double2(u[0], u[1]);
+    } else {
+      uo[i] = u[0];
+      if (mode != MODE_ITER) uo2[i] = u[0];
+    }
   }
   const double csum = block_sum(lsum, red);
   const int anybad = __syncthreads_or(bad);
