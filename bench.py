@@ -506,7 +506,7 @@ def main():
     ap.add_argument("--shard", default="nodes", choices=["nodes", "rows"],
                     help="N > 1: independent node relaxations per GPU (weak) or C2's rows (strong)")
     ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
-    ap.add_argument("--c4-steps", type=int, default=50)
+    ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--c4-scale", type=float, default=1.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
