@@ -42,7 +42,8 @@ namespace l0 {
 
 constexpr int kFzMaxRows = 8;
 constexpr int kFzMaxCs = 16;
-constexpr int kFzSlots = 8;    // partial-slot ring (2 x the forward lead, see flow control)
+constexpr int kFzSlots = 16;   // partial-slot ring (2 x the forward lead, see flow control)
+constexpr int kFzTB = 4;       // tiles per transpose step
 // vectors (16 B) per thread per row: 8 fp64 or 12 fp32 columns per thread,
 // i.e. 24 / 36 fp64 accumulators for the three right-hand sides
 template <typename TX> constexpr int fz_maxv() { return sizeof(TX) == 8 ? 4 : 3; }
@@ -154,7 +155,7 @@ struct FzShared {
   double up[kFzSlots][kFzMaxRows];
   double sy[kFzMaxStages][kFzMaxRows];      // y / u_{t-1} of a stage's rows (bulk copies
   double su[kFzMaxStages][kFzMaxRows];      // under the stage's barrier)
-  double rr[3][kFzMaxRows];                 // r_R, r_N, zeta of the transpose group's tile
+  double rr[3][kFzTB * kFzMaxRows];         // r_R, r_N, zeta of the transpose group's step
   double red[32];
   int bad;
 };
@@ -352,80 +353,116 @@ __global__ void __launch_bounds__(kFzBlock, 1) kf_fused(EngineArgs a, int mode) 
     }
   } else {
     // ===================== transpose group =====================
+    // steps of kFzTB tiles: one gather and two barriers per step; the step's
+    // rows stream from L2 in double-buffered pairs (the loads of the next
+    // pair are in flight while the current pair is accumulated)
     const int lt = tid - kFzFwd;
 #pragma unroll
     for (int i = 0; i < NV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
     const TX* xcols = static_cast<const TX*>(a.X) + c0;
-    // the tile's rows from L2 into registers first (independent of r)
-    typename V::T xv[R][NV];
-    for (int k = 0; k < mytiles; ++k) {
-      const int64_t tile = tile_of(k);
-      const int rows = tile_rows(k);
-      const int q = k % kFzSlots;
+    constexpr int RT = kFzTB * R;                 // rows per step
+    static_assert(RT % 4 == 0, "rows per step");
+    auto row_ok = [&](int k0, int nt, int rho) {
+      const int i = rho / R;
+      return i < nt && (rho % R) < tile_rows(k0 + i);
+    };
+    auto load_pair = [&](int k0, int nt, int g, typename V::T (&dst)[2][NV]) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+      for (int h = 0; h < 2; ++h) {
+        const int rho = 2 * g + h;
+        const bool ok = row_ok(k0, nt, rho);
+        const int64_t row = tile_of(k0 + rho / R) * R + rho % R;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int col = v * kFzTr * VE + lt * VE;
-          if (r < rows && col < wvalid)
-            xv[r][v] = __ldg(reinterpret_cast<const typename V::T*>(xcols + (tile * R + r) * ld + col));
+          if (ok && col < wvalid)
+            dst[h][v] = __ldg(reinterpret_cast<const typename V::T*>(xcols + row * ld + col));
           else
-            xv[r][v] = typename V::T{};
+            dst[h][v] = typename V::T{};
         }
       }
-      mbar_wait_cluster(&sh.xb[q], (uint32_t)((k / kFzSlots) & 1));
-      if (lt == 0) FZ_STAMP(a, k, 2);
-      if (lt < rows) {
-        double u = 0.0;
-        for (int c = 0; c < cs; ++c) u += sh.part[q][c][lt];
-        const int64_t row = tile * R + lt;
-        const double yi = sh.yv[q][lt];
-        const double up = (mode == MODE_ITER) ? sh.up[q][lt] : u;
-        const double dlt = dsub(u, up);
-        const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
-        const double ugN = dadd(u, dmul(cN, dlt));
-        if (!isfinite(ugR)) gbad_R = 1;
-        if (!isfinite(ugN)) gbad_N = 1;
-        sh.rr[0][lt] = loss_grad(a.loss, ugR, yi);
-        sh.rr[1][lt] = loss_grad(a.loss, ugN, yi);
-        const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
-        sh.rr[2][lt] = z;
-        if (crank == 0) {
-          if (mode == MODE_ITER) {
-            a.u[ring(t) * n + row] = u;
-          } else {
-            a.u[row] = u;
-            a.u[2 * n + row] = u;
+    };
+    auto fma_pair = [&](int g, const typename V::T (&src)[2][NV]) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rho = 2 * g + h;
+        const double rR = sh.rr[0][rho], rN = sh.rr[1][rho], rZ = sh.rr[2][rho];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double x[VE];
+          V::widen(src[h][v], x);
+#pragma unroll
+          for (int e = 0; e < VE; ++e) {
+            accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
+            accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+            if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
           }
-          if (!isfinite(u)) bad = 1;
-          loss_acc += loss_term(a.loss, u, yi);
-          if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
         }
+      }
+    };
+    for (int k0 = 0; k0 < mytiles; k0 += kFzTB) {
+      const int nt = min(kFzTB, mytiles - k0);
+      typename V::T xa[2][NV], xb2[2][NV];
+      for (int i = 0; i < nt; ++i) {
+        const int k = k0 + i;
+        mbar_wait_cluster(&sh.xb[k % kFzSlots], (uint32_t)((k / kFzSlots) & 1));
+      }
+      load_pair(k0, nt, 0, xa);                  // first pair's latency overlaps the gather
+      if (lt == 0) FZ_STAMP(a, k0, 2);
+      if (lt < RT) {
+        const int i = lt / R, r = lt % R;
+        double gR = 0.0, gN = 0.0, gZ = 0.0;
+        if (i < nt && r < tile_rows(k0 + i)) {
+          const int k = k0 + i;
+          const int q = k % kFzSlots;
+          double u = 0.0;
+          for (int c = 0; c < cs; ++c) u += sh.part[q][c][r];
+          const int64_t row = tile_of(k) * R + r;
+          const double yi = sh.yv[q][r];
+          const double up = (mode == MODE_ITER) ? sh.up[q][r] : u;
+          const double dlt = dsub(u, up);
+          const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
+          const double ugN = dadd(u, dmul(cN, dlt));
+          if (!isfinite(ugR)) gbad_R = 1;
+          if (!isfinite(ugN)) gbad_N = 1;
+          gR = loss_grad(a.loss, ugR, yi);
+          gN = loss_grad(a.loss, ugN, yi);
+          const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
+          gZ = z;
+          if (crank == 0) {
+            if (mode == MODE_ITER) {
+              a.u[ring(t) * n + row] = u;
+            } else {
+              a.u[row] = u;
+              a.u[2 * n + row] = u;
+            }
+            if (!isfinite(u)) bad = 1;
+            loss_acc += loss_term(a.loss, u, yi);
+            if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
+          }
+        }
+        sh.rr[0][lt] = gR;
+        sh.rr[1][lt] = gN;
+        sh.rr[2][lt] = gZ;
       }
       named_sync(2, kFzTr);
-      // slot q consumed: arm it for tile k + kFzSlots
-      if (lt == 0 && k + kFzSlots < mytiles) mbar_arrive_expect(&sh.xb[q], slot_bytes(k + kFzSlots));
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double rR = sh.rr[0][r], rN = sh.rr[1][r], rZ = sh.rr[2][r];
-        if (r < rows) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double x[VE];
-            V::widen(xv[r][v], x);
-#pragma unroll
-            for (int e = 0; e < VE; ++e) {
-              accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-              accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
-              if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
-            }
-          }
+      // the step's slots are consumed: arm them for the tiles kFzSlots later
+      if (lt == 0)
+        for (int i = 0; i < nt; ++i) {
+          const int k = k0 + i;
+          if (k + kFzSlots < mytiles) mbar_arrive_expect(&sh.xb[k % kFzSlots], slot_bytes(k + kFzSlots));
         }
+#pragma unroll
+      for (int g = 0; g < RT / 2; g += 2) {
+        load_pair(k0, nt, g + 1, xb2);
+        fma_pair(g, xa);
+        if (g + 2 < RT / 2) load_pair(k0, nt, g + 2, xa);
+        fma_pair(g + 1, xb2);
       }
       named_sync(2, kFzTr);      // rr reusable
       if (lt == 0) {
-        FZ_STAMP(a, k, 3);
-        mbar_arrive(&sh.tfree[k % kFzLead]);
+        FZ_STAMP(a, k0, 3);
+        for (int i = 0; i < nt; ++i) mbar_arrive(&sh.tfree[(k0 + i) % kFzLead]);
       }
     }
   }
