@@ -23,6 +23,6 @@ for its in (2, 5, 11, 23, 40, 80):
     eng.native.lib().l0_debug_probe(inst.device_problem().handle, buf)
     v = list(buf)
     d = [(names[i], (v[i] - v[i - 1]) / 1.965e3) for i in range(1, 9) if v[i] and v[i - 1]]
-    extra = f" sort-in-append {(v[9] - v[3]) / 1.965e3:.1f}us" if v[9] and v[3] else ""
+    extra = ""
     print(its, extra, {k: rep.stats[k] for k in ("prox_full_passes", "topk_fallbacks")},
           [(n, round(x, 2)) for n, x in d], "total us", round((v[8] - v[0]) / 1.965e3, 1), flush=True)
