@@ -56,7 +56,9 @@ struct BatchArgs {
   double* fpart;    // [B][rblocks][4]
   double* lpart;    // [B][rblocks][2]
   unsigned* cnt;    // [B] (zero between launches)
-  int* flags;       // [0] alive, [1] any zeta, [2] GEMM_T rows, [3] GEMM_F rows, [4] done count
+  int* flags;       // [0] alive, [1] any zeta, [2] GEMM_T rows, [3] GEMM_F rows, [4] done count,
+                    // [5] active nodes this iteration
+  int* slot;        // [B] row of node b in the contractions this iteration (-1: finished)
   int rblocks;      // row blocks of kb_rhs / kb_obj
   // per-node slab epilogue products (slab_epilogue.cuh), S slabs of kK2Slab columns
   int S;
@@ -110,6 +112,35 @@ __global__ void kb_state_init(BatchArgs g) {
   st->slow_prox = 0;
 }
 
+// Contraction rows for this iteration: the unfinished nodes, compacted in
+// node order (finished nodes drop out of both contractions)
+__global__ void __launch_bounds__(1024) kb_compact(BatchArgs g) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < g.B; b0 += 1024) {
+    const int64_t b = b0 + threadIdx.x;
+    const int act = (b < g.B && !g.st[b].done) ? 1 : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    const int before = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[warp] = __popc(m);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < warp; ++w) off += warp_tot[w];
+    if (b < g.B) g.slot[b] = act ? off + before : -1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < 32; ++w) tot += warp_tot[w];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) g.flags[5] = base;
+}
+
 // R / Z rows of node blockIdx.y for rows [blockIdx.x * kRowsPerBlock, ...)
 __global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
   __shared__ double red[32];
@@ -127,10 +158,12 @@ __global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
   const int64_t n = g.n, nn = g.nn, B = g.B;
   const double* ucur = g.u + (ring(t - 1) * B + b) * nn;
   const double* uprev = g.u + (ring(t - 2) * B + b) * nn;
-  float* rh = g.rh + b * nn;
-  float* rl = g.rl + b * nn;
-  float* zh = g.rh + (B + b) * nn;
-  float* zl = g.rl + (B + b) * nn;
+  // compacted contraction rows: R at slot, Z at (active count) + slot
+  const int64_t pos = g.slot[b], nact = g.flags[5];
+  float* rh = g.rh + pos * nn;
+  float* rl = g.rl + pos * nn;
+  float* zh = g.rh + (nact + pos) * nn;
+  float* zl = g.rl + (nact + pos) * nn;
   double facc[3] = {0.0, 0.0, 0.0};
   int bad = 0;
   const int r0 = blockIdx.x * kRowsPerBlock;
@@ -203,9 +236,9 @@ __global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
 }
 
 __global__ void kb_plan(BatchArgs g) {
-  const int alive = g.flags[0], anyz = g.flags[1];
-  g.flags[2] = alive ? (int)(anyz ? 2 * g.B : g.B) : 0;
-  g.flags[3] = alive ? (int)g.B : 0;
+  const int alive = g.flags[0], anyz = g.flags[1], nact = g.flags[5];
+  g.flags[2] = alive ? (anyz ? 2 * nact : nact) : 0;
+  g.flags[3] = alive ? nact : 0;
   g.flags[0] = 0;
   g.flags[1] = 0;
 }
@@ -257,6 +290,7 @@ __global__ void __launch_bounds__(kK2Slab) kb_step(BatchArgs g) {
   const int64_t t = st->t + 1;
   const double c = momentum(st->phi);
   const int64_t B = g.B, pv = g.pv;
+  const int64_t pos = g.slot[b], nact = g.flags[5];   // compacted contraction rows
   const int64_t j = (int64_t)slab * kK2Slab + threadIdx.x;
   double gsum = 0.0, v = 0.0;
   if (j < g.p) {
@@ -264,11 +298,11 @@ __global__ void __launch_bounds__(kK2Slab) kb_step(BatchArgs g) {
     const int64_t split = 2 * B * g.pp;
     if (wg) {
 #pragma unroll 4
-      for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(ct + s * split + b * g.pp + j);
+      for (int s = 0; s < g.sct; ++s) gsum += (double)__ldcg(ct + s * split + pos * g.pp + j);
     }
     if (wz) {
 #pragma unroll 4
-      for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(ct + s * split + (B + b) * g.pp + j);
+      for (int s = 0; s < g.sct; ++s) v += (double)__ldcg(ct + s * split + (nact + pos) * g.pp + j);
     }
   }
   if (wz && slab == 0 && threadIdx.x == 0) {
@@ -303,11 +337,12 @@ __global__ void __launch_bounds__(kWinThreads, 1) kb_window(BatchArgs g) {
   const bool full = resync_at(t);
   const double* out = a.beta + ring(t) * g.pv;
   const double* bprev = a.beta + ring(t - 1) * g.pv;
+  const int64_t pos = g.slot[b];                      // compacted contraction row
   for (int64_t j = threadIdx.x; j < g.pp; j += kWinThreads) {
     float h = 0.f, l = 0.f;
     if (j < g.p) tf32_split(full ? out[j] : dsub(out[j], bprev[j]), h, l);
-    g.bh[b * g.pp + j] = h;
-    g.bl[b * g.pp + j] = l;
+    g.bh[pos * g.pp + j] = h;
+    g.bl[pos * g.pp + j] = l;
   }
 }
 
@@ -329,7 +364,8 @@ __global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
   const double* uprev = g.u + (ring(t - 1) * B + b) * nn;
   double* uo = g.u + ((mode == MODE_ITER ? ring(t) : 0) * B + b) * nn;
   double* uo2 = g.u + (2 * B + b) * nn;           // MODE_INIT: u_{-1} = u_0
-  const float* cfb = g.cf + b * nn;
+  // compacted contraction row (MODE_INIT: every node, slot = node)
+  const float* cfb = g.cf + (mode == MODE_ITER ? (int64_t)g.slot[b] : b) * nn;
   const int64_t cstride = B * nn;
   const int sf = g.sf;
   const int i0 = (int)r0, i1 = (int)r1;

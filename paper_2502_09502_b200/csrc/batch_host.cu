@@ -82,6 +82,7 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
   g.slab_hfone = (double*)take(8ull * B * g.S);
   g.slab_htop = (double*)take(8ull * B * g.S * kHTop);
   g.flags = (int*)take(4ull * 8);
+  g.slot = (int*)take(4ull * B);
   return off + 1024;
 }
 
@@ -107,6 +108,7 @@ static int batch_iteration(Batch& Bt, cudaStream_t s, cudaEvent_t* ev) {
   auto rec = [&](int i) -> cudaError_t {
     return ev ? cudaEventRecordWithFlags(ev[i], s, cudaEventRecordExternal) : cudaSuccess;
   };
+  kb_compact<<<1, 1024, 0, s>>>(g);
   kb_rhs<<<rgrid, kRowThreads, 0, s>>>(g);
   kb_plan<<<1, 1, 0, s>>>(g);
   L0_B_TRY(cudaGetLastError());

@@ -162,3 +162,32 @@ def test_batched_single_node_and_trivial_root():
         if f.primal_value < cut * (1 - 1e-6):
             assert r.termination.value == "primal_below_incumbent"
             assert r.iterations <= f.iterations
+
+
+def test_batched_finished_nodes_leave_the_contractions():
+    """Nodes that stop early (here: a parent bound above the dual cutoff ends
+    them at the first check) drop out of the compacted contractions; the
+    others must still match their single solves."""
+    from paper_2502_09502_b200 import (FistaOptions, NodeState, lipschitz_constant,
+                                       solve_relaxation, solve_relaxation_batched)
+    inst, nodes = _c4_instance(0.06, 12)
+    L = lipschitz_constant(inst)
+    cut = 1e12
+    mixed = []
+    for i, nd in enumerate(nodes):
+        base = nd or NodeState()
+        pb = 2 * cut if i % 3 == 1 else -np.inf
+        mixed.append(NodeState(fixed_one=base.fixed_one, fixed_zero=base.fixed_zero, parent_bound=pb))
+    # 300 iterations: a restart decision flipped by fp32-class rounding changes
+    # the path, not the limit -- compare near convergence
+    opts = FistaOptions(max_iterations=300, stop_on_gap=False, lipschitz=L, early_dual_cutoff=cut)
+    reps = solve_relaxation_batched(inst, mixed, opts=opts)
+    for i, nd in enumerate(mixed):
+        if i % 3 == 1:
+            assert reps[i].termination.value == "dual_above_incumbent"
+            assert reps[i].iterations == 1
+        else:
+            ref = solve_relaxation(inst, nd, opts=opts)
+            assert reps[i].iterations == ref.iterations == 300
+            assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5, i
+            assert _rel(reps[i].dual_bound, ref.dual_bound) < 1e-5, i
