@@ -197,7 +197,8 @@ int32_t l0_all_finite(const void* d_x, int32_t dtype, int64_t rows, int64_t cols
  * rounding (tolerance 1e-5 relative) whatever the problem's dtype.
  * l0_batch_set_workspace pre-splits X (and X^T) into TF32 hi/lo operands, so
  * X must not change while the batch exists.  Nodes advance in lockstep; a
- * finished node is frozen.  d_beta_out is n_nodes x p (row per node); reps
+ * finished node is frozen and leaves the contractions.  Warm starts (the
+ * parent's beta, fista.py:130-137) come with g(beta_0) per node.  d_beta_out is n_nodes x p (row per node); reps
  * has n_nodes entries.  Trace callbacks are not available in batched mode. */
 typedef struct l0_batch l0_batch;
 int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out);
@@ -205,6 +206,8 @@ int32_t l0_batch_workspace_bytes(const l0_batch* batch, uint64_t* bytes);
 int32_t l0_batch_set_workspace(l0_batch* batch, void* d_ws, uint64_t bytes);
 int32_t l0_batch_solve(l0_batch* batch, int64_t k, double M, double lambda2,
                        const l0_fista_opts* opts, const l0_node* nodes /* n_nodes, nullable */,
+                       const double* d_warm /* nullable, n_nodes x p warm starts */,
+                       const double* h_g0 /* with d_warm: g(beta_0) per node (l0_g_value) */,
                        double* d_beta_out, l0_report* reps, void* stream);
 int32_t l0_batch_destroy(l0_batch* batch);
 

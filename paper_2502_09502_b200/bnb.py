@@ -309,11 +309,16 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
                 continue
             entry["decision"] = f"branch {j}"
             log.append(entry)
+            # children inherit the parent's relaxation beta, projected onto
+            # their fixed-zero pattern, as warm start
+            warm = np.asarray(rep.beta, dtype=np.float64)
             if len(node.fixed_one) + 1 <= instance.k:
                 push(bound, NodeState(fixed_one=node.fixed_one + (j,), fixed_zero=node.fixed_zero,
-                                      depth=node.depth + 1, parent_bound=bound))
+                                      depth=node.depth + 1, parent_bound=bound, warm_start=warm))
+            w0 = warm.copy()
+            w0[j] = 0.0
             push(bound, NodeState(fixed_one=node.fixed_one, fixed_zero=node.fixed_zero + (j,),
-                                  depth=node.depth + 1, parent_bound=bound))
+                                  depth=node.depth + 1, parent_bound=bound, warm_start=w0))
     lb = glb() if heap else inc_obj
     if status is None:
         status = CertificateStatus.OPTIMAL

@@ -84,7 +84,24 @@ __device__ __forceinline__ bool resync_at(int64_t t) { return t % kResync == 0; 
 
 __device__ __forceinline__ int64_t gvs(const BatchArgs& g) { return 3 * g.pv + 8; }
 
-__global__ void kb_state_init(BatchArgs g) {
+// warm starts: beta_0 of every node into ring slots 0 and 2 (t = 0, t = -1)
+// and its TF32 split into the forward contraction's rows
+__global__ void kb_warm(BatchArgs g, const double* warm) {
+  const int64_t b = blockIdx.y;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.pp; j += (int64_t)gridDim.x * blockDim.x) {
+    const double w = j < g.p ? warm[b * g.p + j] : 0.0;
+    if (j < g.pv) {
+      g.beta[(b * 3 + 0) * g.pv + j] = w;
+      g.beta[(b * 3 + 2) * g.pv + j] = w;
+    }
+    float h, l;
+    tf32_split(w, h, l);
+    g.bh[b * g.pp + j] = h;
+    g.bl[b * g.pp + j] = l;
+  }
+}
+
+__global__ void kb_state_init(BatchArgs g, const double* g0) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.B) return;
   State* st = g.st + b;
@@ -103,7 +120,7 @@ __global__ void kb_state_init(BatchArgs g) {
   st->last_restarted = 0;
   st->topk_fallbacks = 0;
   st->obj = 0.0;
-  st->g_next = 0.0;
+  st->g_next = g0 ? g0[b] : 0.0;          // g(beta_0) for the initial objective (fista.py:143)
   st->best_dual = g.prm[b].parent_bound;
   st->gap = CUDART_NAN;
   st->last_dual = CUDART_NAN;

@@ -370,7 +370,8 @@ int32_t l0_batch_destroy(l0_batch* Bt) {
 }
 
 int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const l0_fista_opts* o,
-                       const l0_node* nodes, double* d_beta_out, l0_report* reps, void* stream) {
+                       const l0_node* nodes, const double* d_warm, const double* h_g0,
+                       double* d_beta_out, l0_report* reps, void* stream) {
   if (!Bt || !o || !reps || !d_beta_out) return set_error(L0_INVALID, "null argument");
   if (!Bt->ws) return set_error(L0_INVALID, "batch has no workspace (l0_batch_set_workspace)");
   BatchArgs& g = Bt->g;
@@ -448,12 +449,26 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   L0_B_TRY(cudaMemcpyAsync(g.mask, mask.data(), (size_t)(B * pv), cudaMemcpyHostToDevice, s));
   L0_B_TRY(cudaMemcpyAsync(g.fone, fone.data(), 4ull * B * g.fone_stride, cudaMemcpyHostToDevice, s));
   int64_t launches = 0;
-  kb_state_init<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(g);
+  if (d_warm && !h_g0) return set_error(L0_INVALID, "warm starts need g(beta_0) per node (h_g0)");
+  double* d_g0 = nullptr;
+  if (h_g0) {
+    // g(beta_0) per node rides in the per-node gv scratch until the state init reads it
+    d_g0 = g.gv;   // [B][3 pv + 8] doubles: the first B doubles are free at this point
+    L0_B_TRY(cudaMemcpyAsync(d_g0, h_g0, 8ull * B, cudaMemcpyHostToDevice, s));
+  }
+  kb_state_init<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(g, d_g0);
   ++launches;
-  // cold start: beta_0 = 0 (fista.py:130-137); u_0 = X beta_0 through the forward contraction
-  L0_B_TRY(cudaMemsetAsync(g.beta, 0, 8ull * 3 * B * pv, s));
-  L0_B_TRY(cudaMemsetAsync(g.bh, 0, 4ull * B * g.pp, s));
-  L0_B_TRY(cudaMemsetAsync(g.bl, 0, 4ull * B * g.pp, s));
+  if (d_warm) {
+    // warm starts (fista.py:130-137): beta_0 -> ring slots, split for u_0 = X beta_0
+    kb_warm<<<dim3((unsigned)std::min<int64_t>((g.pp + 255) / 256, 64), (unsigned)B), 256, 0, s>>>(g, d_warm);
+    L0_B_TRY(cudaGetLastError());
+    ++launches;
+  } else {
+    // cold start: beta_0 = 0 (fista.py:130-137); u_0 = X beta_0 through the forward contraction
+    L0_B_TRY(cudaMemsetAsync(g.beta, 0, 8ull * 3 * B * pv, s));
+    L0_B_TRY(cudaMemsetAsync(g.bh, 0, 4ull * B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bl, 0, 4ull * B * g.pp, s));
+  }
   Bt->gf.n_active = nullptr;
   L0_B_TRY(tc_gemm_launch(Bt->m_xh, Bt->m_xl, Bt->m_bh, Bt->m_bl, Bt->gf, std::min(Bt->gf.units, Bt->sms), s));
   Bt->gf.n_active = g.flags + 3;

@@ -130,10 +130,7 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
     nodes = list(nodes)
     if not nodes:
         return []
-    for nd in nodes:
-        EnvelopeParams.for_instance(instance, nd)        # InfeasibleNodeError (fista.py:97)
-        if nd is not None and getattr(nd, "warm_start", None) is not None:
-            raise UnsupportedOperationError("batched mode starts every node cold")
+    params = [EnvelopeParams.for_instance(instance, nd) for nd in nodes]   # InfeasibleNodeError (fista.py:97)
     L = opts.lipschitz if opts.lipschitz is not None else lipschitz_constant(instance)
 
     import torch
@@ -159,11 +156,28 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
         arr[i].n_fixed_zero = f0.size
         arr[i].parent_bound = float(nd.parent_bound)
     p = instance.p
+    # warm starts (NodeState.warm_start; fista.py:130-137): beta_0 per node and
+    # g(beta_0) for the initial objective; cold nodes start at 0 with g = 0
+    warm = g0 = None
+    if any(nd is not None and getattr(nd, "warm_start", None) is not None for nd in nodes):
+        from .perspective import g_value
+        warm = torch.zeros((len(nodes), p), dtype=torch.float64, device=dp.X.device)
+        g0 = np.zeros(len(nodes))
+        for i, nd in enumerate(nodes):
+            ws = getattr(nd, "warm_start", None) if nd is not None else None
+            if ws is None:
+                continue
+            w = _device.to_cuda_f64(ws)
+            if tuple(w.shape) != (p,):
+                raise InvalidInputError("warm start has the wrong dimension")
+            warm[i].copy_(w)
+            g0[i] = g_value(w, params[i])
     beta_out = torch.empty((len(nodes), p), dtype=torch.float64, device=dp.X.device)
     reps = (native.Report * len(nodes))()
     rc = lib.l0_batch_solve(handle, int(instance.k), float(instance.M), float(instance.lambda2),
-                            ctypes.byref(o), ctypes.cast(arr, ctypes.c_void_p), beta_out.data_ptr(),
-                            ctypes.cast(reps, ctypes.c_void_p), _device.stream_handle())
+                            ctypes.byref(o), ctypes.cast(arr, ctypes.c_void_p),
+                            _device.ptr(warm), g0.ctypes.data_as(ctypes.c_void_p) if g0 is not None else None,
+                            beta_out.data_ptr(), ctypes.cast(reps, ctypes.c_void_p), _device.stream_handle())
     if rc == native.NUMERICAL:
         bad = next((r for r in reps if r.status == native.NUMERICAL), None)
         raise NumericalError(native.last_error(),

@@ -97,7 +97,7 @@ _PROTOS = {
     "l0_batch_workspace_bytes": (c_i32, [c_vp, ctypes.POINTER(c_u64)]),
     "l0_batch_set_workspace": (c_i32, [c_vp, c_vp, c_u64]),
     "l0_batch_solve": (c_i32, [c_vp, c_i64, c_f64, c_f64, ctypes.POINTER(FistaOpts),
-                               c_vp, c_vp, c_vp, c_vp]),
+                               c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "l0_batch_destroy": (c_i32, [c_vp]),
     "l0_tc_gemm_workspace_bytes": (c_u64, [c_i64, c_i64, c_i64]),
     "l0_tc_gemm_3xtf32": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i32, c_i64, c_i64,

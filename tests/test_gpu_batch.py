@@ -191,3 +191,27 @@ def test_batched_finished_nodes_leave_the_contractions():
             assert reps[i].iterations == ref.iterations == 300
             assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5, i
             assert _rel(reps[i].dual_bound, ref.dual_bound) < 1e-5, i
+
+
+def test_batched_warm_starts_match_single_solves():
+    """NodeState.warm_start (fista.py:130-137) in batched mode: beta_0 and the
+    initial objective F(X beta_0) + 2 l2 g(beta_0) per node."""
+    from paper_2502_09502_b200 import (FistaOptions, NodeState, lipschitz_constant,
+                                       solve_relaxation, solve_relaxation_batched)
+    inst, nodes = _c4_instance(0.06, 6)
+    L = lipschitz_constant(inst)
+    base = solve_relaxation(inst, None, opts=FistaOptions(max_iterations=40, stop_on_gap=False, lipschitz=L))
+    warm_nodes = []
+    for i, nd in enumerate(nodes):
+        nd = nd or NodeState()
+        w = base.beta.copy()
+        w[list(nd.fixed_zero)] = 0.0
+        warm_nodes.append(NodeState(fixed_one=nd.fixed_one, fixed_zero=nd.fixed_zero,
+                                    warm_start=w if i % 2 == 0 else None))
+    opts = FistaOptions(max_iterations=150, stop_on_gap=False, lipschitz=L)
+    reps = solve_relaxation_batched(inst, warm_nodes, opts=opts)
+    for i, nd in enumerate(warm_nodes):
+        ref = solve_relaxation(inst, nd, opts=opts)
+        assert reps[i].iterations == ref.iterations
+        assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5, i
+        assert _rel(reps[i].dual_bound, ref.dual_bound) < 1e-5, i
