@@ -5,9 +5,10 @@ code for it; SURVEY.md §8(f) ranks it first among the callers of the hot path.
 Behaviour follows the spec:
 
 * ``beam_search_incumbent``: supports grown one feature at a time from the
-  node's fixed-one set, each candidate refit by projected gradient descent on
-  the box-constrained ridge-regularised loss (fixed budget), the
-  ``beam_width`` best kept;
+  node's fixed-one set, each candidate refit on the box-constrained
+  ridge-regularised loss (squared error: the exact ridge solution when the
+  box does not bind; otherwise projected gradient descent with a fixed
+  budget), the ``beam_width`` best kept;
 * ``select_branching_variable``: among the incumbent's unfixed nonzeros, the
   coordinate whose zeroing (no refit) raises the composite loss most;
 * ``certify``: best-first search keyed by the parent bound (ties: deeper
@@ -121,11 +122,25 @@ def _refit(instance: ProblemInstance, supports: Sequence[Tuple[int, ...]], iters
     lam2, M = float(instance.lambda2), float(instance.M)
     L = _CURV[instance.loss] * (Xs * Xs).sum(dim=(1, 2)) + 2.0 * lam2 + 1e-12   # >= curvature
     b = torch.zeros((C, s), dtype=torch.float64, device=dp.X.device)
-    for _ in range(iters):
-        u = torch.einsum("csn,cs->cn", Xs, b)
-        _, g = _loss_and_grad(instance.loss, u, y)
-        grad = torch.einsum("csn,cn->cs", Xs, g) + 2.0 * lam2 * b
-        b = torch.clamp(b - grad / L[:, None], -M, M) * mask
+    todo = torch.ones(C, dtype=torch.bool, device=dp.X.device)
+    if instance.loss is LossKind.SQUARED_ERROR:
+        # exact ridge solution per support; projected gradient only where the box binds
+        G = torch.einsum("csn,ctn->cst", Xs, Xs) + lam2 * torch.eye(s, dtype=torch.float64,
+                                                                     device=dp.X.device)
+        G = G + torch.diag_embed(1.0 - mask)              # padded coordinates: identity rows
+        rhs = torch.einsum("csn,n->cs", Xs, dp.y)
+        b = torch.linalg.solve(G, rhs[:, :, None])[:, :, 0] * mask
+        todo = (b.abs() > M).any(dim=1)
+        b = torch.clamp(b, -M, M)
+    if bool(todo.any()):
+        bt = b[todo]
+        Xt, Lt, mt = Xs[todo], L[todo], mask[todo]
+        for _ in range(iters):
+            u = torch.einsum("csn,cs->cn", Xt, bt)
+            _, g = _loss_and_grad(instance.loss, u, y)
+            grad = torch.einsum("csn,cn->cs", Xt, g) + 2.0 * lam2 * bt
+            bt = torch.clamp(bt - grad / Lt[:, None], -M, M) * mt
+        b[todo] = bt
     u = torch.einsum("csn,cs->cn", Xs, b)
     f, _ = _loss_and_grad(instance.loss, u, y)
     obj = f + lam2 * (b * b).sum(-1)
