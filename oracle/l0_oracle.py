@@ -59,6 +59,8 @@ import scipy.special as _scipy_special
 SQUARED_ERROR = "squared_error"
 LOGISTIC = "logistic"
 SQUARED_HINGE = "squared_hinge"
+POISSON = "poisson"              # bound-grade (values, conjugates, bounds only)
+GAMMA = "gamma"
 SOLVER_LOSSES = (SQUARED_ERROR, LOGISTIC, SQUARED_HINGE)
 
 LIPSCHITZ_SAFETY = 1.01          # model.py:32
@@ -413,6 +415,10 @@ def loss_value(kind: str, u, y) -> float:
     if kind == SQUARED_HINGE:
         h = np.maximum(0.0, 1.0 - y * u)
         return float(h @ h)
+    if kind == POISSON:                                   # model.py:174-175
+        return float(np.sum(np.exp(u) - y * u))
+    if kind == GAMMA:                                     # model.py:176-177
+        return float(np.sum(y * np.exp(-u) + u))
     raise ValueError(kind)
 
 
@@ -426,6 +432,10 @@ def loss_grad(kind: str, u, y) -> np.ndarray:
         return -y * _expit(-y * u)
     if kind == SQUARED_HINGE:
         return -2.0 * y * np.maximum(0.0, 1.0 - y * u)
+    if kind == POISSON:                                   # model.py:196-197 (_gradient_any)
+        return np.exp(u) - y
+    if kind == GAMMA:                                     # model.py:198-199
+        return 1.0 - y * np.exp(-u)
     raise ValueError(kind)
 
 
@@ -452,6 +462,18 @@ def loss_conj_neg(kind: str, zeta, y) -> float:
             return math.inf
         z = np.minimum(z, 0.0)
         return float(np.sum(z + 0.25 * z * z))
+    if kind == POISSON:                                   # model.py:259-264
+        z = y - zeta
+        if np.any(z < -DOMAIN_SLACK):
+            return math.inf
+        z = np.maximum(z, 0.0)
+        return float(np.sum(_xlogx(z) - z))
+    if kind == GAMMA:                                     # model.py:266-273
+        z = (1.0 + zeta) / y
+        if np.any(z < -DOMAIN_SLACK):
+            return math.inf
+        z = np.maximum(z, 0.0)
+        return float(np.sum(y * (_xlogx(z) - z)))
     raise ValueError(kind)
 
 

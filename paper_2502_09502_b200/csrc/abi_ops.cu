@@ -203,7 +203,7 @@ int32_t l0_huber(const double* d_x, int64_t n, double w, double M, int32_t prox,
 int32_t l0_loss_value(int32_t loss, const double* d_u, const double* d_y, int64_t n,
                       double* h_value, double* d_grad, int32_t* h_nonfinite, void* d_ws,
                       uint64_t ws_bytes, void* stream) {
-  if (loss < 0 || loss > 2) return set_error(ST_UNSUPPORTED, "loss not solver-grade");
+  if (loss < 0 || loss > 4) return set_error(ST_UNSUPPORTED, "loss not evaluated by the engine");
   OpsWs w;
   int rc = ops_ws(1, d_ws, ws_bytes, &w);
   if (rc) return rc;
@@ -220,7 +220,7 @@ int32_t l0_loss_value(int32_t loss, const double* d_u, const double* d_y, int64_
 
 int32_t l0_loss_conjugate(int32_t loss, const double* d_zeta, const double* d_y, int64_t n,
                           double* h_out, void* d_ws, uint64_t ws_bytes, void* stream) {
-  if (loss < 0 || loss > 2) return set_error(ST_UNSUPPORTED, "loss not solver-grade");
+  if (loss < 0 || loss > 4) return set_error(ST_UNSUPPORTED, "loss not evaluated by the engine");
   OpsWs w;
   int rc = ops_ws(1, d_ws, ws_bytes, &w);
   if (rc) return rc;

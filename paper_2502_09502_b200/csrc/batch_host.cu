@@ -377,6 +377,7 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   BatchArgs& g = Bt->g;
   const int64_t p = g.p, B = g.B, pv = g.pv;
   std::memset(reps, 0, sizeof(l0_report) * (size_t)B);
+  if (g.loss > SQUARED_HINGE) return set_error(L0_UNSUPPORTED, "bound-grade loss: the relaxation solver needs a solver-grade loss");
   if (!(k >= 1 && k <= p)) return set_error(L0_INVALID, "k must satisfy 1 <= k <= p");
   if (!(M > 0 && std::isfinite(M))) return set_error(L0_INVALID, "M must be a positive finite real");
   if (!(lambda2 > 0 && std::isfinite(lambda2))) return set_error(L0_INVALID, "lambda2 must be a positive finite real");

@@ -15,7 +15,10 @@
 
 namespace l0 {
 
-enum Loss : int { SQUARED_ERROR = 0, LOGISTIC = 1, SQUARED_HINGE = 2 };
+// solver-grade (0..2) and the bound-grade losses the engine evaluates (3, 4;
+// model.py:174-177, :196-199, :259-273): they have no global gradient
+// Lipschitz constant, so only the bound operations accept them
+enum Loss : int { SQUARED_ERROR = 0, LOGISTIC = 1, SQUARED_HINGE = 2, POISSON = 3, GAMMA = 4 };
 enum Dtype : int { F64 = 0, F32 = 1 };
 enum Status : int {
   ST_OK = 0, ST_INVALID = 1, ST_NUMERICAL = 2, ST_INFEASIBLE = 3, ST_UNSUPPORTED = 4, ST_CUDA = 5
@@ -69,6 +72,8 @@ __device__ __forceinline__ double expit(double x) { return ddiv(1.0, dadd(1.0, e
 __device__ __forceinline__ double loss_term(int loss, double u, double y) {
   if (loss == SQUARED_ERROR) { double d = dsub(u, y); return dmul(d, d); }
   if (loss == LOGISTIC) return logaddexp0(dmul(-y, u));
+  if (loss == POISSON) return dsub(exp(u), dmul(y, u));           // model.py:174-175
+  if (loss == GAMMA) return dadd(dmul(y, exp(-u)), u);            // model.py:176-177
   double m = fmax(0.0, dsub(1.0, dmul(y, u)));
   return dmul(m, m);
 }
@@ -77,6 +82,8 @@ __device__ __forceinline__ double loss_term(int loss, double u, double y) {
 __device__ __forceinline__ double loss_grad(int loss, double u, double y) {
   if (loss == SQUARED_ERROR) return dmul(2.0, dsub(u, y));
   if (loss == LOGISTIC) return dmul(-y, expit(dmul(-y, u)));
+  if (loss == POISSON) return dsub(exp(u), y);                    // model.py:196-197
+  if (loss == GAMMA) return dsub(1.0, dmul(y, exp(-u)));          // model.py:198-199
   double m = fmax(0.0, dsub(1.0, dmul(y, u)));
   return dmul(dmul(-2.0, y), m);
 }
@@ -97,6 +104,16 @@ __device__ __forceinline__ void conj_accumulate(int loss, double zeta, double y,
     if (r < -kDomainSlack || r > dadd(1.0, kDomainSlack)) { acc[2] += 1.0; return; }
     r = fmin(fmax(r, 0.0), 1.0);
     acc[0] = dadd(acc[0], dadd(xlogx(r), xlogx(dsub(1.0, r))));
+  } else if (loss == POISSON) {                                   // model.py:259-264
+    double z = dsub(y, zeta);
+    if (z < -kDomainSlack) { acc[2] += 1.0; return; }
+    z = fmax(z, 0.0);
+    acc[0] = dadd(acc[0], dsub(xlogx(z), z));
+  } else if (loss == GAMMA) {                                     // model.py:266-273
+    double z = ddiv(dadd(1.0, zeta), y);
+    if (z < -kDomainSlack) { acc[2] += 1.0; return; }
+    z = fmax(z, 0.0);
+    acc[0] = dadd(acc[0], dmul(y, dsub(xlogx(z), z)));
   } else {
     double z = dmul(-y, zeta);
     if (z > kDomainSlack) { acc[2] += 1.0; return; }

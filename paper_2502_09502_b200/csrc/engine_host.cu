@@ -365,7 +365,8 @@ int32_t l0_problem_create(const void* d_X, int32_t dtype, int64_t n, int64_t p, 
   const int64_t es = dtype == F64 ? 8 : 4;
   if (ld < p || (ld * es) % 16 != 0) return set_error(ST_INVALID, "ld must be >= p and a multiple of 16 bytes");
   if (((uintptr_t)d_X) % 16 != 0) return set_error(ST_INVALID, "X must be 16-byte aligned");
-  if (loss < 0 || loss > 2) return set_error(ST_UNSUPPORTED, "loss must be squared_error, logistic or squared_hinge");
+  if (loss < 0 || loss > 4)
+    return set_error(ST_UNSUPPORTED, "loss must be squared_error, logistic, squared_hinge, poisson or gamma");
   l0_problem* P = new l0_problem();
   P->a.X = d_X;
   P->a.y = d_y;
@@ -501,6 +502,8 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   EngineArgs& a = P->a;
   const int64_t p = a.p;
   // ---- validation (model.py:102-107, fista.py:55-61, perspective.py:36-47) ----
+  if (a.loss > SQUARED_HINGE)   // fista.py:92-95: the solver needs a Lipschitz-smooth loss
+    return set_error(ST_UNSUPPORTED, "bound-grade loss: the relaxation solver needs a solver-grade loss");
   if (!(k >= 1 && k <= p)) return set_error(ST_INVALID, "k must satisfy 1 <= k <= p");
   if (!(M > 0 && std::isfinite(M))) return set_error(ST_INVALID, "M must be a positive finite real");
   if (!(lambda2 > 0 && std::isfinite(lambda2)))

@@ -11,8 +11,10 @@ behaviour):
 * ``X`` may be a torch tensor (CUDA-resident data is used in place).
 
 Solver-grade losses (squared error, logistic, squared hinge) are what the
-engine accelerates; the bound-grade ones (Poisson, gamma, multinomial) keep
-their enum values but raise UnsupportedOperationError here.
+engine solves; the bound-grade Poisson and gamma losses are evaluated on the
+GPU for values, conjugates and safe bounds (the solver rejects them, as the
+reference does); multinomial (matrix predictions) raises
+UnsupportedOperationError.
 """
 
 from __future__ import annotations
@@ -59,11 +61,17 @@ def is_solver_grade(loss: LossKind) -> bool:
     return loss in _SOLVER_GRADE
 
 
+_ENGINE_LOSSES = _SOLVER_GRADE + (LossKind.POISSON, LossKind.GAMMA)
+
+
 def _engine_loss(loss: LossKind) -> int:
-    if loss not in _SOLVER_GRADE:
+    """Engine code of a loss the kernels evaluate: the solver-grade ones and,
+    for values, conjugates and bounds only, Poisson and gamma.  Multinomial
+    (matrix predictions) stays host-side unsupported."""
+    if loss not in _ENGINE_LOSSES:
         raise UnsupportedOperationError(
-            f"{loss.value} is a bound-grade loss; the B200 engine evaluates the "
-            "solver-grade losses (squared_error, logistic, squared_hinge)")
+            f"{loss.value}: the B200 engine evaluates squared_error, logistic, squared_hinge "
+            "(solver-grade) and poisson, gamma (bound-grade)")
     return native.LOSS_CODES[loss.value]
 
 

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libl0b200.so")
 
 OK, INVALID, NUMERICAL, INFEASIBLE, UNSUPPORTED, CUDA_ERR, ABORTED = range(7)
 F64, F32 = 0, 1
-LOSS_CODES = {"squared_error": 0, "logistic": 1, "squared_hinge": 2}
+LOSS_CODES = {"squared_error": 0, "logistic": 1, "squared_hinge": 2, "poisson": 3, "gamma": 4}
 TERMINATIONS = ("converged", "iteration_limit", "time_limit", "primal_below_incumbent",
                 "dual_above_incumbent")
 FREE, FIXED_ONE, FIXED_ZERO = 0, 1, 2

@@ -117,9 +117,10 @@ def safe_lower_bound(instance: ProblemInstance, beta_hat, node: Optional[NodeSta
     (perspective.py:162-190)."""
     if instance.loss is LossKind.MULTINOMIAL:
         raise UnsupportedOperationError("multinomial instances have no vector-coefficient bound")
-    if instance.loss not in (LossKind.SQUARED_ERROR, LossKind.LOGISTIC, LossKind.SQUARED_HINGE):
+    if instance.loss not in (LossKind.SQUARED_ERROR, LossKind.LOGISTIC, LossKind.SQUARED_HINGE,
+                             LossKind.POISSON, LossKind.GAMMA):
         raise UnsupportedOperationError(
-            f"{instance.loss.value}: the B200 engine evaluates bounds for solver-grade losses")
+            f"{instance.loss.value}: the B200 engine evaluates bounds for vector GLM losses")
     from . import _device
     bd = _device.to_cuda_f64(beta_hat)
     import torch
