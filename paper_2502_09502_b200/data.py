@@ -14,20 +14,36 @@ the GPU engine and the CPU oracle see identical inputs:
 * ``standardize``   — data.py:224-242
 
 ``make_config(name)`` builds the five BASELINE configs.
+
+Instance ingest (same names, arguments, file formats
+and errors as the reference's ``l0cert.data``): ``SyntheticParams`` /
+``generate_synthetic`` (data.py:36-115), ``load_dataset`` (delimited and
+libsvm-style sparse text, data.py:122-202), ``StandardizeTransform`` /
+``standardize`` (data.py:205-242; a CUDA tensor is standardized on the
+device), ``write_instance`` / ``read_instance`` (the ``l0cert-instance``
+text format, data.py:248-317).
 """
 
 from __future__ import annotations
 
 import dataclasses
 import math
-from typing import Optional, Tuple
+import re
+from typing import List, Optional, Tuple
 
 import numpy as np
 
+from .errors import DataFormatError, InvalidInputError
+
 __all__ = [
     "true_support", "ar1_rows", "synthetic", "standardize", "ConfigData",
-    "make_config", "CONFIGS", "random_nodes",
+    "make_config", "CONFIGS", "random_nodes", "SyntheticParams", "generate_synthetic",
+    "load_dataset", "StandardizeTransform", "write_instance", "read_instance",
+    "DEFAULT_M", "DEFAULT_LAMBDA2",
 ]
+
+DEFAULT_M = 2.0          # data.py:30-31 (benchmark defaults of generated instances)
+DEFAULT_LAMBDA2 = 1.0
 
 
 def true_support(p: int, k_true: int) -> np.ndarray:
@@ -83,18 +99,240 @@ def synthetic(n: int, p: int, k_true: int, sigma: float = 0.5, snr: float = 5.0,
     return X, y, beta_true
 
 
-def standardize(X) -> Tuple[np.ndarray, np.ndarray]:
-    """Centre columns, scale to unit norm, drop constant ones — data.py:224-242.
+@dataclasses.dataclass
+class StandardizeTransform:
+    """What ``standardize`` did (data.py:205-221): kept / dropped columns, the
+    kept columns' means and centred norms."""
+    kept: np.ndarray
+    dropped: np.ndarray
+    means: np.ndarray
+    norms: np.ndarray
 
-    Returns (X_std, kept_columns)."""
+    def map_coefficients(self, beta_std) -> Tuple[np.ndarray, float]:
+        """Coefficients of the standardized problem on the original scale (zero
+        at dropped columns) and the intercept shift of the centring."""
+        b = np.asarray(beta_std, dtype=np.float64) / self.norms
+        out = np.zeros(self.kept.size + self.dropped.size)
+        out[self.kept] = b
+        return out, float(-(self.means @ b))
+
+
+def standardize(X):
+    """Centre every column, scale it to unit Euclidean norm, drop the constant
+    ones (data.py:224-242).  Returns (X_std, StandardizeTransform); a CUDA
+    tensor is processed on its device and returned as one."""
+    try:
+        import torch
+        on_gpu = isinstance(X, torch.Tensor) and X.device.type == "cuda"
+    except ImportError:  # pragma: no cover
+        on_gpu = False
+    if on_gpu:
+        Xd = X.to(torch.float64)
+        if Xd.ndim != 2 or Xd.shape[0] < 2:
+            raise InvalidInputError("standardize needs a 2-d matrix with n >= 2")
+        means = Xd.mean(dim=0)
+        cen = Xd - means
+        norms = torch.linalg.vector_norm(cen, dim=0)
+        scale = Xd.abs().amax(dim=0)
+        keep = norms > 1e-12 * torch.clamp(scale, min=1.0)
+        if not bool(keep.any()):
+            raise InvalidInputError("all columns are constant")
+        kept = torch.nonzero(keep).flatten()
+        out = cen[:, kept] / norms[kept]
+        kh = kept.cpu().numpy()
+        return out, StandardizeTransform(kept=kh, dropped=np.flatnonzero(~keep.cpu().numpy()),
+                                         means=means[kept].cpu().numpy(),
+                                         norms=norms[kept].cpu().numpy())
     X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[0] < 2:
+        raise InvalidInputError("standardize needs a 2-d matrix with n >= 2")
     means = X.mean(axis=0)
     centered = X - means
     norms = np.linalg.norm(centered, axis=0)
     scale = np.abs(X).max(axis=0)
     keep = norms > 1e-12 * np.maximum(1.0, scale)
+    if not keep.any():
+        raise InvalidInputError("all columns are constant")
     kept = np.nonzero(keep)[0]
-    return centered[:, kept] / norms[kept], kept
+    return centered[:, kept] / norms[kept], StandardizeTransform(
+        kept=kept, dropped=np.nonzero(~keep)[0], means=means[kept], norms=norms[kept])
+
+
+@dataclasses.dataclass
+class SyntheticParams:
+    """data.py:36-60 (validated on construction)."""
+    n: int
+    p: int
+    k_true: int
+    sigma: float = 0.5
+    snr: float = 5.0
+    task: str = "regression"
+    seed: int = 0
+    snr_scale: str = "variance"
+
+    def __post_init__(self):
+        if self.n < 1 or self.p < 1:
+            raise InvalidInputError("n and p must be positive")
+        if not 1 <= self.k_true <= self.p:
+            raise InvalidInputError("k_true must satisfy 1 <= k_true <= p")
+        if not 0.0 <= self.sigma < 1.0:
+            raise InvalidInputError("sigma must lie in [0, 1)")
+        if not self.snr > 0:
+            raise InvalidInputError("snr must be positive")
+        if self.task not in ("regression", "classification"):
+            raise InvalidInputError("task must be 'regression' or 'classification'")
+        if self.snr_scale not in ("variance", "std"):
+            raise InvalidInputError("snr_scale must be 'variance' or 'std'")
+
+
+def generate_synthetic(params: SyntheticParams):
+    """The seeded instance of data.py:88-115 (cardinality k_true, M and
+    lambda2 at the benchmark defaults, ground truth attached)."""
+    from .model import LossKind, ProblemInstance
+    X, y, bt = synthetic(params.n, params.p, params.k_true, params.sigma, params.snr,
+                         params.seed, params.task, params.snr_scale)
+    loss = LossKind.SQUARED_ERROR if params.task == "regression" else LossKind.LOGISTIC
+    return ProblemInstance(X=X, y=y, loss=loss, k=params.k_true, M=DEFAULT_M,
+                           lambda2=DEFAULT_LAMBDA2, beta_true=bt)
+
+
+_FIELD_SPLIT = re.compile(r"[,\s]+")
+
+
+def _data_lines(path):
+    """(line number, stripped text) of the non-blank, non-comment lines."""
+    with open(path) as fh:
+        for no, raw in enumerate(fh, start=1):
+            text = raw.strip()
+            if text and not text.startswith("#"):
+                yield no, text
+
+
+def load_dataset(path, fmt: str = "delimited", label_column: str = "last",
+                 n_features: Optional[int] = None):
+    """(X, y) from a text file (data.py:122-202).  ``delimited``: one sample per
+    line, comma or whitespace separated, the label first or last;
+    ``sparse``: ``label idx:value ...`` with 1-based feature indices."""
+    if fmt not in ("delimited", "sparse"):
+        raise InvalidInputError(f"unknown dataset format {fmt!r}")
+    if label_column not in ("last", "first"):
+        raise InvalidInputError("label_column must be 'last' or 'first'")
+    if fmt == "delimited":
+        X, y, width = [], [], None
+        for no, text in _data_lines(path):
+            parts = [f for f in _FIELD_SPLIT.split(text) if f]
+            if width is None:
+                if len(parts) < 2:
+                    raise DataFormatError(f"line {no}: need at least one feature and a label", line=no)
+                width = len(parts)
+            elif len(parts) != width:
+                raise DataFormatError(f"line {no}: expected {width} fields, found {len(parts)}", line=no)
+            try:
+                vals = [float(f) for f in parts]
+            except ValueError as exc:
+                raise DataFormatError(f"line {no}: {exc}", line=no) from None
+            if label_column == "last":
+                X.append(vals[:-1]); y.append(vals[-1])
+            else:
+                X.append(vals[1:]); y.append(vals[0])
+        if not X:
+            raise DataFormatError("file contains no data rows")
+        return np.asarray(X, dtype=np.float64), np.asarray(y, dtype=np.float64)
+    samples, top = [], 0
+    for no, text in _data_lines(path):
+        parts = text.split()
+        try:
+            lab = float(parts[0])
+            feats = []
+            for tok in parts[1:]:
+                j_s, v_s = tok.split(":", 1)
+                j = int(j_s)
+                if j < 1:
+                    raise ValueError(f"feature index {j} is not 1-based")
+                feats.append((j, float(v_s)))
+        except (ValueError, IndexError) as exc:
+            raise DataFormatError(f"line {no}: {exc}", line=no) from None
+        top = max([top] + [j for j, _ in feats])
+        samples.append((lab, feats))
+    if not samples:
+        raise DataFormatError("file contains no data rows")
+    width = n_features if n_features is not None else top
+    if top > width:
+        raise DataFormatError(f"feature index {top} exceeds declared width {width}")
+    X = np.zeros((len(samples), width))
+    y = np.empty(len(samples))
+    for i, (lab, feats) in enumerate(samples):
+        y[i] = lab
+        for j, v in feats:
+            X[i, j - 1] = v
+    return X, y
+
+
+def write_instance(path, instance) -> None:
+    """The ``l0cert-instance`` text format (data.py:248-266): a key/value
+    header, ``data``, then one sample per line with the label last; the
+    ground-truth support is written 1-based.  Floats round-trip (repr)."""
+    X = np.asarray(instance.X, dtype=np.float64) if not hasattr(instance.X, "cpu") else \
+        instance.X.detach().cpu().numpy().astype(np.float64)
+    y = np.asarray(instance.y, dtype=np.float64)
+    lines = ["format l0cert-instance 1", f"n {X.shape[0]}", f"p {X.shape[1]}",
+             f"loss {instance.loss.value}", f"k {instance.k}", f"M {float(instance.M)!r}",
+             f"lambda2 {float(instance.lambda2)!r}"]
+    if instance.beta_true is not None:
+        sup = np.flatnonzero(np.asarray(instance.beta_true)) + 1
+        lines.append("support_true " + ",".join(str(int(j)) for j in sup))
+    lines.append("data")
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+        for i in range(X.shape[0]):
+            fh.write(" ".join(repr(float(v)) for v in X[i]) + f" {float(y[i])!r}\n")
+
+
+def _num(tok: str) -> float:
+    # the reference's writer emits numpy-2 reprs for numpy scalars
+    # ("np.float64(-1.0)", data.py:266); accept them so its files load here
+    if tok.startswith("np.float64(") and tok.endswith(")"):
+        tok = tok[len("np.float64("):-1]
+    return float(tok)
+
+
+def read_instance(path):
+    """Inverse of ``write_instance`` (data.py:269-317); also reads files the
+    reference wrote under numpy 2 (labels as ``np.float64(...)`` reprs)."""
+    from .model import LossKind, ProblemInstance
+    head, rows, body = {}, [], False
+    for no, text in _data_lines(path):
+        if not body:
+            if text == "data":
+                body = True
+                continue
+            kv = text.split(None, 1)
+            if len(kv) != 2:
+                raise DataFormatError(f"line {no}: malformed header line", line=no)
+            head[kv[0]] = kv[1].strip()
+            continue
+        try:
+            rows.append([_num(f) for f in text.split()])
+        except ValueError as exc:
+            raise DataFormatError(f"line {no}: {exc}", line=no) from None
+    for key in ("n", "p", "loss", "k", "M", "lambda2"):
+        if key not in head:
+            raise DataFormatError(f"missing header field {key!r}")
+    n, p = int(head["n"]), int(head["p"])
+    names = {kind.value: kind for kind in LossKind}
+    if head["loss"] not in names:
+        raise DataFormatError(f"unknown loss {head['loss']!r}")
+    if len(rows) != n:
+        raise DataFormatError(f"header declares n={n} but found {len(rows)} data rows")
+    if any(len(r) != p + 1 for r in rows):
+        raise DataFormatError(f"every data row needs p + 1 = {p + 1} fields")
+    A = np.asarray(rows, dtype=np.float64).reshape(n, p + 1)
+    bt = None
+    if "support_true" in head and head["support_true"]:
+        bt = np.zeros(p)
+        bt[[int(j) - 1 for j in head["support_true"].split(",")]] = 1.0
+    return ProblemInstance(X=A[:, :p], y=A[:, p], loss=names[head["loss"]], k=int(head["k"]),
+                           M=float(head["M"]), lambda2=float(head["lambda2"]), beta_true=bt)
 
 
 @dataclasses.dataclass
