@@ -18,9 +18,11 @@ Behaviour follows the spec:
 B200 specifics: open nodes are evaluated in batches through
 ``solve_relaxation_batched`` (the spec's optional parallel mode: one stale
 incumbent per batch, which keeps pruning sound) with ``early_primal_cutoff``
-and ``early_dual_cutoff`` at the incumbent; the incumbent refits run as
-batched projected-gradient steps on the GPU and the screening gradients
-``X^T grad F`` use the engine's transpose kernel.
+and ``early_dual_cutoff`` at the incumbent; every node's bound in the
+certificate is then the fp64 ``safe_lower_bound`` at its final iterate (the
+batched contraction is 3xTF32); the incumbent refits are batched exact ridge
+solves on the GPU and the screening gradients ``X^T grad F`` use the engine's
+transpose kernel.
 """
 
 from __future__ import annotations
@@ -305,7 +307,12 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
         reps = solve_relaxation_batched(instance, nodes, opts=ropts)[:len(batch)]
         explored += len(batch)
         for (pbound, node), rep in zip(batch, reps):
-            bound = max(pbound, rep.dual_bound) if math.isfinite(rep.dual_bound) else pbound
+            # the certificate uses the fp64 Fenchel bound at the node's final
+            # iterate (two fp64 X passes, perspective.py:162-190): the batched
+            # engine's own bound carries 3xTF32 rounding and only steers its
+            # stopping tests
+            safe = safe_lower_bound(instance, rep.beta, node)
+            bound = max(pbound, safe) if math.isfinite(safe) else pbound
             entry = {"depth": node.depth, "fixed_one": node.fixed_one, "fixed_zero": node.fixed_zero,
                      "bound": bound, "termination": rep.termination.value}
             if pruned(bound):
