@@ -353,7 +353,7 @@ def run_ours(args):
     if single:
         # KF reads X once: both gradient candidates, X^T zeta and u_t from one pass
         kf_bytes = n * p * s + 8 * (4 * n + p)        # X, y, u_{t-1}, u_t (write), beta slice
-        dom, dom_bytes, dom_ms = "kf_fused", kf_bytes, k2_avg
+        dom, dom_bytes, dom_ms = "kf_fused_s", kf_bytes, k2_avg
         others = {"kr_reduce_epilogue": {"launch_ms": k1_avg},
                   "k3_prox_window": {"launch_ms": k3_avg}}
     else:

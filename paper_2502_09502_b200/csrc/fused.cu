@@ -72,19 +72,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   }
 }
-// cluster-scope acquire of remote st.async data; backs off so waiting warps
-// leave the issue slots to the forward group
+// wait for a partial slot filled by st.async from the cluster peers.  The
+// data sits in this CTA's shared memory and the phase completes only once
+// every byte counted by complete_tx has landed, so a CTA-scope acquire
+// suffices (-DL0_FZ_ACQ_CLUSTER builds use the cluster-scope form, whose L1
+// invalidation (CCTL.IVALL) stalls the shared-memory pipe on every wait).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   uint32_t ok = 0;
   for (;;) {
+#ifdef L0_FZ_ACQ_CLUSTER
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(saddr(bar)), "r"(phase)
         : "memory");
+#else
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(phase)
+        : "memory");
+#endif
     if (ok) break;
-    __nanosleep(100);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -182,6 +193,93 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+
+// Shared tail of the single-pass kernels: per-cluster transpose partials to
+// fz_part, per-cluster loss / flags / F* sums to fz_cpart, and in the last CTA
+// of the grid the fixed-order reduction over clusters and the objective /
+// restart logic.  Transpose thread lt owns columns c0 + v*kFzTr*VE + lt*VE + e.
+template <int NA, int VE>
+__device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t t, bool want_z, int cid,
+                                          uint32_t crank, int64_t c0, bool is_tr, int lt,
+                                          const double* accR, const double* accN, const double* accZ,
+                                          double loss_acc, const double* f_acc, int bad, int gbad_R,
+                                          int gbad_N, int* sbad, double* sred) {
+  const int tid = threadIdx.x;
+  const int cs = a.fz_cs;
+  const int ncl = a.fz_ncl;
+  const int64_t pv = a.pv;
+  State* st = a.st;
+  if (is_tr) {
+#pragma unroll
+    for (int v = 0; v < NA / VE; ++v) {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        const int64_t col = c0 + (int64_t)v * kFzTr * VE + lt * VE + e;
+        if (col < pv) {
+          a.fz_part[(0 * (int64_t)ncl + cid) * pv + col] = accR[v * VE + e];
+          a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
+          if (want_z) a.fz_part[(2 * (int64_t)ncl + cid) * pv + col] = accZ[v * VE + e];
+        }
+      }
+    }
+  }
+  if (bad) *sbad = 1;
+  if (gbad_R) atomicOr(sbad, 2);
+  if (gbad_N) atomicOr(sbad, 4);
+  const double lsum = block_sum(loss_acc, sred);
+  const double f0 = block_sum(f_acc[0], sred);
+  const double f1 = block_sum(f_acc[1], sred);
+  const double f2 = block_sum(f_acc[2], sred);
+  if (crank == 0 && tid == 0) {
+    double* cp = a.fz_cpart + 8 * (int64_t)cid;
+    cp[0] = lsum;
+    cp[1] = (double)*sbad;
+    cp[2] = f0;
+    cp[3] = f1;
+    cp[4] = f2;
+  }
+  if (cs > 1) cluster_barrier();  // no st.async into this CTA is still in flight
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  if (tid == 0) s_last = (atomicAdd(cnt_fused(a), 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- last CTA: loss over clusters (fixed order), objective / restart ---------
+  if (tid == 0) {
+    *cnt_fused(a) = 0u;
+    double tot = 0.0, fs0 = 0.0, fs1 = 0.0, fs2 = 0.0;
+    int flags = 0;
+    for (int c = 0; c < ncl; ++c) {
+      const double* cp = a.fz_cpart + 8 * (int64_t)c;
+      tot += __ldcg(cp);
+      flags |= (int)__ldcg(cp + 1);
+      fs0 += __ldcg(cp + 2);
+      fs1 += __ldcg(cp + 3);
+      fs2 += __ldcg(cp + 4);
+    }
+    a.gv[2 * pv + 0] = fs0;
+    a.gv[2 * pv + 1] = fs1;
+    a.gv[2 * pv + 2] = fs2;
+    a.gv[2 * pv + 6] = (double)flags;   // gradient-candidate validity for KR
+    a.gv[2 * pv + 7] = want_z ? 1.0 : 0.0;
+    if (a.multi) {
+      a.gv[2 * pv + 4] = tot;
+      a.gv[2 * pv + 5] = (double)(flags & 1);
+    } else if (flags & 1) {
+      st->err = ST_INVALID;
+      st->err_iter = (mode == MODE_ITER) ? t : 0;
+      if (mode == MODE_ITER) st->t = t;
+      st->done = 1;
+    } else if (mode == MODE_ITER) {
+      objective_update(st, a.prm, tot);
+    } else {
+      st->loss_cur = tot;
+      st->obj = dadd(tot, dmul(a.prm->two_l2, st->g_next));  // fista.py:143
+    }
+  }
 }
 
 // shared memory: FzShared | beta slice (W doubles) | stages x (R x W x sizeof(TX))
@@ -467,82 +565,362 @@ __global__ void __launch_bounds__(kFzBlock, 1) kf_fused(EngineArgs a, int mode) 
     }
   }
   __syncthreads();
-
-  // ---- publish per-cluster partials (transpose group) ---------------------------
-  const int64_t pv = a.pv;
-  if (warp >= kFzFwdWarps) {
-    const int lt = tid - kFzFwd;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-#pragma unroll
-      for (int e = 0; e < VE; ++e) {
-        const int64_t col = c0 + (int64_t)v * kFzTr * VE + lt * VE + e;
-        if (col < pv) {
-          a.fz_part[(0 * (int64_t)ncl + cid) * pv + col] = accR[v * VE + e];
-          a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
-          if (want_z) a.fz_part[(2 * (int64_t)ncl + cid) * pv + col] = accZ[v * VE + e];
-        }
-      }
-    }
-  }
-  if (bad) sh.bad = 1;
-  if (gbad_R) atomicOr(&sh.bad, 2);
-  if (gbad_N) atomicOr(&sh.bad, 4);
-  const double lsum = block_sum(loss_acc, sh.red);
-  const double f0 = block_sum(f_acc[0], sh.red);
-  const double f1 = block_sum(f_acc[1], sh.red);
-  const double f2 = block_sum(f_acc[2], sh.red);
-  if (crank == 0 && tid == 0) {
-    double* cp = a.fz_cpart + 8 * (int64_t)cid;
-    cp[0] = lsum;
-    cp[1] = (double)sh.bad;
-    cp[2] = f0;
-    cp[3] = f1;
-    cp[4] = f2;
-  }
-  if (cs > 1) cluster_barrier();  // no st.async into this CTA is still in flight
-  __threadfence();
-  __syncthreads();
-  __shared__ int s_last;
-  if (tid == 0) s_last = (atomicAdd(cnt_fused(a), 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // ---- last CTA: loss over clusters (fixed order), objective / restart ---------
-  if (tid == 0) {
-    *cnt_fused(a) = 0u;
-    double tot = 0.0, fs0 = 0.0, fs1 = 0.0, fs2 = 0.0;
-    int flags = 0;
-    for (int c = 0; c < ncl; ++c) {
-      const double* cp = a.fz_cpart + 8 * (int64_t)c;
-      tot += __ldcg(cp);
-      flags |= (int)__ldcg(cp + 1);
-      fs0 += __ldcg(cp + 2);
-      fs1 += __ldcg(cp + 3);
-      fs2 += __ldcg(cp + 4);
-    }
-    a.gv[2 * pv + 0] = fs0;
-    a.gv[2 * pv + 1] = fs1;
-    a.gv[2 * pv + 2] = fs2;
-    a.gv[2 * pv + 6] = (double)flags;   // gradient-candidate validity for KR
-    a.gv[2 * pv + 7] = want_z ? 1.0 : 0.0;
-    if (a.multi) {
-      a.gv[2 * pv + 4] = tot;
-      a.gv[2 * pv + 5] = (double)(flags & 1);
-    } else if (flags & 1) {
-      st->err = ST_INVALID;
-      st->err_iter = (mode == MODE_ITER) ? t : 0;
-      if (mode == MODE_ITER) st->t = t;
-      st->done = 1;
-    } else if (mode == MODE_ITER) {
-      objective_update(st, a.prm, tot);
-    } else {
-      st->loss_cur = tot;
-      st->obj = dadd(tot, dmul(a.prm->two_l2, st->g_next));  // fista.py:143
-    }
-  }
+  kf_finish<NV * VE, VE>(a, mode, t, want_z, cid, crank, c0, warp >= kFzFwdWarps, tid - kFzFwd, accR,
+                         accN, accZ, loss_acc, f_acc, bad, gbad_R, gbad_N, &sh.bad, sh.red);
 }
 
+// ---------------------------------------------------------------------------
+// KF-S: the single pass with the transpose served from shared memory.
+//
+// Same cluster layout and exchange as kf_fused, but a row tile stays in its
+// shared-memory stage until it has been accumulated into X^T r, so X crosses
+// the SM <-> L2 interface once per iteration (kf_fused re-reads each tile from
+// L2).  Five warp roles, no CTA-wide barrier on the per-tile path:
+//   * forward (4 warps): split the tile's columns in quarters, keep their beta
+//     quarter in registers, push per-(warp, row) partial dots to every CTA of
+//     the cluster (st.async, transaction-count mbarrier per partial slot);
+//   * gather (kFsGather warps, tiles round-robin): for tile k, sums the
+//     cs x 4 partials of each row in a fixed order (identical in every CTA),
+//     forms the residuals of the two momentum candidates and zeta (one lane
+//     per row), publishes them in the stage's residual slot (rfull[stage]) and
+//     re-arms the partial slot;
+//   * accumulate (8 warps): each warp on its own, as soon as a stage's
+//     residuals are published, accumulates its columns of X^T [r_R | r_N |
+//     zeta] from the stage and arrives on empty[stage];
+//   * producer (1 warp, one lane): refills a stage with tile k + S once all
+//     eight accumulate warps left it.
+// The gather of tile k+1 overlaps the accumulation of tile k, and the
+// stage refill waits only for the accumulation.
+// Slot reuse: a peer writes partial slot j only after its gather consumed my
+// partial of tile j - S, i.e. after my forward of j - S, which needed my stage
+// refilled after my accumulation (hence my gather, which re-armed the slot) of
+// tile j - 2S: a slot ring of 2 S tiles is never written before it is re-armed.
+constexpr int kFsMaxStages = 16;
+constexpr int kFsMaxSlots = 32;
+constexpr int kFsMaxR = 4;
+constexpr int kFsGather = 4;                        // gather warps (tiles round-robin)
+constexpr int kFsGatherWarp = kFzFwdWarps;          // warps 4..4+kFsGather-1
+constexpr int kFsProdWarp = kFzFwdWarps + kFsGather;          // then the producer warp
+constexpr int kFsAccWarp0 = kFsProdWarp + 1;                  // then eight accumulate warps
+constexpr int kFsBlock = (kFsAccWarp0 + kFzTrWarps) * 32;
+
+struct FsShared {
+  uint64_t full[kFsMaxStages];        // stage landed (bulk-copy complete_tx)
+  uint64_t empty[kFsMaxStages];       // the accumulate warps left the stage
+  uint64_t rfull[kFsMaxStages];       // the stage's residuals are published
+  uint64_t xb[kFsMaxSlots];           // partial slot complete (st.async from every peer)
+  double sy[kFsMaxStages][kFsMaxR];   // y / u_{t-1} of the stage's rows (bulk copies)
+  double su[kFsMaxStages][kFsMaxR];
+  double rr[kFsMaxStages][3][kFsMaxR];   // r_R, r_N, zeta of the stage's rows
+  double red[32];
+  int bad;
+};
+
+__host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~size_t(127); }
+
+// shared memory: FsShared | partial slots [NS][cs][4][R] | stages x (R x W x sizeof(TX))
+template <typename TX, int R, int NV>
+__global__ void __launch_bounds__(kFsBlock, 1) kf_fused_s(EngineArgs a, int mode) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  using V = FzVec<TX>;
+  constexpr int VE = V::N;
+  constexpr int W = NV * kFzTr * VE;           // columns per CTA
+  constexpr int QW = W / kFzFwdWarps;          // columns per forward warp
+  constexpr int FV = QW / (32 * VE);           // vectors per forward lane per row
+  static_assert(R <= kFsMaxR, "rows per tile");
+  static_assert(FV * 32 * VE * kFzFwdWarps == W, "forward column split");
+  FsShared& sh = *reinterpret_cast<FsShared*>(smem);
+  const int cs = a.fz_cs;
+  const int S = a.fz_stages;
+  const int NS = a.fz_slots;
+  double* part = reinterpret_cast<double*>(smem + fs_align(sizeof(FsShared)));
+  const size_t part_bytes = fs_align((size_t)NS * cs * kFzFwdWarps * R * 8);
+  TX* tiles = reinterpret_cast<TX*>(reinterpret_cast<unsigned char*>(part) + part_bytes);
+
+  State* st = a.st;
+  int64_t t = 0;
+  double cN = 0.25;
+  bool want_z = false;
+  if (mode == MODE_ITER) {
+    if (st->done || st->dual_only) return;
+    t = st->t + 1;
+    cN = momentum(st->phi + 1);
+    want_z = is_check(t, a.prm->bci) || !isfinite(st->best_dual);
+  }
+  const double cR = 0.25;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cs > 1 ? cluster_rank() : 0;
+  const int cid = cs > 1 ? (int)cluster_id() : (int)blockIdx.x;
+  const int ncl = a.fz_ncl;
+  const int64_t n = a.n, ld = a.ld;
+  const int64_t c0 = (int64_t)crank * W;
+  const int wvalid = (int)max((int64_t)0, min((int64_t)W, ld - c0));
+  const uint32_t row_bytes = (uint32_t)wvalid * (uint32_t)sizeof(TX);
+  const double* bsrc = (mode == MODE_ITER) ? a.beta + ring(t) * a.pv : a.beta;
+  const double* uprev = a.u + ((mode == MODE_ITER) ? ring(t - 1) * n : 0);
+
+  const int ntiles = (int)a.fz_tiles;
+  const int mytiles = cid < ntiles ? (ntiles - cid + ncl - 1) / ncl : 0;
+  auto tile_of = [&](int k) -> int64_t { return (int64_t)cid + (int64_t)k * ncl; };
+  auto tile_rows = [&](int k) -> int { return (int)min((int64_t)R, n - tile_of(k) * R); };
+  auto slot_bytes = [&](int k) -> uint32_t {
+    return (uint32_t)(cs * kFzFwdWarps * tile_rows(k) * (int)sizeof(double));
+  };
+  // y / u_{t-1} ride along with a tile when their segments are 16-byte bulk copies
+  const bool side_ok = (n % 2 == 0) && (R % 2 == 0);
+  auto side = [&](int k) { return side_ok && (tile_rows(k) % 2 == 0); };
+
+  // columns [wvalid, W) of every stage row are never copied: zero them once
+  // so every role can run over full rows
+  for (int i = tid; i < S * R * (W - wvalid); i += kFsBlock) {
+    const int row = i / (W - wvalid), col = wvalid + i % (W - wvalid);
+    tiles[(int64_t)row * W + col] = TX(0);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kFzTrWarps);
+      mbar_init(&sh.rfull[i], 1);
+    }
+    for (int i = 0; i < NS; ++i) mbar_init(&sh.xb[i], 1);
+    sh.bad = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < NS && k < mytiles; ++k) mbar_arrive_expect(&sh.xb[k], slot_bytes(k));
+  if (cs > 1) cluster_barrier();
+  else __syncthreads();
+
+  double accR[NV * VE], accN[NV * VE], accZ[NV * VE];
+  double loss_acc = 0.0, f_acc[3] = {0.0, 0.0, 0.0};
+  int bad = 0, gbad_R = 0, gbad_N = 0;
+
+  if (warp < kFzFwdWarps) {
+    // ===================== forward =====================
+    const int qc = warp * QW;                  // this warp's column quarter
+    double bq[FV * VE];
+#pragma unroll
+    for (int j = 0; j < FV; ++j)
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        const int64_t col = c0 + qc + (j * 32 + lane) * VE + e;
+        bq[j * VE + e] = col < a.p ? bsrc[col] : 0.0;
+      }
+    int buf = 0, q = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < mytiles; ++k) {
+      const int rows = tile_rows(k);
+      if (tid == 0) FZ_STAMP(a, k, 0);
+      mbar_wait(&sh.full[buf], ph);
+      if (tid == 0) FZ_STAMP(a, k, 1);
+      const TX* tl = tiles + (int64_t)buf * R * W;
+      double d[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double d0 = 0.0, d1 = 0.0;
+        if (r < rows) {
+#pragma unroll
+          for (int j = 0; j < FV; ++j) {   // columns >= wvalid are zero in every stage
+            const int col = qc + (j * 32 + lane) * VE;
+            double x[VE];
+            V::widen(*reinterpret_cast<const typename V::T*>(tl + r * W + col), x);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+              if (((j * VE + e) & 1) == 0) d0 = fma(x[e], bq[j * VE + e], d0);
+              else d1 = fma(x[e], bq[j * VE + e], d1);
+            }
+          }
+        }
+        d[r] = d0 + d1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+      if (lane < cs) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r < rows)
+            st_async_f64(part + (((size_t)q * cs + crank) * kFzFwdWarps + warp) * R + r, &sh.xb[q],
+                         (uint32_t)lane, d[r]);
+      }
+      if (tid == 0) FZ_STAMP(a, k, 2);
+      if (++buf == S) { buf = 0; ph ^= 1u; }
+      if (++q == NS) q = 0;
+    }
+  } else if (warp < kFsGatherWarp + kFsGather) {
+    // ===================== gather =====================
+    const int gw = warp - kFsGatherWarp;
+    const int np = cs * kFzFwdWarps;           // partials per row
+    for (int k = gw; k < mytiles; k += kFsGather) {
+      const int buf = k % S, q = k % NS;
+      const uint32_t ph = (uint32_t)((k / S) & 1), qph = (uint32_t)((k / NS) & 1);
+      const int rows = tile_rows(k);
+      mbar_wait_cluster(&sh.xb[q], qph);
+      mbar_wait(&sh.full[buf], ph);            // y / u_{t-1} of the stage
+      if (lane == 0) FZ_STAMP(a, k, 3);
+      double us[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double v = lane < np ? part[((size_t)q * np + lane) * R + r] : 0.0;
+        for (int j = lane + 32; j < np; j += 32) v += part[((size_t)q * np + j) * R + r];
+        us[r] = v;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) us[r] += __shfl_xor_sync(0xffffffffu, us[r], o);
+      __syncwarp();
+      if (lane == 0 && k + NS < mytiles) mbar_arrive_expect(&sh.xb[q], slot_bytes(k + NS));
+      if (lane < R) {
+        const int r = lane;
+        double u = us[0];
+#pragma unroll
+        for (int i = 1; i < R; ++i)
+          if (r == i) u = us[i];
+        double gR = 0.0, gN = 0.0, gZ = 0.0;
+        if (r < rows) {
+          const int64_t row = tile_of(k) * R + r;
+          double yi, up;
+          if (side(k)) {
+            yi = sh.sy[buf][r];
+            up = (mode == MODE_ITER) ? sh.su[buf][r] : u;
+          } else {
+            yi = a.y[row];
+            up = (mode == MODE_ITER) ? uprev[row] : u;
+          }
+          const double dlt = dsub(u, up);
+          const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
+          const double ugN = dadd(u, dmul(cN, dlt));
+          if (!isfinite(ugR)) gbad_R = 1;
+          if (!isfinite(ugN)) gbad_N = 1;
+          gR = loss_grad(a.loss, ugR, yi);
+          gN = loss_grad(a.loss, ugN, yi);
+          const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
+          gZ = z;
+          if (crank == 0) {
+            if (mode == MODE_ITER) {
+              a.u[ring(t) * n + row] = u;
+            } else {
+              a.u[row] = u;
+              a.u[2 * n + row] = u;
+            }
+            if (!isfinite(u)) bad = 1;
+            loss_acc += loss_term(a.loss, u, yi);
+            if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
+          }
+        }
+        sh.rr[buf][0][r] = gR;
+        sh.rr[buf][1][r] = gN;
+        sh.rr[buf][2][r] = gZ;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.rfull[buf]);
+    }
+  } else if (warp == kFsProdWarp) {
+    // ===================== producer =====================
+    if (lane == 0) {
+      auto issue = [&](int k, int b) {
+        const int64_t tile = tile_of(k);
+        const int rows = tile_rows(k);
+        TX* dst = tiles + (int64_t)b * R * W;
+        const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
+        mbar_arrive_expect(&sh.full[b], row_bytes * rows + sb);
+        if (row_bytes > 0)
+          for (int r = 0; r < rows; ++r)
+            bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
+                     row_bytes, &sh.full[b]);
+        if (sb) {
+          bulk_g2s(&sh.sy[b][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
+          if (mode == MODE_ITER) bulk_g2s(&sh.su[b][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
+        }
+      };
+      for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
+      int buf = 0;
+      uint32_t ph = 0;
+      for (int k = 0; k + S < mytiles; ++k) {
+        mbar_wait(&sh.empty[buf], ph);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + S, buf);
+        if (lane == 0) FZ_STAMP(a, k, 5);
+        if (++buf == S) { buf = 0; ph ^= 1u; }
+      }
+    }
+  } else {
+    // ===================== accumulate =====================
+    const int lt = tid - kFsAccWarp0 * 32;
+#pragma unroll
+    for (int i = 0; i < NV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
+    int buf = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < mytiles; ++k) {
+      const int rows = tile_rows(k);
+      mbar_wait(&sh.rfull[buf], ph);
+      mbar_wait(&sh.full[buf], ph);
+      const TX* tl = tiles + (int64_t)buf * R * W + lt * VE;
+      if (rows == R) {
+        // rows in pairs: a pair's loads are issued before its FMAs
+        constexpr int RP = R >= 2 ? 2 : 1;
+#pragma unroll
+        for (int r0 = 0; r0 < R; r0 += RP) {
+          typename V::T xv[RP][NV];
+#pragma unroll
+          for (int h = 0; h < RP; ++h)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              xv[h][v] = *reinterpret_cast<const typename V::T*>(tl + (r0 + h) * W + v * kFzTr * VE);
+#pragma unroll
+          for (int h = 0; h < RP; ++h) {
+            const int r = r0 + h;
+            const double rR = sh.rr[buf][0][r], rN = sh.rr[buf][1][r];
+            const double rZ = want_z ? sh.rr[buf][2][r] : 0.0;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              double x[VE];
+              V::widen(xv[h][v], x);
+#pragma unroll
+              for (int e = 0; e < VE; ++e) {
+                accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
+                accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+              }
+              if (want_z) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+              }
+            }
+          }
+        }
+      } else {
+        // the last, partial tile of the grid: rows past n hold stale data
+        for (int r = 0; r < rows; ++r) {
+          const double rR = sh.rr[buf][0][r], rN = sh.rr[buf][1][r], rZ = sh.rr[buf][2][r];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double x[VE];
+            V::widen(*reinterpret_cast<const typename V::T*>(tl + r * W + v * kFzTr * VE), x);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+              accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
+              accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+              if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[buf]);
+      if (lt == 0) FZ_STAMP(a, k, 4);
+      if (++buf == S) { buf = 0; ph ^= 1u; }
+    }
+  }
+  __syncthreads();
+  kf_finish<NV * VE, VE>(a, mode, t, want_z, cid, crank, c0, warp >= kFsAccWarp0,
+                         tid - kFsAccWarp0 * 32, accR, accN, accZ, loss_acc, f_acc, bad, gbad_R, gbad_N,
+                         &sh.bad, sh.red);
+}
+
+// ---------------------------------------------------------------------------
 // KR: reduce the per-cluster partials (fixed order), pick the candidate of
 // the restart decision, slab epilogue.  One CTA per 256-column slab.
 __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int epilogue) {
@@ -617,6 +995,10 @@ __global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a) {
 // ---------------------------------------------------------------------------
 static size_t fused_smem(const EngineArgs& a) {
   const size_t es = a.dtype == F64 ? 8 : 4;
+  if (a.fz_smem)
+    return fs_align(sizeof(FsShared)) +
+           fs_align((size_t)a.fz_slots * a.fz_cs * kFzFwdWarps * a.fz_rows * 8) +
+           (size_t)a.fz_stages * (size_t)a.fz_rows * (size_t)a.fz_w * es;
   return ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)a.fz_w +
          (size_t)a.fz_stages * (size_t)a.fz_rows * (size_t)a.fz_w * es;
 }
@@ -634,8 +1016,24 @@ static KfFn kf_pick_nv(int nv) {
   }
 }
 
+template <typename TX, int R>
+static KfFn kfs_pick_nv(int nv) {
+  switch (nv) {
+    case 1: return kf_fused_s<TX, R, 1>;
+    case 2: return kf_fused_s<TX, R, 2>;
+    case 3: return kf_fused_s<TX, R, 3>;
+    case 4: return sizeof(TX) == 8 ? (KfFn)kf_fused_s<TX, R, 4> : nullptr;
+    default: return nullptr;
+  }
+}
+
 static KfFn kf_pick(const EngineArgs& a) {
   const bool f64 = a.dtype == F64;
+  if (a.fz_smem) {
+    if (a.fz_rows == 2) return f64 ? kfs_pick_nv<double, 2>(a.fz_nv) : kfs_pick_nv<float, 2>(a.fz_nv);
+    if (a.fz_rows == 4) return f64 ? kfs_pick_nv<double, 4>(a.fz_nv) : kfs_pick_nv<float, 4>(a.fz_nv);
+    return nullptr;
+  }
   if (a.fz_rows == 4) return f64 ? kf_pick_nv<double, 4>(a.fz_nv) : kf_pick_nv<float, 4>(a.fz_nv);
   if (a.fz_rows == 8) return f64 ? kf_pick_nv<double, 8>(a.fz_nv) : kf_pick_nv<float, 8>(a.fz_nv);
   return nullptr;
@@ -654,7 +1052,7 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3((unsigned)(a.fz_cs * a.fz_ncl));
-  cfg.blockDim = dim3(kFzBlock);
+  cfg.blockDim = dim3(a.fz_smem ? kFsBlock : kFzBlock);
   cfg.dynamicSmemBytes = smem;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.fz_cs;
@@ -665,10 +1063,13 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   return cudaSuccess;
 }
 
-// Choose cluster size, rows per tile and ring depth: the smallest cluster
-// (override: L0_FZ_CS) whose column slice fits the per-thread registers,
-// R = 8 rows per tile (L0_FZ_R: 4 or 8), as many stages as ~200 KB of shared
-// memory holds (<= kFzMaxStages).
+// Choose the kernel variant, cluster size, rows per tile and ring depth.
+//   kf_fused_s (default; L0_FZ_MODE=0 selects kf_fused): the smallest cluster
+//   whose column slice fits the transpose registers, R = 2 rows per tile
+//   (L0_FZ_R: 2 or 4), as many stages as the shared memory holds next to the
+//   partial slots (<= kFsMaxStages, slots = 2 x stages).
+//   kf_fused: R = 4 (L0_FZ_R: 4 or 8), stages within ~170 KB (L0_FZ_KB).
+// L0_FZ_CS forces the cluster size.
 int fused_plan(EngineArgs& a, int sms) {
   (void)sms;
   const int VE = a.dtype == F64 ? 2 : 4;
@@ -677,20 +1078,47 @@ int fused_plan(EngineArgs& a, int sms) {
   const int maxv = a.dtype == F64 ? 4 : 3;
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
+  const char* menv = getenv("L0_FZ_MODE");
+  const int smode = menv ? (atoi(menv) != 0) : 1;
   const char* renv = getenv("L0_FZ_R");
-  const int R = (renv && atoi(renv) == 8) ? 8 : 4;
-  const size_t budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) : 170) * 1024;
+  int R;
+  size_t budget;
+  if (smode) {
+    R = (renv && atoi(renv) == 4) ? 4 : 2;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) * 1024 : std::max(optin, 0));
+  } else {
+    R = (renv && atoi(renv) == 8) ? 8 : 4;
+    budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) : 170) * 1024;
+  }
   for (int cs : {1, 2, 4, 8, 16}) {
     if (want_cs > 0 && cs != want_cs) continue;
     const int64_t need = (a.p + cs - 1) / cs;
     const int64_t W = ((need + unit - 1) / unit) * unit;
     const int nv = (int)(W / unit);
     if (nv > maxv) continue;
-    const size_t fixed = ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)W;
-    if (fixed >= budget) continue;
-    int S = (int)((budget - fixed) / ((size_t)R * (size_t)W * es));
-    S = std::min(S, kFzMaxStages);
-    if (S < 2) continue;
+    int S;
+    if (smode) {
+      // stages S and slots 2S: fixed + 2S*cs*4*R*8 (+ align) + S*R*W*es <= budget
+      const size_t fixed = fs_align(sizeof(FsShared)) + 128;
+      if (fixed >= budget) continue;
+      const size_t per = 2 * (size_t)cs * kFzFwdWarps * R * 8 + (size_t)R * (size_t)W * es;
+      S = (int)((budget - fixed) / per);
+      S = std::min(S, std::min(kFsMaxStages, kFsMaxSlots / 2));
+      if (getenv("L0_FZ_S")) S = std::min(S, atoi(getenv("L0_FZ_S")));
+      if (S < 2) continue;
+      a.fz_slots = 2 * S;
+    } else {
+      const size_t fixed = ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)W;
+      if (fixed >= budget) continue;
+      S = (int)((budget - fixed) / ((size_t)R * (size_t)W * es));
+      S = std::min(S, kFzMaxStages);
+      if (S < 2) continue;
+      a.fz_slots = kFzSlots;
+    }
+    a.fz_smem = smode;
     a.fz_cs = cs;
     a.fz_w = W;
     a.fz_nv = nv;
@@ -710,8 +1138,8 @@ int fused_plan(EngineArgs& a, int sms) {
     }
     e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
     if (getenv("L0_DEBUG"))
-      fprintf(stderr, "fused_plan: cs=%d W=%lld nv=%d R=%d S=%d smem=%zu ncl=%d (%s)\n", cs,
-              (long long)W, nv, R, S, fused_smem(a), ncl, cudaGetErrorString(e));
+      fprintf(stderr, "fused_plan: mode=%d cs=%d W=%lld nv=%d R=%d S=%d slots=%d smem=%zu ncl=%d (%s)\n",
+              smode, cs, (long long)W, nv, R, S, a.fz_slots, fused_smem(a), ncl, cudaGetErrorString(e));
     if (e != cudaSuccess || ncl < 1) {
       cudaGetLastError();
       return 0;

@@ -2,7 +2,7 @@
 python tools/ncu_summary.py out.json rep1.ncu-rep [rep2 ...]"""
 import csv, json, re, subprocess, sys
 
-SHORT = [("kf_fused", "kf_fused"), ("k1_forward", "k1_forward"), ("k2_transpose", "k2_transpose"),
+SHORT = [("kf_fused_s", "kf_fused_s"), ("kf_fused", "kf_fused"), ("k1_forward", "k1_forward"), ("k2_transpose", "k2_transpose"),
          ("k3_prox_window", "k3_prox_window"), ("kr_reduce", "kr_reduce"), ("tc_gemm_kernel", "tc_gemm_kernel"),
          ("kb_window", "kb_window"), ("kb_step", "kb_step"), ("kb_obj", "kb_obj"), ("kb_rhs", "kb_rhs")]
 METRICS = {"gpu__time_duration.sum": ("duration_us", 1.0), "dram__bytes_read.sum": ("dram_read_bytes", None),

@@ -6,7 +6,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 tail -3 gpurun_out/bench.err
 timeout 600 $B > gpurun_out/plain.log 2>&1; echo plain_rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo launch_rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:kf_fused -s 3 -c 1 -o gpurun_out/prof_kf $B > gpurun_out/ncu_kf.log 2>&1; echo kf_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:kf_fused_s -s 3 -c 1 -o gpurun_out/prof_kf $B > gpurun_out/ncu_kf.log 2>&1; echo kf_rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k3_prox_window" -s 16 -c 1 -o gpurun_out/prof_k3 $B > gpurun_out/ncu_k3.log 2>&1; echo k3_rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kr_reduce" -s 16 -c 1 -o gpurun_out/prof_kr $B > gpurun_out/ncu_kr.log 2>&1; echo kr_rc=$?
 timeout 600 $B --engine two_pass > gpurun_out/plain2.log 2>&1; echo plain2_rc=$?
