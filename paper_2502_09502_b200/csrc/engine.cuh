@@ -79,8 +79,7 @@ struct EngineArgs {
   int fused;         // 1: iterations run K3 -> KF -> KR instead of K2 -> K3 -> K1
   int fz_cs, fz_ncl, fz_nv, fz_rows;   // cluster size, clusters, vectors/thread, rows/tile
   int fz_stages;     // shared-memory tile ring depth
-  int fz_slots;      // partial-slot ring depth (kf_fused_s)
-  int fz_smem;       // 1: kf_fused_s (transpose from the shared-memory stage), 0: kf_fused
+  int fz_slots;      // partial-slot ring depth
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)
   int64_t fz_tiles;  // row tiles
   double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta)

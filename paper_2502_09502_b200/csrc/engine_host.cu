@@ -566,11 +566,11 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   hp.node_mode = node_mode ? 1 : 0;
   hp.loss = a.loss;
   // engine path: auto = the single physical pass where it is measured faster
-  // (fp64 X far beyond L2 with a 4..8-CTA cluster per row block: C2 1847 vs
-  // 1419 it/s), the two-pass engine otherwise (fp32 X: the transposes
-  // dominate; small X: L2 serves the second pass)
-  const double x_bytes = (double)a.n * (double)a.ld * 8.0;
-  const int auto_fused = P->fused_planned && a.dtype == F64 && a.fz_cs >= 4 && a.fz_cs <= 8 &&
+  // (X far beyond L2 with a 4..8-CTA cluster per row block: C2 2322 vs 1442
+  // it/s, C5 73.6 vs 64.3, C3 even), the two-pass engine otherwise (small X:
+  // L2 serves the second pass)
+  const double x_bytes = (double)a.n * (double)a.ld * (a.dtype == F64 ? 8.0 : 4.0);
+  const int auto_fused = P->fused_planned && a.fz_cs >= 4 && a.fz_cs <= 8 &&
                          x_bytes > 512e6;   // L2-resident X (C1): the second pass hits L2
   const int want_fused = (o->engine_path == 2) ? P->fused_planned
                          : (o->engine_path == 1) ? 0 : auto_fused;

@@ -4,32 +4,27 @@
 // gradient X^T grad F(u_t + c_{t+1} (u_t - u_{t-1})), whose momentum c_{t+1}
 // depends on the restart decision, i.e. on ALL rows of u_t.  KF computes both
 // candidates -- c = 1/4 (restart, phi -> 1) and c = (phi+1)/(phi+4) (no
-// restart) -- plus X^T zeta_t for the bound check, from the same X tile:
+// restart) -- plus X^T zeta_t for the bound check, from ONE read of each X
+// tile (kf_fused_s below):
 //
 //   * a thread-block cluster of fz_cs CTAs spans a full row block; CTA c owns
-//     columns [c W, (c+1) W) with its beta slice in shared memory;
+//     columns [c W, (c+1) W);
 //   * row tiles (fz_rows rows x W columns) stream HBM -> shared memory with
-//     cp.async.bulk into a ring of fz_stages buffers (one mbarrier each);
-//   * forward: per-row partial dots of tile k+D (D tiles of lookahead),
-//     block-reduced in a fixed order and pushed to EVERY CTA of the cluster
-//     with st.async into a ring of kFzSlots partial slots, each completing a
+//     cp.async.bulk into a ring of fz_stages buffers and stay there until
+//     their rows are accumulated into X^T r;
+//   * per-row partial dots are pushed to EVERY CTA of the cluster with
+//     st.async into a ring of partial slots, each completing a
 //     transaction-count mbarrier in the receiving CTA -- no cluster barrier
-//     on the per-tile path, the exchange latency hides behind D tiles;
-//   * transpose: when tile k's partials are complete, u for its rows is the
-//     fixed-order sum over the cluster (identical in every CTA), and the same
-//     shared-memory tile accumulates X^T [r_R | r_N | zeta] in registers;
+//     on the per-tile path;
+//   * when tile k's partials are complete, u for its rows is the fixed-order
+//     sum over the cluster (identical in every CTA), and the tile in shared
+//     memory accumulates X^T [r_R | r_N | zeta] in registers;
 //   * the last CTA of the grid reduces the per-cluster loss (fixed order) and
 //     runs the objective / restart logic (control.cuh).
 //
 // KR then reduces the per-cluster partials over clusters (fixed order), picks
 // the candidate matching the restart decision and runs the slab epilogue
 // (gradient step, keys, window candidates, Huber values).
-//
-// Flow control: a CTA's forward group works on tile j only once its
-// transpose group freed stage j - S, which needed every peer's partials of
-// j - S; a peer that published those has its own transpose past j - 2S, so
-// partial slot j (mod kFzSlots) is never one the peer still has to read as
-// long as kFzSlots >= 2 S.
 
 #include <cstdio>
 #include <cstdlib>
@@ -40,13 +35,6 @@
 
 namespace l0 {
 
-constexpr int kFzMaxRows = 8;
-constexpr int kFzMaxCs = 16;
-constexpr int kFzSlots = 16;   // partial-slot ring (2 x the forward lead, see flow control)
-constexpr int kFzTB = 4;       // tiles per transpose step
-// vectors (16 B) per thread per row: 8 fp64 or 12 fp32 columns per thread,
-// i.e. 24 / 36 fp64 accumulators for the three right-hand sides
-template <typename TX> constexpr int fz_maxv() { return sizeof(TX) == 8 ? 4 : 3; }
 
 // ---------------------------------------------------------------------------
 // PTX helpers: mbarrier, bulk copy, cluster barrier, DSMEM
@@ -148,28 +136,9 @@ template <> struct FzVec<float> {
   }
 };
 
-constexpr int kFzFwdWarps = 4;                      // forward group
-constexpr int kFzTrWarps = 8;                       // transpose group
-constexpr int kFzFwd = kFzFwdWarps * 32;            // 128 threads
-constexpr int kFzTr = kFzTrWarps * 32;              // 256 threads
-constexpr int kFzBlock = kFzFwd + kFzTr;            // 384 threads
-constexpr int kFzMaxStages = 12;
-constexpr int kFzLead = kFzSlots / 2;   // forward may run at most this many tiles ahead
-
-struct FzShared {
-  uint64_t full[kFzMaxStages];              // tile ring (bulk-copy complete_tx)
-  uint64_t empty[kFzMaxStages];             // forward warps done reading a stage
-  uint64_t xb[kFzSlots];                    // partial slots (st.async complete_tx)
-  uint64_t tfree[kFzLead];                  // transpose group finished tile j (ring)
-  double part[kFzSlots][kFzMaxCs][kFzMaxRows];   // [slot][source rank][row]
-  double yv[kFzSlots][kFzMaxRows];          // y and u_{t-1} of the slot's rows (self st.async)
-  double up[kFzSlots][kFzMaxRows];
-  double sy[kFzMaxStages][kFzMaxRows];      // y / u_{t-1} of a stage's rows (bulk copies
-  double su[kFzMaxStages][kFzMaxRows];      // under the stage's barrier)
-  double rr[3][kFzTB * kFzMaxRows];         // r_R, r_N, zeta of the transpose group's step
-  double red[32];
-  int bad;
-};
+constexpr int kFzFwdWarps = 4;                      // forward warps
+constexpr int kFzTrWarps = 8;                       // accumulate warps
+constexpr int kFzTr = kFzTrWarps * 32;              // 256 accumulate threads
 
 __device__ __forceinline__ double gtimer() {
   uint64_t t;
@@ -188,9 +157,6 @@ __device__ __forceinline__ double gtimer() {
 #define FZ_STAMP(a, slotk, which) do { } while (0)
 #endif
 
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
 }
@@ -282,300 +248,12 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
   }
 }
 
-// shared memory: FzShared | beta slice (W doubles) | stages x (R x W x sizeof(TX))
-//
-// Warps 0-3 (forward group) stream tiles through the bulk-copy ring; warp w
-// owns rows w, w+4, ... of a tile: its lanes dot the row with the beta slice,
-// one warp reduction per row, and lanes 0..cs-1 push the row's partial to
-// every CTA of the cluster with st.async (lane 0 also y / u_{t-1} to this
-// CTA).  The stage is refilled as soon as the four warps have read it, so all
-// but one stage are in flight.  Warps 4-11 (transpose group) consume tiles in
-// order: the tile's rows are re-read from L2 into registers first (the loads
-// do not depend on r), then u and r from the complete partials, then the
-// three accumulations.  HBM sees X once.
-//   R  rows per tile (multiple of 4)     NV 16-byte vectors per transpose thread
-template <typename TX, int R, int NV>
-__global__ void __launch_bounds__(kFzBlock, 1) kf_fused(EngineArgs a, int mode) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  using V = FzVec<TX>;
-  constexpr int VE = V::N;
-  constexpr int W = NV * kFzTr * VE;          // columns per CTA
-  constexpr int FV = W / (32 * VE);            // vectors per forward lane per row
-  constexpr int RPW = R / kFzFwdWarps;         // rows per forward warp
-  static_assert(R % kFzFwdWarps == 0 && R <= kFzMaxRows, "rows per tile");
-  FzShared& sh = *reinterpret_cast<FzShared*>(smem);
-  double* sbeta = reinterpret_cast<double*>(smem + ((sizeof(FzShared) + 127) & ~size_t(127)));
-  TX* tiles = reinterpret_cast<TX*>(sbeta + W);
-  const int S = a.fz_stages;
-
-  State* st = a.st;
-  int64_t t = 0;
-  double cN = 0.25;
-  bool want_z;
-  if (mode == MODE_ITER) {
-    if (st->done || st->dual_only) return;
-    t = st->t + 1;
-    cN = momentum(st->phi + 1);
-    // zeta_t is needed by a bound check at t, or by a final bound pass
-    want_z = is_check(t, a.prm->bci) || !isfinite(st->best_dual);
-  } else {
-    want_z = false;
-  }
-  const double cR = 0.25;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cs = a.fz_cs;
-  const uint32_t crank = cs > 1 ? cluster_rank() : 0;
-  const int cid = cs > 1 ? (int)cluster_id() : (int)blockIdx.x;
-  const int ncl = a.fz_ncl;
-  const int64_t n = a.n, ld = a.ld;
-  const int64_t c0 = (int64_t)crank * W;                      // first column of this CTA
-  const int wvalid = (int)max((int64_t)0, min((int64_t)W, ld - c0));   // columns inside the row
-  const uint32_t row_bytes = (uint32_t)wvalid * (uint32_t)sizeof(TX);
-  const double* bsrc = (mode == MODE_ITER) ? a.beta + ring(t) * a.pv : a.beta;
-  const double* uprev = a.u + ((mode == MODE_ITER) ? ring(t - 1) * n : 0);
-
-  // static tile schedule of this cluster: cid, cid + ncl, ...
-  const int ntiles = (int)a.fz_tiles;
-  const int mytiles = cid < ntiles ? (ntiles - cid + ncl - 1) / ncl : 0;
-  auto tile_of = [&](int k) -> int64_t { return (int64_t)cid + (int64_t)k * ncl; };
-  auto tile_rows = [&](int k) -> int { return (int)min((int64_t)R, n - tile_of(k) * R); };
-  auto slot_bytes = [&](int k) -> uint32_t {
-    return (uint32_t)((cs + 2) * tile_rows(k) * (int)sizeof(double));
-  };
-
-  for (int j = tid; j < W; j += kFzBlock) {
-    const int64_t col = c0 + j;
-    sbeta[j] = col < a.p ? bsrc[col] : 0.0;
-  }
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&sh.full[i], 1);
-      mbar_init(&sh.empty[i], kFzFwdWarps);
-    }
-    for (int i = 0; i < kFzSlots; ++i) mbar_init(&sh.xb[i], 1);
-    for (int i = 0; i < kFzLead; ++i) mbar_init(&sh.tfree[i], 1);
-    sh.bad = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < kFzSlots && k < mytiles; ++k) mbar_arrive_expect(&sh.xb[k], slot_bytes(k));
-  // every CTA's barriers are initialised and armed before anyone sends
-  if (cs > 1) cluster_barrier();
-  else __syncthreads();
-
-  // y / u_{t-1} ride along with a tile when their segments are 16-byte bulk
-  // copies (even row counts and offsets); otherwise the forward group loads them
-  const bool side_ok = (n % 2 == 0);
-  auto side = [&](int k) { return side_ok && (tile_rows(k) % 2 == 0); };
-  auto issue = [&](int k, int buf) {
-    const int64_t tile = tile_of(k);
-    const int rows = tile_rows(k);
-    TX* dst = tiles + (int64_t)buf * R * W;
-    const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
-    mbar_arrive_expect(&sh.full[buf], row_bytes * rows + sb);
-    if (row_bytes > 0)
-      for (int r = 0; r < rows; ++r)
-        bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
-                 row_bytes, &sh.full[buf]);
-    if (sb) {
-      bulk_g2s(&sh.sy[buf][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[buf]);
-      if (mode == MODE_ITER) bulk_g2s(&sh.su[buf][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[buf]);
-    }
-  };
-
-  double accR[NV * VE], accN[NV * VE], accZ[NV * VE];
-  double loss_acc = 0.0, f_acc[3] = {0.0, 0.0, 0.0};
-  int bad = 0, gbad_R = 0, gbad_N = 0;
-
-  if (warp < kFzFwdWarps) {
-    // ===================== forward group =====================
-    if (tid == 0)
-      for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
-    int buf = 0;
-    uint32_t ph = 0;
-    for (int k = 0; k < mytiles; ++k) {
-      const int rows = tile_rows(k);
-      const int q = k % kFzSlots;
-      if (tid == 0) FZ_STAMP(a, k, 0);
-      // flow control: at most kFzLead tiles ahead of this CTA's transpose group
-      if (k >= kFzLead) mbar_wait(&sh.tfree[(k - kFzLead) % kFzLead], (uint32_t)(((k - kFzLead) / kFzLead) & 1));
-      mbar_wait(&sh.full[buf], ph);
-      const TX* tl = tiles + (int64_t)buf * R * W;
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int r = warp + i * kFzFwdWarps;
-        if (r < rows) {
-          double d0 = 0.0, d1 = 0.0;      // two chains for ILP
-#pragma unroll
-          for (int j = 0; j < FV; ++j) {
-            const int col = (j * 32 + lane) * VE;
-            if (col < wvalid) {
-              double x[VE];
-              V::widen(*reinterpret_cast<const typename V::T*>(tl + r * W + col), x);
-#pragma unroll
-              for (int e = 0; e < VE; ++e) {
-                if (((j * VE + e) & 1) == 0) d0 = fma(x[e], sbeta[col + e], d0);
-                else d1 = fma(x[e], sbeta[col + e], d1);
-              }
-            }
-          }
-          const double dsum = warp_sum(d0 + d1);
-          if (lane < cs) st_async_f64(&sh.part[q][crank][r], &sh.xb[q], (uint32_t)lane, dsum);
-          if (lane == 0) {
-            double yv, uv;
-            if (side(k)) {
-              yv = sh.sy[buf][r];
-              uv = (mode == MODE_ITER) ? sh.su[buf][r] : 0.0;
-            } else {
-              const int64_t row = tile_of(k) * R + r;
-              yv = a.y[row];
-              uv = (mode == MODE_ITER) ? uprev[row] : 0.0;
-            }
-            st_async_f64(&sh.yv[q][r], &sh.xb[q], crank, yv);
-            st_async_f64(&sh.up[q][r], &sh.xb[q], crank, uv);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[buf]);
-      if (tid == 0) {
-        FZ_STAMP(a, k, 1);
-        if (k + S < mytiles) {
-          mbar_wait(&sh.empty[buf], ph);           // all four warps read the stage
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(k + S, buf);
-        }
-      }
-      if (++buf == S) { buf = 0; ph ^= 1u; }
-    }
-  } else {
-    // ===================== transpose group =====================
-    // steps of kFzTB tiles: one gather and two barriers per step; the step's
-    // rows stream from L2 in double-buffered pairs (the loads of the next
-    // pair are in flight while the current pair is accumulated)
-    const int lt = tid - kFzFwd;
-#pragma unroll
-    for (int i = 0; i < NV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
-    const TX* xcols = static_cast<const TX*>(a.X) + c0;
-    constexpr int RT = kFzTB * R;                 // rows per step
-    static_assert(RT % 4 == 0, "rows per step");
-    auto row_ok = [&](int k0, int nt, int rho) {
-      const int i = rho / R;
-      return i < nt && (rho % R) < tile_rows(k0 + i);
-    };
-    auto load_pair = [&](int k0, int nt, int g, typename V::T (&dst)[2][NV]) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rho = 2 * g + h;
-        const bool ok = row_ok(k0, nt, rho);
-        const int64_t row = tile_of(k0 + rho / R) * R + rho % R;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int col = v * kFzTr * VE + lt * VE;
-          if (ok && col < wvalid)
-            dst[h][v] = __ldg(reinterpret_cast<const typename V::T*>(xcols + row * ld + col));
-          else
-            dst[h][v] = typename V::T{};
-        }
-      }
-    };
-    auto fma_pair = [&](int g, const typename V::T (&src)[2][NV]) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rho = 2 * g + h;
-        const double rR = sh.rr[0][rho], rN = sh.rr[1][rho], rZ = sh.rr[2][rho];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double x[VE];
-          V::widen(src[h][v], x);
-#pragma unroll
-          for (int e = 0; e < VE; ++e) {
-            accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-            accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
-            if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
-          }
-        }
-      }
-    };
-    for (int k0 = 0; k0 < mytiles; k0 += kFzTB) {
-      const int nt = min(kFzTB, mytiles - k0);
-      typename V::T xa[2][NV], xb2[2][NV];
-      for (int i = 0; i < nt; ++i) {
-        const int k = k0 + i;
-        mbar_wait_cluster(&sh.xb[k % kFzSlots], (uint32_t)((k / kFzSlots) & 1));
-      }
-      load_pair(k0, nt, 0, xa);                  // first pair's latency overlaps the gather
-      if (lt == 0) FZ_STAMP(a, k0, 2);
-      if (lt < RT) {
-        const int i = lt / R, r = lt % R;
-        double gR = 0.0, gN = 0.0, gZ = 0.0;
-        if (i < nt && r < tile_rows(k0 + i)) {
-          const int k = k0 + i;
-          const int q = k % kFzSlots;
-          double u = 0.0;
-          for (int c = 0; c < cs; ++c) u += sh.part[q][c][r];
-          const int64_t row = tile_of(k) * R + r;
-          const double yi = sh.yv[q][r];
-          const double up = (mode == MODE_ITER) ? sh.up[q][r] : u;
-          const double dlt = dsub(u, up);
-          const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
-          const double ugN = dadd(u, dmul(cN, dlt));
-          if (!isfinite(ugR)) gbad_R = 1;
-          if (!isfinite(ugN)) gbad_N = 1;
-          gR = loss_grad(a.loss, ugR, yi);
-          gN = loss_grad(a.loss, ugN, yi);
-          const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
-          gZ = z;
-          if (crank == 0) {
-            if (mode == MODE_ITER) {
-              a.u[ring(t) * n + row] = u;
-            } else {
-              a.u[row] = u;
-              a.u[2 * n + row] = u;
-            }
-            if (!isfinite(u)) bad = 1;
-            loss_acc += loss_term(a.loss, u, yi);
-            if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
-          }
-        }
-        sh.rr[0][lt] = gR;
-        sh.rr[1][lt] = gN;
-        sh.rr[2][lt] = gZ;
-      }
-      named_sync(2, kFzTr);
-      // the step's slots are consumed: arm them for the tiles kFzSlots later
-      if (lt == 0)
-        for (int i = 0; i < nt; ++i) {
-          const int k = k0 + i;
-          if (k + kFzSlots < mytiles) mbar_arrive_expect(&sh.xb[k % kFzSlots], slot_bytes(k + kFzSlots));
-        }
-#pragma unroll
-      for (int g = 0; g < RT / 2; g += 2) {
-        load_pair(k0, nt, g + 1, xb2);
-        fma_pair(g, xa);
-        if (g + 2 < RT / 2) load_pair(k0, nt, g + 2, xa);
-        fma_pair(g + 1, xb2);
-      }
-      named_sync(2, kFzTr);      // rr reusable
-      if (lt == 0) {
-        FZ_STAMP(a, k0, 3);
-        for (int i = 0; i < nt; ++i) mbar_arrive(&sh.tfree[(k0 + i) % kFzLead]);
-      }
-    }
-  }
-  __syncthreads();
-  kf_finish<NV * VE, VE>(a, mode, t, want_z, cid, crank, c0, warp >= kFzFwdWarps, tid - kFzFwd, accR,
-                         accN, accZ, loss_acc, f_acc, bad, gbad_R, gbad_N, &sh.bad, sh.red);
-}
-
 // ---------------------------------------------------------------------------
-// KF-S: the single pass with the transpose served from shared memory.
-//
-// Same cluster layout and exchange as kf_fused, but a row tile stays in its
-// shared-memory stage until it has been accumulated into X^T r, so X crosses
-// the SM <-> L2 interface once per iteration (kf_fused re-reads each tile from
-// L2).  Five warp roles, no CTA-wide barrier on the per-tile path:
+// kf_fused_s: a row tile stays in its shared-memory stage until it has been
+// accumulated into X^T r, so X crosses the SM <-> L2 interface once per
+// iteration (round 1's first single-pass kernel re-read every tile from L2
+// for the transpose and ran at 0.485 ms on C2, this one at 0.353 ms).  Four
+// warp roles, no CTA-wide barrier on the per-tile path:
 //   * forward (4 warps): split the tile's columns in quarters, keep their beta
 //     quarter in registers, push per-(warp, row) partial dots to every CTA of
 //     the cluster (st.async, transaction-count mbarrier per partial slot);
@@ -995,26 +673,11 @@ __global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a) {
 // ---------------------------------------------------------------------------
 static size_t fused_smem(const EngineArgs& a) {
   const size_t es = a.dtype == F64 ? 8 : 4;
-  if (a.fz_smem)
-    return fs_align(sizeof(FsShared)) +
-           fs_align((size_t)a.fz_slots * a.fz_cs * kFzFwdWarps * a.fz_rows * 8) +
-           (size_t)a.fz_stages * (size_t)a.fz_rows * (size_t)a.fz_w * es;
-  return ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)a.fz_w +
+  return fs_align(sizeof(FsShared)) + fs_align((size_t)a.fz_slots * a.fz_cs * kFzFwdWarps * a.fz_rows * 8) +
          (size_t)a.fz_stages * (size_t)a.fz_rows * (size_t)a.fz_w * es;
 }
 
 using KfFn = void (*)(EngineArgs, int);
-
-template <typename TX, int R>
-static KfFn kf_pick_nv(int nv) {
-  switch (nv) {
-    case 1: return kf_fused<TX, R, 1>;
-    case 2: return kf_fused<TX, R, 2>;
-    case 3: return kf_fused<TX, R, 3>;
-    case 4: return sizeof(TX) == 8 ? (KfFn)kf_fused<TX, R, 4> : nullptr;
-    default: return nullptr;
-  }
-}
 
 template <typename TX, int R>
 static KfFn kfs_pick_nv(int nv) {
@@ -1029,13 +692,8 @@ static KfFn kfs_pick_nv(int nv) {
 
 static KfFn kf_pick(const EngineArgs& a) {
   const bool f64 = a.dtype == F64;
-  if (a.fz_smem) {
-    if (a.fz_rows == 2) return f64 ? kfs_pick_nv<double, 2>(a.fz_nv) : kfs_pick_nv<float, 2>(a.fz_nv);
-    if (a.fz_rows == 4) return f64 ? kfs_pick_nv<double, 4>(a.fz_nv) : kfs_pick_nv<float, 4>(a.fz_nv);
-    return nullptr;
-  }
-  if (a.fz_rows == 4) return f64 ? kf_pick_nv<double, 4>(a.fz_nv) : kf_pick_nv<float, 4>(a.fz_nv);
-  if (a.fz_rows == 8) return f64 ? kf_pick_nv<double, 8>(a.fz_nv) : kf_pick_nv<float, 8>(a.fz_nv);
+  if (a.fz_rows == 2) return f64 ? kfs_pick_nv<double, 2>(a.fz_nv) : kfs_pick_nv<float, 2>(a.fz_nv);
+  if (a.fz_rows == 4) return f64 ? kfs_pick_nv<double, 4>(a.fz_nv) : kfs_pick_nv<float, 4>(a.fz_nv);
   return nullptr;
 }
 
@@ -1052,7 +710,7 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3((unsigned)(a.fz_cs * a.fz_ncl));
-  cfg.blockDim = dim3(a.fz_smem ? kFsBlock : kFzBlock);
+  cfg.blockDim = dim3(kFsBlock);
   cfg.dynamicSmemBytes = smem;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.fz_cs;
@@ -1063,62 +721,41 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   return cudaSuccess;
 }
 
-// Choose the kernel variant, cluster size, rows per tile and ring depth.
-//   kf_fused_s (default; L0_FZ_MODE=0 selects kf_fused): the smallest cluster
-//   whose column slice fits the transpose registers, R = 2 rows per tile
-//   (L0_FZ_R: 2 or 4), as many stages as the shared memory holds next to the
-//   partial slots (<= kFsMaxStages, slots = 2 x stages).
-//   kf_fused: R = 4 (L0_FZ_R: 4 or 8), stages within ~170 KB (L0_FZ_KB).
-// L0_FZ_CS forces the cluster size.
+// Cluster size, rows per tile and ring depth: the smallest cluster (override:
+// L0_FZ_CS) whose column slice fits the accumulate registers, R = 2 rows per
+// tile (L0_FZ_R: 2 or 4; measured on C2: 0.352 vs 0.39 ms with the R = 4
+// register spill), and as many stages as the shared memory holds next to the
+// partial slots (<= kFsMaxStages; slots = 2 x stages, see the slot-reuse
+// argument above; L0_FZ_S caps the stages).
 int fused_plan(EngineArgs& a, int sms) {
   (void)sms;
   const int VE = a.dtype == F64 ? 2 : 4;
-  const int64_t unit = (int64_t)kFzTr * VE;   // columns per transpose-thread vector sweep
+  const int64_t unit = (int64_t)kFzTr * VE;   // columns per accumulate-thread vector sweep
   const size_t es = a.dtype == F64 ? 8 : 4;
   const int maxv = a.dtype == F64 ? 4 : 3;
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
-  const char* menv = getenv("L0_FZ_MODE");
-  const int smode = menv ? (atoi(menv) != 0) : 1;
   const char* renv = getenv("L0_FZ_R");
-  int R;
-  size_t budget;
-  if (smode) {
-    R = (renv && atoi(renv) == 4) ? 4 : 2;
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) * 1024 : std::max(optin, 0));
-  } else {
-    R = (renv && atoi(renv) == 8) ? 8 : 4;
-    budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) : 170) * 1024;
-  }
+  const int R = (renv && atoi(renv) == 4) ? 4 : 2;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t budget = (size_t)(getenv("L0_FZ_KB") ? atoi(getenv("L0_FZ_KB")) * 1024 : std::max(optin, 0));
   for (int cs : {1, 2, 4, 8, 16}) {
     if (want_cs > 0 && cs != want_cs) continue;
     const int64_t need = (a.p + cs - 1) / cs;
     const int64_t W = ((need + unit - 1) / unit) * unit;
     const int nv = (int)(W / unit);
     if (nv > maxv) continue;
-    int S;
-    if (smode) {
-      // stages S and slots 2S: fixed + 2S*cs*4*R*8 (+ align) + S*R*W*es <= budget
-      const size_t fixed = fs_align(sizeof(FsShared)) + 128;
-      if (fixed >= budget) continue;
-      const size_t per = 2 * (size_t)cs * kFzFwdWarps * R * 8 + (size_t)R * (size_t)W * es;
-      S = (int)((budget - fixed) / per);
-      S = std::min(S, std::min(kFsMaxStages, kFsMaxSlots / 2));
-      if (getenv("L0_FZ_S")) S = std::min(S, atoi(getenv("L0_FZ_S")));
-      if (S < 2) continue;
-      a.fz_slots = 2 * S;
-    } else {
-      const size_t fixed = ((sizeof(FzShared) + 127) & ~size_t(127)) + 8 * (size_t)W;
-      if (fixed >= budget) continue;
-      S = (int)((budget - fixed) / ((size_t)R * (size_t)W * es));
-      S = std::min(S, kFzMaxStages);
-      if (S < 2) continue;
-      a.fz_slots = kFzSlots;
-    }
-    a.fz_smem = smode;
+    // stages S and slots 2S: fixed + 2S*cs*4*R*8 (+ align) + S*R*W*es <= budget
+    const size_t fixed = fs_align(sizeof(FsShared)) + 128;
+    if (fixed >= budget) continue;
+    const size_t per = 2 * (size_t)cs * kFzFwdWarps * R * 8 + (size_t)R * (size_t)W * es;
+    int S = (int)((budget - fixed) / per);
+    S = std::min(S, std::min(kFsMaxStages, kFsMaxSlots / 2));
+    if (getenv("L0_FZ_S")) S = std::min(S, atoi(getenv("L0_FZ_S")));
+    if (S < 2) continue;
+    a.fz_slots = 2 * S;
     a.fz_cs = cs;
     a.fz_w = W;
     a.fz_nv = nv;
@@ -1138,8 +775,8 @@ int fused_plan(EngineArgs& a, int sms) {
     }
     e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
     if (getenv("L0_DEBUG"))
-      fprintf(stderr, "fused_plan: mode=%d cs=%d W=%lld nv=%d R=%d S=%d slots=%d smem=%zu ncl=%d (%s)\n",
-              smode, cs, (long long)W, nv, R, S, a.fz_slots, fused_smem(a), ncl, cudaGetErrorString(e));
+      fprintf(stderr, "fused_plan: cs=%d W=%lld nv=%d R=%d S=%d slots=%d smem=%zu ncl=%d (%s)\n", cs,
+              (long long)W, nv, R, S, a.fz_slots, fused_smem(a), ncl, cudaGetErrorString(e));
     if (e != cudaSuccess || ncl < 1) {
       cudaGetLastError();
       return 0;
