@@ -305,3 +305,46 @@ def test_single_pass_engine_matches_two_pass(engine, case):
     for x, y in zip(ra, rb):
         assert y["primal"] == pytest.approx(x["primal"], rel=1e-12)
     np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,dtype,loss", [
+    (1001, 3001, "fp64", "squared_error"),    # odd n: y / u_{t-1} loaded per row; odd p: padded columns
+    (7, 5, "fp64", "squared_error"),          # one partial tile, one CTA per cluster
+    (301, 20000, "fp64", "squared_error"),    # 16-CTA (non-portable) clusters, 3 vectors per thread
+    (999, 5003, "fp32", "logistic"),          # fp32 X, odd n, partial last tile
+    (2048, 9000, "fp64", "logistic"),         # 8-CTA clusters, last CTA's slice partly past p
+])
+def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
+    """kf_fused_s on ragged shapes (odd rows, partial last tile, slices past p,
+    every cluster size the plan can pick) against the two-pass engine."""
+    rng = np.random.default_rng(n * 7 + p)
+    X = rng.standard_normal((n, p))
+    if dtype == "fp32":
+        X = X.astype(np.float32)
+    beta_true = np.zeros(p)
+    beta_true[:: max(1, p // 5)] = 1.0
+    u = X.astype(np.float64) @ beta_true
+    if loss == "logistic":
+        y = np.where(rng.random(n) < 1.0 / (1.0 + np.exp(-u)), 1.0, -1.0)
+    else:
+        y = u + rng.standard_normal(n)
+    k = min(5, p)
+    inst = engine.ProblemInstance(X, y, engine.LossKind(loss), k, 2.0, 0.5, dtype=dtype)
+    curv = 0.25 if loss == "logistic" else 2.0
+    L = curv * 1.01 * float(np.linalg.norm(X.astype(np.float64), 2) ** 2)
+    res = {}
+    for path in ("two_pass", "single_pass"):
+        rec = []
+        res[path] = (engine.solve_relaxation(inst, opts=engine.FistaOptions(
+            lipschitz=L, max_iterations=30, gap_tolerance=1e-300, engine_path=path,
+            trace_hook=rec.append)), rec)
+    (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
+    assert b.stats["single_pass"] and not a.stats["single_pass"]
+    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 2, 9000: 8}[p]
+    assert a.iterations == b.iterations == 30
+    assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
+    assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9, abs=1e-12)
+    for x, y_ in zip(ra, rb):
+        assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
+    np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
