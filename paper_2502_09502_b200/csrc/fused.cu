@@ -257,7 +257,7 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
 //   * forward (4 warps): split the tile's columns in quarters, keep their beta
 //     quarter in registers, push per-(warp, row) partial dots to every CTA of
 //     the cluster (st.async, transaction-count mbarrier per partial slot);
-//   * gather (kFsGather warps, tiles round-robin): for tile k, sums the
+//   * gather (G warps, tiles round-robin): for tile k, sums the
 //     cs x 4 partials of each row in a fixed order (identical in every CTA),
 //     forms the residuals of the two momentum candidates and zeta (one lane
 //     per row), publishes them in the stage's residual slot (rfull[stage]) and
@@ -276,11 +276,16 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
 constexpr int kFsMaxStages = 16;
 constexpr int kFsMaxSlots = 32;
 constexpr int kFsMaxR = 4;
-constexpr int kFsGather = 4;                        // gather warps (tiles round-robin)
-constexpr int kFsGatherWarp = kFzFwdWarps;          // warps 4..4+kFsGather-1
-constexpr int kFsProdWarp = kFzFwdWarps + kFsGather;          // then the producer warp
-constexpr int kFsAccWarp0 = kFsProdWarp + 1;                  // then eight accumulate warps
-constexpr int kFsBlock = (kFsAccWarp0 + kFzTrWarps) * 32;
+// warps: forward 0..3 | gather 4..4+G-1 | producer | eight accumulate warps.
+// G = 4 gather warps for fp64 X (17 warps, 96 registers per thread); fp32 X
+// (1.5x the accumulators per thread) takes 2, so the 15-warp CTA keeps 128
+// registers per thread without spills (3 spill), and 4-row tiles halve the
+// per-tile gather work.
+constexpr int kFsGatherWarp = kFzFwdWarps;
+template <int G> constexpr int fs_prod_warp() { return kFzFwdWarps + G; }
+template <int G> constexpr int fs_acc_warp0() { return kFzFwdWarps + G + 1; }
+template <int G> constexpr int fs_block() { return (kFzFwdWarps + G + 1 + kFzTrWarps) * 32; }
+template <typename TX> constexpr int fs_gather() { return sizeof(TX) == 8 ? 4 : 2; }
 
 struct FsShared {
   uint64_t full[kFsMaxStages];        // stage landed (bulk-copy complete_tx)
@@ -298,7 +303,11 @@ __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~si
 
 // shared memory: FsShared | partial slots [NS][cs][4][R] | stages x (R x W x sizeof(TX))
 template <typename TX, int R, int NV>
-__global__ void __launch_bounds__(kFsBlock, 1) kf_fused_s(EngineArgs a, int mode) {
+__global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
+  constexpr int G = fs_gather<TX>();
+  constexpr int kFsProdWarp = fs_prod_warp<G>();
+  constexpr int kFsAccWarp0 = fs_acc_warp0<G>();
+  constexpr int kFsBlock = fs_block<G>();
   extern __shared__ __align__(128) unsigned char smem[];
   using V = FzVec<TX>;
   constexpr int VE = V::N;
@@ -427,11 +436,11 @@ __global__ void __launch_bounds__(kFsBlock, 1) kf_fused_s(EngineArgs a, int mode
       if (++buf == S) { buf = 0; ph ^= 1u; }
       if (++q == NS) q = 0;
     }
-  } else if (warp < kFsGatherWarp + kFsGather) {
+  } else if (warp < kFsGatherWarp + G) {
     // ===================== gather =====================
     const int gw = warp - kFsGatherWarp;
     const int np = cs * kFzFwdWarps;           // partials per row
-    for (int k = gw; k < mytiles; k += kFsGather) {
+    for (int k = gw; k < mytiles; k += G) {
       const int buf = k % S, q = k % NS;
       const uint32_t ph = (uint32_t)((k / S) & 1), qph = (uint32_t)((k / NS) & 1);
       const int rows = tile_rows(k);
@@ -710,7 +719,7 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3((unsigned)(a.fz_cs * a.fz_ncl));
-  cfg.blockDim = dim3(kFsBlock);
+  cfg.blockDim = dim3(a.dtype == F64 ? fs_block<fs_gather<double>()>() : fs_block<fs_gather<float>()>());
   cfg.dynamicSmemBytes = smem;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.fz_cs;
@@ -723,8 +732,8 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
 
 // Cluster size, rows per tile and ring depth: the smallest cluster (override:
 // L0_FZ_CS) whose column slice fits the accumulate registers, R = 2 rows per
-// tile (L0_FZ_R: 2 or 4; measured on C2: 0.352 vs 0.39 ms with the R = 4
-// register spill), and as many stages as the shared memory holds next to the
+// tile for fp64 X (C2: 0.352 ms; R = 4 spills at 17 warps: 0.39 ms) and 4 for
+// fp32 X (C5: 9.96 vs 12.0 ms, C3: 1.18 vs 1.59 ms; L0_FZ_R overrides), and as many stages as the shared memory holds next to the
 // partial slots (<= kFsMaxStages; slots = 2 x stages, see the slot-reuse
 // argument above; L0_FZ_S caps the stages).
 int fused_plan(EngineArgs& a, int sms) {
@@ -736,7 +745,7 @@ int fused_plan(EngineArgs& a, int sms) {
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
   const char* renv = getenv("L0_FZ_R");
-  const int R = (renv && atoi(renv) == 4) ? 4 : 2;
+  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : (a.dtype == F64 ? 2 : 4);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
