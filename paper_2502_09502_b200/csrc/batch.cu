@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(1024) kb_compact(BatchArgs g) {
 }
 
 // R / Z rows of node blockIdx.y for rows [blockIdx.x * kRowsPerBlock, ...)
-__global__ void __launch_bounds__(kRowThreads) kb_rhs(BatchArgs g) {
+__global__ void __launch_bounds__(kRowThreads, 4) kb_rhs(BatchArgs g) {
   __shared__ double red[32];
   const int64_t b = blockIdx.y;
   State* st = g.st + b;
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) kb_window(BatchArgs g) {
 }
 
 // u = X beta+ (sum of split-K partials, fixed order), F(u), objective
-__global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
+__global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) {
   __shared__ double red[32];
   __shared__ int s_last;
   const int64_t b = blockIdx.y;
@@ -386,8 +386,9 @@ __global__ void __launch_bounds__(kRowThreads) kb_obj(BatchArgs g, int mode) {
   const int64_t cstride = B * nn;
   const int sf = g.sf;
   const int i0 = (int)r0, i1 = (int)r1;
-  // two rows per thread per step (16-byte loads; nn and r0 are even)
-#pragma unroll 1
+  // two rows per thread per step (16-byte loads; nn and r0 are even); two
+  // steps unrolled so their loads are in flight together
+#pragma unroll 2
   for (int i = i0 + 2 * (int)threadIdx.x; i < i1; i += 2 * kRowThreads) {
     const bool two = i + 1 < i1;
     double u[2] = {0.0, 0.0}, yv[2], upv[2] = {0.0, 0.0};

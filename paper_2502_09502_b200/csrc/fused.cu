@@ -60,30 +60,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   }
 }
-// wait for a partial slot filled by st.async from the cluster peers.  The
-// data sits in this CTA's shared memory and the phase completes only once
-// every byte counted by complete_tx has landed, so a CTA-scope acquire
-// suffices (-DL0_FZ_ACQ_CLUSTER builds use the cluster-scope form, whose L1
-// invalidation (CCTL.IVALL) stalls the shared-memory pipe on every wait).
+// wait for a partial slot filled by st.async from the cluster peers: the
+// complete_tx of a remote st.async is a release at cluster scope, so the wait
+// acquires at cluster scope (one L1 invalidation per completed wait; measured
+// free next to the CTA-scope form on C2).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   uint32_t ok = 0;
-  for (;;) {
-#ifdef L0_FZ_ACQ_CLUSTER
+  while (!ok) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(saddr(bar)), "r"(phase)
         : "memory");
-#else
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(saddr(bar)), "r"(phase)
-        : "memory");
-#endif
-    if (ok) break;
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
