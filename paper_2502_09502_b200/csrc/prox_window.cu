@@ -90,19 +90,27 @@ __device__ void select_window(const double* key, int64_t p, unsigned long long u
     const unsigned mask = (1u << w) - 1u;
     for (int i = tid; i < kHistBins; i += kWinThreads) sm.u.hist[i] = 0u;
     __syncthreads();
-    for (int64_t j0 = 0; j0 < p; j0 += kWinThreads) {
-      const int64_t j = j0 + tid;
-      int digit = -1;
-      if (j < p) {
-        const double k = key[j];
+    // U keys per thread in flight per step (the single CTA is latency-bound on L2)
+    constexpr int U = 8;
+    for (int64_t j0 = 0; j0 < p; j0 += (int64_t)U * kWinThreads) {
+      double kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + (int64_t)u * kWinThreads + tid;
+        kv[u] = j < p ? __ldcg(key + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int digit = -1;
+        const double k = kv[u];
         if (k > 0.0) {
           const unsigned long long b = key_bits(k);
           const bool in_prefix = hi_shift >= 64 || (b >> hi_shift) == (prefix >> hi_shift);
           if (b < ub && in_prefix) digit = (int)((b >> shift) & mask);
         }
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sm.u.hist[digit], (unsigned)__popc(peers));
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, digit);
-      if (digit >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sm.u.hist[digit], (unsigned)__popc(peers));
     }
     __syncthreads();
     // bins in descending order: thread t owns bins kHistBins-1-B*t .. kHistBins-B-B*t
@@ -163,8 +171,9 @@ __device__ void compact_window(const double* key, int64_t p, unsigned long long 
   const int64_t j0 = min(p, (int64_t)tid * per), j1 = min(p, j0 + per);
   int cnt = 0;
   double below = 0.0;
+#pragma unroll 8
   for (int64_t j = j0; j < j1; ++j) {
-    const double k = key[j];
+    const double k = __ldcg(key + j);
     if (k > 0.0) {
       const unsigned long long b = key_bits(k);
       if (b >= lb && b < ub) ++cnt;
@@ -173,8 +182,9 @@ __device__ void compact_window(const double* key, int64_t p, unsigned long long 
   }
   int off = 0;
   cub::BlockScan<int, kWinThreads>(sm.u.iscan).ExclusiveSum(cnt, off);
+#pragma unroll 8
   for (int64_t j = j0; j < j1; ++j) {
-    const double k = key[j];
+    const double k = __ldcg(key + j);
     if (k > 0.0) {
       const unsigned long long b = key_bits(k);
       if (b >= lb && b < ub) {
@@ -558,6 +568,7 @@ __device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) 
   if (dirty) {
     // recompute every non-prefix coordinate (K2's speculative outputs cover a
     // smaller prefix than the one sorted here)
+#pragma unroll 4
     for (int64_t j = tid; j < p; j += kWinThreads) {
       const int cls = node ? a.mask[j] : FREE;
       const double gin = a.gam[j];
@@ -590,6 +601,7 @@ __device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) 
   }
   const bool smem_prefix = !dirty;   // fast path: the whole prefix is the smem window
   if (how == 2) {
+#pragma unroll 4
     for (int64_t pos = tid; pos < len; pos += kWinThreads) {
       const int j = smem_prefix ? sm.widx[pos] : a.perm[pos];
       const double x = smem_prefix ? sm.wkey[pos] : a.xs[pos];
