@@ -297,6 +297,68 @@ def run_batched(args):
             "cpu_baseline": cpu}
 
 
+def run_config(name, iters):
+    """One more BASELINE config on one GPU (C1: L2-resident fp64; C3: fp32
+    logistic): K fixed iterations un-instrumented (iterations/s), then again
+    with per-kernel events (the HBM roofline of the dominant pass)."""
+    import torch
+    import paper_2502_09502_b200 as eng
+    from paper_2502_09502_b200 import data
+    t0 = time.time()
+    cd = data.make_config(name, scale=1.0)
+    inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype=cd.dtype)
+    # L: the reference's power iteration stops at 500 iterations without converging
+    # on C3 (SURVEY.md §3.5); 300 power iterations on the GPU, x 1.05
+    Xd = torch.from_numpy(cd.X).cuda().double()
+    v = torch.randn(Xd.shape[1], device="cuda", dtype=torch.float64, generator=torch.Generator("cuda").manual_seed(0))
+    for _ in range(300):
+        w = Xd.T @ (Xd @ v)
+        lam = float(w.norm())
+        v = w / lam
+    del Xd, v, w
+    torch.cuda.empty_cache()
+    L = {"squared_error": 2.0, "logistic": 0.25}[cd.loss] * lam * 1.05
+    gen_s = time.time() - t0
+    o = lambda k, prof: eng.FistaOptions(lipschitz=L, max_iterations=k, gap_tolerance=1e-300,
+                                         stop_on_gap=False, profile=prof)
+    eng.solve_relaxation(inst, opts=o(5, False), return_device=True)
+    eng.solve_relaxation(inst, opts=o(5, True), return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep = eng.solve_relaxation(inst, opts=o(iters, False), return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rep_p = eng.solve_relaxation(inst, opts=o(iters, True), return_device=True)
+    st = rep_p.stats
+    peak, _ = measured_peak()
+    s_el = 8 if cd.dtype == "fp64" else 4
+    n, p = cd.n, cd.p
+    avg = lambda k: st[k + "_ms"] / max(1, st[k + "_count"])
+    xb = n * p * s_el
+    if st.get("single_pass"):
+        kern = {"kf_fused_s": {"launch_ms": avg("k2"), "achieved_gbs": (xb + 8 * (4 * n + p)) / avg("k2") / 1e6},
+                "kr_reduce": {"launch_ms": avg("k1")}, "k3_prox_window": {"launch_ms": avg("k3")}}
+        kern["kf_fused_s"]["frac"] = kern["kf_fused_s"]["achieved_gbs"] / peak
+    else:
+        kern = {"k1_forward": {"launch_ms": avg("k1"), "achieved_gbs": (xb + 8 * (p + 2 * n)) / avg("k1") / 1e6},
+                "k2_transpose": {"launch_ms": avg("k2"), "achieved_gbs": (xb + 8 * (3 * n + 5 * p)) / avg("k2") / 1e6},
+                "k3_prox_window": {"launch_ms": avg("k3")}}
+        for k in ("k1_forward", "k2_transpose"):
+            kern[k]["frac"] = kern[k]["achieved_gbs"] / peak
+    out = {"config": name, "n": n, "p": p, "dtype": cd.dtype, "loss": cd.loss, "k": cd.k, "M": cd.M,
+           "lambda2": cd.lambda2, "lipschitz": L, "iterations": iters,
+           "value": iters / (ms / 1e3), "unit": "iters/s", "ms_per_iteration": ms / iters,
+           "engine_path": "single_pass" if st.get("single_pass") else "two_pass",
+           "x_bytes": xb, "l2_resident": xb < 100e6, "kernels": kern, "peak_gbs": peak,
+           "primal": rep.primal_value, "dual": rep.dual_bound, "restarts": rep.restarts,
+           "setup_s": gen_s}
+    del inst
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # ours
 # ---------------------------------------------------------------------------
@@ -427,6 +489,13 @@ def run_ours(args):
             log(f"[bench] C4 {batched['value']:.0f} node-it/s {batched['ms_per_iteration_split']}")
         except Exception as exc:   # reported, never silently dropped
             batched = {"error": repr(exc)}
+    others = []
+    for name in [c for c in args.configs.split(",") if c and c != "none"]:
+        try:
+            others.append(run_config(name, args.config_steps))
+            log(f"[bench] {name} {others[-1]['value']:.1f} it/s {others[-1]['kernels']}")
+        except Exception as exc:   # reported, never silently dropped
+            others.append({"config": name, "error": repr(exc)})
     line = {"metric": METRIC,
             "value": value, "unit": "iters/s", "n_gpus": 1, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True,
@@ -437,7 +506,7 @@ def run_ours(args):
             "engine_path": "single_pass" if single else "two_pass",
             "restarts": rep.restarts, "final_gap": rep.gap,
             "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks"),
-            "batched_nodes": batched}
+            "batched_nodes": batched, "other_configs": others}
     print(json.dumps(line), flush=True)
 
 
@@ -520,6 +589,8 @@ def main():
     ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--c4-scale", type=float, default=1.0)
+    ap.add_argument("--configs", default="C1,C3", help="extra single-GPU configs reported under other_configs")
+    ap.add_argument("--config-steps", type=int, default=200)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -1,7 +1,7 @@
 # Round profile set: bench line, launch list, ncu --set full of the top kernels.
 # usage (on the GPU box): bash tools/profile_round.sh
 set -x
-B="python bench.py --steps 20 --warmup 3 --no-cpu --e2e-solves 0 --c4-nodes 0"
+B="python bench.py --steps 20 --warmup 3 --no-cpu --e2e-solves 0 --c4-nodes 0 --configs none"
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
 tail -3 gpurun_out/bench.err
 timeout 600 $B > gpurun_out/plain.log 2>&1; echo plain_rc=$?
