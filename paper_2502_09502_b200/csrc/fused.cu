@@ -134,8 +134,9 @@ __device__ __forceinline__ double gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return (double)t;
 }
-// L0_PROBE builds: per-tile timestamps of two CTAs into a.scratch
-//   [cta 0 | cta cs-1][tile][fwd start, fwd end, transpose start, transpose end, -, -]
+// L0_PROBE builds (tools/probe_kfs.py): per-tile globaltimer stamps of CTA 0
+// and CTA cs-1 into a.scratch, [cta][tile][which]: 0 forward start, 1 tile
+// landed, 2 partials sent, 3 gather start, 4 accumulated, 5 refill issued
 #ifdef L0_PROBE
 #define FZ_STAMP(a, slotk, which)                                                           \
   do {                                                                                     \
