@@ -34,6 +34,7 @@ struct Batch {
   int profile = 0;
   std::vector<cudaEvent_t> ev;   // profile: [iter][gemm_t b,e | step+window b,e | gemm_f b,e]
   int64_t graph_kernels = 0;
+  int sf_cap = 1, sct_cap = 1;   // split-K partial capacity carved for the measured choice
 };
 
 static uint64_t batch_carve(Batch& Bt, char* base) {
@@ -54,8 +55,8 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
   g.bl = (float*)take(4ull * B * pp);
   g.rh = (float*)take(4ull * 2 * B * nn);
   g.rl = (float*)take(4ull * 2 * B * nn);
-  g.cf = (float*)take(4ull * g.sf * B * nn);
-  g.ct = (float*)take(4ull * g.sct * 2 * B * pp);
+  g.cf = (float*)take(4ull * Bt.sf_cap * B * nn);
+  g.ct = (float*)take(4ull * Bt.sct_cap * 2 * B * pp);
   g.u = (double*)take(8ull * 3 * B * nn);
   g.st = (State*)take(sizeof(State) * B);
   g.prm = (Params*)take(sizeof(Params) * B);
@@ -183,6 +184,62 @@ struct l0_batch : l0::Batch {};
 
 using namespace l0;
 
+// Split-K of the forward contraction, measured: every split count up to the
+// carved capacity is timed on the real operands (all node rows live; two
+// launches each after a warm-up) and the fastest kept (C4: 8 splits, 0.42 ms,
+// vs the model's 2, 0.50 ms -- the model underrates the wave quantisation of
+// splits x tiles over the SMs).  The transpose keeps the model's choice.
+static cudaError_t tune_one(Batch& Bt, TcGemmArgs& gm, const CUtensorMap& ah, const CUtensorMap& al,
+                            const CUtensorMap& bh, const CUtensorMap& bl, int cap, cudaStream_t s) {
+  if (cap <= 1) return cudaSuccess;
+  cudaEvent_t e0, e1;
+  cudaError_t e = cudaEventCreate(&e0);
+  if (e != cudaSuccess) return e;
+  e = cudaEventCreate(&e1);
+  if (e != cudaSuccess) return e;
+  int best = gm.S;
+  float best_ms = 1e30f;
+  for (int S = 1; S <= cap; ++S) {
+    if (S > 1 && gm.kb_total / S < 4) break;
+    TcGemmArgs g = gm;
+    g.S = S;
+    g.units = S * g.m_tiles * g.n_tiles;
+    const int grid = std::min(g.units, Bt.sms);
+    e = tc_gemm_launch(ah, al, bh, bl, g, grid, s);
+    if (e != cudaSuccess) break;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < 2; ++r) tc_gemm_launch(ah, al, bh, bl, g, grid, s);
+    cudaEventRecord(e1, s);
+    e = cudaEventSynchronize(e1);
+    if (e != cudaSuccess) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (getenv("L0_DEBUG")) fprintf(stderr, "tune M=%lld N=%lld K=%lld S=%d: %.4f ms\n", (long long)g.M,
+                                    (long long)g.N, (long long)g.K, S, ms / 2);
+    if (ms < best_ms * 0.98f) { best_ms = ms; best = S; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  gm.S = best;
+  gm.units = best * gm.m_tiles * gm.n_tiles;
+  return e;
+}
+
+static cudaError_t tune_splits(Batch& Bt, cudaStream_t s) {
+  BatchArgs& g = Bt.g;
+  // every node row live during the timing
+  int h[8] = {0, 0, (int)g.B, (int)g.B, 0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(g.flags, h, sizeof(h), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = tune_one(Bt, Bt.gf, Bt.m_xh, Bt.m_xl, Bt.m_bh, Bt.m_bl, Bt.sf_cap, s);
+  if (e != cudaSuccess) return e;
+  e = tune_one(Bt, Bt.gt, Bt.m_xth, Bt.m_xtl, Bt.m_rh, Bt.m_rl, Bt.sct_cap, s);
+  if (e != cudaSuccess) return e;
+  g.sf = Bt.gf.S;
+  g.sct = Bt.gt.S;
+  return cudaMemsetAsync(g.flags, 0, 4ull * 8, s);
+}
+
 extern "C" {
 
 uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
@@ -289,6 +346,14 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   gt.units = gt.S * gt.m_tiles * gt.n_tiles;
   g.sf = gf.S;
   g.sct = gt.S;
+  // partial capacity for the measured split choice (l0_batch_set_workspace)
+  Bt->sf_cap = std::max(gf.S, std::min(8, std::max(1, gf.kb_total / 8)));
+  // the transpose keeps the model's split: timed alone more splits look
+  // faster (C4: 9 vs 5), but kb_step's re-read of the extra partials costs
+  // more than they save (end to end 1.565 vs 1.510 ms per batched iteration)
+  Bt->sct_cap = gt.S;
+  if (getenv("L0_TC_SF")) Bt->sf_cap = gf.S;
+  if (getenv("L0_TC_ST")) Bt->sct_cap = gt.S;
   Bt->ws_bytes = batch_carve(*Bt, nullptr);
   cudaError_t e = cudaStreamCreateWithFlags(&Bt->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&Bt->ev_in, cudaEventDisableTiming);
@@ -354,6 +419,7 @@ int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
   gt.c_split = 2 * g.B * g.pp;
   gt.C = g.ct;
   gt.n_active = g.flags + 2;
+  L0_B_TRY(tune_splits(*Bt, s));
   L0_B_TRY(cudaStreamSynchronize(s));
   return L0_OK;
 }
