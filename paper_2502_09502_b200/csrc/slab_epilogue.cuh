@@ -29,7 +29,7 @@ struct EpiSmem {
     typename cub::BlockScan<int, kK2Slab>::TempStorage scan;
     typename cub::BlockRadixSort<double, kK2Slab, 1>::TempStorage sort;
   } u;
-  double red[32];
+  double red[96];
 };
 
 // how the free coordinates are treated (prox.py:104-112): 0 pass-through,
@@ -84,9 +84,8 @@ __device__ void slab_epilogue(const EngineArgs& a, int slab, int64_t t, double c
       a.cand_key[(int64_t)slab * kK2Slab + pos] = key;
       a.cand_idx[(int64_t)slab * kK2Slab + pos] = (int)j;
     }
-    const double s = block_sum(ab, sm.red);
-    const double m = block_max(ab, sm.red);
-    const double bl = block_max(below, sm.red);
+    double s = ab, m = ab, bl = below;
+    block_sum_max_max(s, m, bl, sm.red);
     if (tid == 0) {
       a.slab_cnt[slab] = count;
       a.slab_sum[slab] = s;
