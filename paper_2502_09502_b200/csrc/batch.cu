@@ -127,6 +127,7 @@ __global__ void kb_state_init(BatchArgs g, const double* g0) {
   st->loss_cur = 0.0;
   st->theta = 0.0;
   st->slow_prox = 0;
+  st->win_ext = 0;
 }
 
 // Contraction rows for this iteration: the unfinished nodes, compacted in

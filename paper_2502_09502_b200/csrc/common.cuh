@@ -263,7 +263,7 @@ struct State {
   int stop_term;          // termination applied after the pending check (-1: none)
   int last_restarted;
   int topk_fallbacks;     // diagnostics: g top-k window verification misses
-  int pad_;
+  int win_ext;            // diagnostics: K3 iterations whose pool reached past the candidate window
   double obj;             // composite objective at beta_t
   double g_next;          // g(beta_next) from the prox kernel
   double best_dual;

@@ -77,6 +77,7 @@ struct Graph {
   cudaGraphExec_t exec = nullptr;
   int G = 0;
   int profile = 0;
+  int full_sort = 0;   // K3 variant captured (EngineArgs::prox_full_sort)
   int64_t kernels = 0;
   std::vector<cudaEvent_t> ev;  // profile: [iter][k2b,k2e,k3b,k3e,k1b,k1e]
 };
@@ -134,6 +135,7 @@ static int compute_layout(Problem& P) {
   a.k2_rows = ceil_div(n, chunks);
   a.k2_chunks = (int)ceil_div(n, a.k2_rows);
   a.k2_grid = (int)std::min<int64_t>(k2_res, k2_groups * a.k2_chunks);
+  a.prox_full_sort = getenv("L0_FULL_SORT") ? atoi(getenv("L0_FULL_SORT")) : 0;
   a.fused = fused_plan(a, sms) ? 1 : 0;
   P.fused_planned = a.fused;
   if (!a.fused) { a.fz_ncl = 1; a.fz_cs = 1; }
@@ -265,7 +267,7 @@ static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
 
 static int build_graph(Problem& P, int which, int G, int profile) {
   Graph& g = P.graph[which];
-  if (g.exec && g.G == G && g.profile == profile) return ST_OK;
+  if (g.exec && g.G == G && g.profile == profile && g.full_sort == P.a.prox_full_sort) return ST_OK;
   if (g.exec) {
     cudaGraphExecDestroy(g.exec);
     for (auto e : g.ev) cudaEventDestroy(e);
@@ -306,6 +308,7 @@ static int build_graph(Problem& P, int which, int G, int profile) {
   if (e != cudaSuccess) return set_error(ST_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
   g.G = G;
   g.profile = profile;
+  g.full_sort = P.a.prox_full_sort;
   g.kernels = kernels;
   return ST_OK;
 }
@@ -578,6 +581,13 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     return set_error(ST_UNSUPPORTED, "the single-pass kernel does not fit this problem");
   if (want_fused != a.fused) destroy_graphs(*P);
   a.fused = want_fused;
+  // K3 variant: the windowed top-of-order sort, switched to the full key sort
+  // for the rest of the solve once most iterations of a chunk needed window
+  // extensions (a PAVA pool spanning much of p, as on C3: K3 0.34 -> 0.19 ms);
+  // L0_FULL_SORT=0/1 pins either variant
+  const char* full_env = getenv("L0_FULL_SORT");
+  a.prox_full_sort = full_env ? atoi(full_env) : 0;
+  const bool auto_full = full_env == nullptr;
   // the captured graphs always see the node buffers; Params::node_mode gates their use
   a.mask = P->d_mask;
   a.fone = P->d_fone;
@@ -639,7 +649,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   int64_t chunks = 0;
   bool aborted = false, stop_sent = false;
   int64_t t_before[2] = {0, 0};
-  int64_t t_prev = 0;
+  int64_t t_prev = 0, ext_prev = 0;
   State* last = nullptr;
   int inflight = 0;
   int next = 0;
@@ -660,6 +670,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     L0_CUDA_TRY(cudaEventSynchronize(P->ev_chunk[w]));
     --inflight;
     ++chunks;
+    launches += P->graph[w].kernels;
     State* h = P->h_st[w];
     last = h;
     // profile: accumulate the kernel times of the iterations this chunk executed
@@ -673,6 +684,12 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
         if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 4], g.ev[i * 6 + 5]) == cudaSuccess) { rep->k1_ms += ms; rep->k1_count++; }
       }
     }
+    // window extensions in this chunk -> full key sort from the next launch on
+    const int64_t did_chunk = h->t - t_prev;
+    const int64_t ext_now = (int64_t)h->win_ext + h->slow_prox;
+    if (auto_full && !a.prox_full_sort && did_chunk >= 4 && 2 * (ext_now - ext_prev) >= did_chunk)
+      a.prox_full_sort = 1;
+    ext_prev = ext_now;
     t_prev = h->t;
     (void)t_before;
     // trace records, in order (fista.py:185-194)
@@ -692,6 +709,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
         L0_CUDA_TRY(cudaEventSynchronize(P->ev_chunk[next]));
         --inflight;
         ++chunks;
+        launches += P->graph[next].kernels;
         if (P->h_st[next]->t >= h->t) last = P->h_st[next];
       }
       break;
@@ -708,11 +726,14 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
       }
       stop_sent = true;
     }
+    if (P->graph[w].full_sort != a.prox_full_sort) {
+      rc = build_graph(*P, w, G, o->profile ? 1 : 0);
+      if (rc) return rc;
+    }
     rc = launch_chunk(w);
     if (rc) return rc;
     ++inflight;
   }
-  launches += chunks * P->graph[0].kernels;
   const State* h = last;
   if (aborted) {
     L0_CUDA_TRY(cudaStreamSynchronize(s));

@@ -248,6 +248,7 @@ __global__ void k_state_init(State* st, double parent_bound) {
   st->loss_cur = 0.0;
   st->theta = 0.0;
   st->slow_prox = 0;
+  st->win_ext = 0;
 }
 
 // host-requested stop (time limit, trace-hook abort): fista.py:204-206

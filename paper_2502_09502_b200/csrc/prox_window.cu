@@ -519,7 +519,10 @@ __device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) 
       ub = key_bits(theta);
       window_search(sm.wkey, sm.wtail, len, kk, rho, M, nf > len, below, sm);
       L0_STAMP(st, 5);
-      if (sm.res == 3) dirty = true;   // pool reaches below theta: extend windows
+      if (sm.res == 3) {                 // pool reaches below theta: extend windows
+        dirty = true;
+        if (tid == 0) st->win_ext += 1;
+      }
     } else {
       dirty = true;
       if (tid == 0) st->slow_prox += 1;

@@ -348,3 +348,34 @@ def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
     for x, y_ in zip(ra, rb):
         assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
     np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
+
+
+@pytest.mark.gpu
+def test_k3_variants_agree(engine, monkeypatch):
+    """The windowed K3 (pinned, L0_FULL_SORT=0), the full key sort (pinned, =1)
+    and the automatic switch (unset: window first, full sort once a chunk's
+    pools keep reaching past the window) run the same exact prox: identical
+    trajectories on a C3-like problem whose PAVA pool spans most of p."""
+    cd = mydata.make_config("C3", scale=1 / 10)
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype="fp32")
+    L = 0.25 * 1.01 * float(np.linalg.norm(cd.X.astype(np.float64), 2) ** 2)
+    res = {}
+    for mode in ("0", "1", None):
+        if mode is None:
+            monkeypatch.delenv("L0_FULL_SORT", raising=False)
+        else:
+            monkeypatch.setenv("L0_FULL_SORT", mode)
+        rec = []
+        res[mode] = (engine.solve_relaxation(inst, opts=engine.FistaOptions(
+            lipschitz=L, max_iterations=60, gap_tolerance=1e-300, chunk_iterations=4,
+            trace_hook=rec.append)), rec)
+    a, ra = res["0"]
+    for mode in ("1", None):
+        b, rb = res[mode]
+        assert b.iterations == a.iterations == 60
+        assert b.restarts == a.restarts
+        assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
+        assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9)
+        for x, y_ in zip(ra, rb):
+            assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
+        np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
