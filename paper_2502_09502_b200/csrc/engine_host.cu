@@ -122,7 +122,8 @@ static int compute_layout(Problem& P) {
   a.k1_slabs = (int)ceil_div(p, kK1Slab);
   int64_t k1_res = (int64_t)sms * k1_blocks_per_sm(a.dtype);
   int64_t chunks = std::max<int64_t>(1, ceil_div(k1_res * 8, a.k1_slabs));
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, 8)));
+  const int64_t k1_min_rows = getenv("L0_K1_ROWS") ? atoi(getenv("L0_K1_ROWS")) : 8;
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, k1_min_rows)));
   a.k1_rows = ceil_div(n, chunks);
   a.k1_chunks = (int)ceil_div(n, a.k1_rows);
   a.k1_grid = (int)std::min<int64_t>(k1_res, (int64_t)a.k1_slabs * a.k1_chunks);
@@ -131,7 +132,11 @@ static int compute_layout(Problem& P) {
   const int64_t k2_groups = ceil_div(a.k2_slabs, a.dtype == F32 ? kK2Cw<float> : kK2Cw<double>);
   int64_t k2_res = (int64_t)sms * k2_blocks_per_sm(a.dtype);
   chunks = std::max<int64_t>(1, ceil_div(k2_res * 8, k2_groups));
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, 16)));
+  // >= 64 rows per K2 item: on small X the cross-chunk reduction of the last
+  // CTA per slab dominates (C1: 23.6 -> 17.2 us per K2); large X never hits
+  // the cap.  L0_K2_ROWS / L0_K1_ROWS override.
+  const int64_t k2_min_rows = getenv("L0_K2_ROWS") ? atoi(getenv("L0_K2_ROWS")) : 64;
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, ceil_div(n, k2_min_rows)));
   a.k2_rows = ceil_div(n, chunks);
   a.k2_chunks = (int)ceil_div(n, a.k2_rows);
   a.k2_grid = (int)std::min<int64_t>(k2_res, k2_groups * a.k2_chunks);
