@@ -178,6 +178,32 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return r;
 }
 
+// block_sum of four values in one pass (same trees and arithmetic as four
+// block_sum calls); `scratch` needs 4 x 32 doubles.
+__device__ __forceinline__ void block_sum4(double (&v)[4], double* scratch) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) scratch[32 * i + w] = v[i];
+  __syncthreads();
+  if (w == 0) {
+    double x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = warp_sum(lane < nw ? scratch[32 * i + lane] : 0.0);
+    __syncwarp();
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) scratch[32 * i] = x[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = scratch[32 * i];
+  __syncthreads();
+}
+
 // block_sum(s), block_max(m1), block_max(m2) in one pass: the same trees and
 // the same arithmetic as the three calls, three barriers instead of twelve.
 // `scratch` needs 3 x 32 doubles.

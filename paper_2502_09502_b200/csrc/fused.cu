@@ -183,10 +183,9 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
   if (bad) *sbad = 1;
   if (gbad_R) atomicOr(sbad, 2);
   if (gbad_N) atomicOr(sbad, 4);
-  const double lsum = block_sum(loss_acc, sred);
-  const double f0 = block_sum(f_acc[0], sred);
-  const double f1 = block_sum(f_acc[1], sred);
-  const double f2 = block_sum(f_acc[2], sred);
+  double sums[4] = {loss_acc, f_acc[0], f_acc[1], f_acc[2]};
+  block_sum4(sums, sred);
+  const double lsum = sums[0], f0 = sums[1], f1 = sums[2], f2 = sums[3];
   if (crank == 0 && tid == 0) {
     double* cp = a.fz_cpart + 8 * (int64_t)cid;
     cp[0] = lsum;
@@ -285,7 +284,7 @@ struct FsShared {
   double sy[kFsMaxStages][kFsMaxR];   // y / u_{t-1} of the stage's rows (bulk copies)
   double su[kFsMaxStages][kFsMaxR];
   double rr[kFsMaxStages][3][kFsMaxR];   // r_R, r_N, zeta of the stage's rows
-  double red[32];
+  double red[128];
   int bad;
 };
 
