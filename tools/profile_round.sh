@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kr_
 timeout 600 $B --engine two_pass > gpurun_out/plain2.log 2>&1; echo plain2_rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_forward|k2_transpose" -s 30 -c 2 -o gpurun_out/prof_2p $B --engine two_pass > gpurun_out/ncu_2p.log 2>&1; echo 2p_rc=$?
 timeout 600 python tools/bench_c4.py 1.0 512 10 > gpurun_out/c4_plain.log 2>&1; echo c4_rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm|kb_window|kb_step|kb_obj|kb_rhs" -s 12 -c 5 -o gpurun_out/prof_tc python tools/bench_c4.py 1.0 512 10 > gpurun_out/ncu_tc.log 2>&1; echo tc_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm|kb_window|kb_step|kb_obj|kb_rhs" -s 66 -c 6 -o gpurun_out/prof_tc python tools/bench_c4.py 1.0 512 10 > gpurun_out/ncu_tc.log 2>&1; echo tc_rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c4_launches.csv python tools/bench_c4.py 1.0 512 10 > gpurun_out/c4_ncu.log 2>&1; echo c4l_rc=$?
 python tools/ncu_summary.py gpurun_out/ncu_summary.json gpurun_out/prof_kf.ncu-rep gpurun_out/prof_k3.ncu-rep gpurun_out/prof_kr.ncu-rep gpurun_out/prof_2p.ncu-rep gpurun_out/prof_tc.ncu-rep; echo summary_rc=$?
 for r in kf k3 kr 2p tc; do ncu -i gpurun_out/prof_$r.ncu-rep --page details --csv > gpurun_out/details_$r.csv 2>/dev/null; done
