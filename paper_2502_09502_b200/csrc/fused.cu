@@ -365,6 +365,25 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
   __syncthreads();
   if (tid == 0)
     for (int k = 0; k < NS && k < mytiles; ++k) mbar_arrive_expect(&sh.xb[k], slot_bytes(k));
+  auto issue = [&](int k, int b) {
+    const int64_t tile = tile_of(k);
+    const int rows = tile_rows(k);
+    TX* dst = tiles + (int64_t)b * R * W;
+    const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
+    mbar_arrive_expect(&sh.full[b], row_bytes * rows + sb);
+    if (row_bytes > 0)
+      for (int r = 0; r < rows; ++r)
+        bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
+                 row_bytes, &sh.full[b]);
+    if (sb) {
+      bulk_g2s(&sh.sy[b][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
+      if (mode == MODE_ITER) bulk_g2s(&sh.su[b][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
+    }
+  };
+  // the first S tiles only need this CTA's barriers: in flight across the
+  // cluster barrier (which orders the peers' barrier init before any st.async)
+  if (warp == kFsProdWarp && lane == 0)
+    for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
   if (cs > 1) cluster_barrier();
   else __syncthreads();
 
@@ -497,22 +516,6 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
   } else if (warp == kFsProdWarp) {
     // ===================== producer =====================
     if (lane == 0) {
-      auto issue = [&](int k, int b) {
-        const int64_t tile = tile_of(k);
-        const int rows = tile_rows(k);
-        TX* dst = tiles + (int64_t)b * R * W;
-        const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
-        mbar_arrive_expect(&sh.full[b], row_bytes * rows + sb);
-        if (row_bytes > 0)
-          for (int r = 0; r < rows; ++r)
-            bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
-                     row_bytes, &sh.full[b]);
-        if (sb) {
-          bulk_g2s(&sh.sy[b][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
-          if (mode == MODE_ITER) bulk_g2s(&sh.su[b][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
-        }
-      };
-      for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
       int buf = 0;
       uint32_t ph = 0;
       for (int k = 0; k + S < mytiles; ++k) {
