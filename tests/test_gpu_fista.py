@@ -314,6 +314,7 @@ def test_single_pass_engine_matches_two_pass(engine, case):
     (301, 20000, "fp64", "squared_error"),    # 16-CTA (non-portable) clusters, 3 vectors per thread
     (999, 5003, "fp32", "logistic"),          # fp32 X, odd n, partial last tile
     (2048, 9000, "fp64", "logistic"),         # 8-CTA clusters, last CTA's slice partly past p
+    (1500, 4100, "fp64", "squared_hinge"),    # the third solver-grade loss through the gather warps
 ])
 def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
     """kf_fused_s on ragged shapes (odd rows, partial last tile, slices past p,
@@ -325,7 +326,7 @@ def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
     beta_true = np.zeros(p)
     beta_true[:: max(1, p // 5)] = 1.0
     u = X.astype(np.float64) @ beta_true
-    if loss == "logistic":
+    if loss in ("logistic", "squared_hinge"):
         y = np.where(rng.random(n) < 1.0 / (1.0 + np.exp(-u)), 1.0, -1.0)
     else:
         y = u + rng.standard_normal(n)
@@ -341,7 +342,7 @@ def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
             trace_hook=rec.append)), rec)
     (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
     assert b.stats["single_pass"] and not a.stats["single_pass"]
-    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 2, 9000: 8}[p]
+    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 2, 9000: 8, 4100: 4}[p]
     assert a.iterations == b.iterations == 30
     assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
     assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9, abs=1e-12)
