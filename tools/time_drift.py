@@ -1,5 +1,6 @@
 """C2 iteration time over back-to-back 400-iteration solves with nvidia-smi clocks,
 temperatures and power after each (run-to-run drift under sustained load)."""
+import sys, time
 sys.path.insert(0, ".")
 import torch, subprocess
 import paper_2502_09502_b200 as eng
