@@ -380,3 +380,42 @@ def test_k3_variants_agree(engine, monkeypatch):
         for x, y_ in zip(ra, rb):
             assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
         np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stop", ["converged", "primal_cutoff", "dual_cutoff", "iteration_limit_check"])
+def test_single_pass_stopping_rules(engine, stop):
+    """Termination paths of the single-pass engine (K3 bound checks, the
+    objective's cutoffs, the final bound pass) against the two-pass engine."""
+    cd = mydata.make_config("C2", scale=1 / 8)
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+    L = 2.0 * 1.01 * float(np.linalg.norm(cd.X, 2) ** 2)
+    base = engine.solve_relaxation(inst, opts=engine.FistaOptions(lipschitz=L, max_iterations=60,
+                                                                  gap_tolerance=1e-300))
+    kw = {"lipschitz": L}
+    if stop == "converged":
+        kw.update(max_iterations=5000, gap_tolerance=1e-4 * abs(base.primal_value))
+    elif stop == "primal_cutoff":
+        kw.update(max_iterations=5000, early_primal_cutoff=base.primal_value * (1 + 1e-3))
+    elif stop == "dual_cutoff":
+        kw.update(max_iterations=5000, early_dual_cutoff=base.dual_bound * (1 - 1e-3))
+    else:
+        kw.update(max_iterations=37, gap_tolerance=1e-300)   # stops between bound checks
+    res = {}
+    for path in ("two_pass", "single_pass"):
+        rec = []
+        res[path] = (engine.solve_relaxation(inst, opts=engine.FistaOptions(
+            engine_path=path, trace_hook=rec.append, **kw)), rec)
+    (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
+    assert b.stats["single_pass"] and not a.stats["single_pass"]
+    assert b.termination == a.termination
+    assert a.termination.value == {"converged": "converged", "primal_cutoff": "primal_below_incumbent",
+                                   "dual_cutoff": "dual_above_incumbent",
+                                   "iteration_limit_check": "iteration_limit"}[stop]
+    assert b.iterations == a.iterations
+    assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
+    assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9)
+    assert len(ra) == len(rb)
+    for x, y_ in zip(ra, rb):
+        assert y_["iteration"] == x["iteration"]
+        assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
