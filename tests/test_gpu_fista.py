@@ -383,7 +383,8 @@ def test_k3_variants_agree(engine, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("stop", ["converged", "primal_cutoff", "dual_cutoff", "iteration_limit_check"])
+@pytest.mark.parametrize("stop", ["converged", "primal_cutoff", "dual_cutoff", "iteration_limit_check",
+                                  "warm_node"])
 def test_single_pass_stopping_rules(engine, stop):
     """Termination paths of the single-pass engine (K3 bound checks, the
     objective's cutoffs, the final bound pass) against the two-pass engine."""
@@ -399,19 +400,28 @@ def test_single_pass_stopping_rules(engine, stop):
         kw.update(max_iterations=5000, early_primal_cutoff=base.primal_value * (1 + 1e-3))
     elif stop == "dual_cutoff":
         kw.update(max_iterations=5000, early_dual_cutoff=base.dual_bound * (1 - 1e-3))
+    elif stop == "warm_node":
+        kw.update(max_iterations=5000, gap_tolerance=1e-4 * abs(base.primal_value))
     else:
         kw.update(max_iterations=37, gap_tolerance=1e-300)   # stops between bound checks
+    node, warm = None, None
+    if stop == "warm_node":   # a branch-and-bound child warm-started from its parent's iterate
+        order = np.argsort(-np.abs(base.beta))
+        node = engine.NodeState(fixed_one=(int(order[0]),), fixed_zero=(int(order[1]), int(order[-1])),
+                                parent_bound=base.dual_bound)
+        warm = base.beta.copy()
+        warm[[int(order[1]), int(order[-1])]] = 0.0
     res = {}
     for path in ("two_pass", "single_pass"):
         rec = []
-        res[path] = (engine.solve_relaxation(inst, opts=engine.FistaOptions(
+        res[path] = (engine.solve_relaxation(inst, node=node, warm_start=warm, opts=engine.FistaOptions(
             engine_path=path, trace_hook=rec.append, **kw)), rec)
     (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
     assert b.stats["single_pass"] and not a.stats["single_pass"]
     assert b.termination == a.termination
     assert a.termination.value == {"converged": "converged", "primal_cutoff": "primal_below_incumbent",
                                    "dual_cutoff": "dual_above_incumbent",
-                                   "iteration_limit_check": "iteration_limit"}[stop]
+                                   "iteration_limit_check": "iteration_limit", "warm_node": "converged"}[stop]
     assert b.iterations == a.iterations
     assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
     assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9)
