@@ -429,3 +429,23 @@ def test_single_pass_stopping_rules(engine, stop):
     for x, y_ in zip(ra, rb):
         assert y_["iteration"] == x["iteration"]
         assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_single_pass_time_limit(engine, dtype):
+    """The host-side time limit on the single-pass engine: the solve stops
+    between graph replays with TIME_LIMIT and a finite bound from the final
+    bound pass at the last iterate (fista.py:204-209), weakly dual."""
+    cd = mydata.make_config("C2", scale=1 / 8)
+    X = cd.X.astype(np.float32) if dtype == "fp32" else cd.X
+    inst = engine.ProblemInstance(X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2, dtype=dtype)
+    L = 2.0 * 1.01 * float(np.linalg.norm(X.astype(np.float64), 2) ** 2)
+    rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
+        lipschitz=L, max_iterations=10 ** 7, gap_tolerance=1e-300, time_limit=0.05,
+        engine_path="single_pass"))
+    assert rep.stats["single_pass"]
+    assert rep.termination.value == "time_limit"
+    assert 0 < rep.iterations < 10 ** 7
+    assert np.isfinite(rep.dual_bound) and np.isfinite(rep.primal_value)
+    assert rep.dual_bound <= rep.primal_value * (1 + 1e-12)
