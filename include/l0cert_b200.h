@@ -49,7 +49,11 @@ enum l0_status {
   L0_CUDA = 5,         /* CUDA runtime failure                          */
   L0_ABORTED = 6       /* the trace callback asked to stop              */
 };
-enum l0_loss { L0_SQUARED_ERROR = 0, L0_LOGISTIC = 1, L0_SQUARED_HINGE = 2 };
+/* solver-grade losses 0..2; Poisson and gamma (model.py:174-177) are bound-grade:
+ * l0_loss_value / l0_loss_conjugate / l0_safe_lower_bound accept them, the
+ * solver rejects them with L0_UNSUPPORTED (no global Lipschitz constant) */
+enum l0_loss { L0_SQUARED_ERROR = 0, L0_LOGISTIC = 1, L0_SQUARED_HINGE = 2, L0_POISSON = 3,
+               L0_GAMMA = 4 };
 enum l0_dtype { L0_F64 = 0, L0_F32 = 1 };
 enum l0_termination {
   L0_CONVERGED = 0, L0_ITERATION_LIMIT = 1, L0_TIME_LIMIT = 2,
@@ -69,7 +73,7 @@ typedef struct l0_fista_opts {
   double early_dual_cutoff;     /* fista.py:49, NaN = None */
   int32_t bound_check_interval; /* fista.py:50 */
   int32_t restart;              /* fista.py:51 */
-  double lipschitz;             /* fista.py:52; must be > 0 (L = max(L, 1e-12) applied) */
+  double lipschitz;             /* fista.py:52; L = max(L, 1e-12) is applied (fista.py:101); NaN rejected */
   /* extensions */
   double gap_tolerance_rel;     /* also stop when gap <= rel * |primal| (0: off) */
   int32_t stop_on_gap;          /* 0: fixed-iteration mode (no gap stop) */
@@ -137,6 +141,16 @@ int32_t l0_nccl_unique_id(void* h_out128);
 
 /* diagnostics: clock64 phase stamps of the last prox kernel (L0_PROBE builds) */
 int32_t l0_debug_probe(l0_problem* prob, int64_t* h_out16);
+/* verification: record, for every iteration of later l0_fista_solve calls, the
+ * prox's decisions into a device ring of cap records of (8 + width) int32:
+ * [iteration, case (0 copy / 1 elementwise / 2 sort+PAVA), pool found,
+ *  a*, c* (sorted positions of the merged PAVA pool), sorted prefix length,
+ *  path (0 window, 1 window extended, 2 full key sort), free count]
+ * then the first `width` coordinate ids of the stable descending order of
+ * |rho gamma| over the free coordinates (-1 past the prefix).  Record of
+ * iteration t sits at slot t % cap.  prox.py:111 (argsort) and :46-98 (pool).
+ * d_ring = NULL turns recording off. */
+int32_t l0_problem_set_prox_record(l0_problem* prob, int32_t* d_ring, int32_t cap, int32_t width);
 /* diagnostics: copy the engine's p-length scratch vector (per-tile timestamps of
  * the single-pass kernel in L0_PROBE builds) */
 int32_t l0_debug_scratch(l0_problem* prob, double* h_out, int64_t count);

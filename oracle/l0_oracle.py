@@ -550,14 +550,18 @@ def fista(X, y, kind: str, k: int, M: float, lam2: float, L: Optional[float] = N
           bci: int = 10, restart: bool = True,
           trace: Optional[Callable[[dict], None]] = None,
           stop_on_gap: bool = True,
-          on_iteration: Optional[Callable[[int, np.ndarray, float, bool], None]] = None) -> dict:
+          on_iteration: Optional[Callable[[int, np.ndarray, float, bool], None]] = None,
+          on_prox: Optional[Callable[[int, np.ndarray, Optional[tuple]], None]] = None) -> dict:
     """Restarted FISTA on the perspective relaxation — fista.py:76-222.
 
     Same operation order as the reference (three X passes per iteration, the
     dual at t == 1 and every ``bci``).  ``stop_on_gap=False`` is the engine's
     fixed-iteration extension (the reference has no such switch; with it left
     True the behaviour is the reference's).  ``on_iteration(t, beta, obj,
-    restarted)`` is a test hook that sees every iterate.
+    restarted)`` is a test hook that sees every iterate; ``on_prox(t, order,
+    pool, sorted_keys)`` sees the prox's stable descending order (coordinate ids of the free
+    coordinates, prox.py:111) and merged PAVA pool (a*, c*) or None
+    (prox.py:46-98) at every iteration.
     """
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
@@ -571,9 +575,23 @@ def fista(X, y, kind: str, k: int, M: float, lam2: float, L: Optional[float] = N
     L = max(L, 1e-12)
     rho = L / two
 
+    cur_t = [0]
+
+    def _conj(mu_free, kk, ids=None):
+        if on_prox is None:
+            return prox_conj(mu_free, rho, kk, M)
+        res, order, pool = prox_conj(mu_free, rho, kk, M, instrument=True)
+        keys = None
+        if order is not None:
+            keys = np.abs(mu_free)[order]
+            if ids is not None:
+                order = ids[order]
+        on_prox(cur_t[0], order, pool, keys)
+        return res
+
     if not restricted:
         def step(gam):
-            return gam - prox_conj(rho * gam, rho, k, M) / rho
+            return gam - _conj(rho * gam, k, np.arange(p)) / rho
     else:
         free = free_indices(p, fixed_one, fixed_zero)
         fone = np.asarray(fixed_one, dtype=np.int64)
@@ -590,7 +608,7 @@ def fista(X, y, kind: str, k: int, M: float, lam2: float, L: Optional[float] = N
                 part = mu[fone]
                 shrunk[fone] = np.sign(part) * hprox(np.abs(part), rho, M)
             if free.size:
-                shrunk[free] = prox_conj(mu[free], rho, k_rem, M)
+                shrunk[free] = _conj(mu[free], k_rem, free)
             res = gam - shrunk / rho
             res[zero_mask] = 0.0
             return res
@@ -607,6 +625,7 @@ def fista(X, y, kind: str, k: int, M: float, lam2: float, L: Optional[float] = N
     it = 0
     for t in range(1, max_iter + 1):
         it = t
+        cur_t[0] = t
         gam = beta + (phi / (phi + 3.0)) * (beta - beta_prev)
         grad = X.T @ loss_grad(kind, X @ gam, y)
         gam -= grad / L

@@ -135,13 +135,16 @@ def _refit(instance: ProblemInstance, supports: Sequence[Tuple[int, ...]], iters
         todo = (b.abs() > M).any(dim=1)
         b = torch.clamp(b, -M, M)
     if bool(todo.any()):
+        # accelerated projected gradient (FISTA on the box) from the current point
         bt = b[todo]
+        bp = bt.clone()
         Xt, Lt, mt = Xs[todo], L[todo], mask[todo]
-        for _ in range(iters):
-            u = torch.einsum("csn,cs->cn", Xt, bt)
+        for it in range(iters):
+            z = bt + ((it - 1.0) / (it + 2.0) if it > 0 else 0.0) * (bt - bp)
+            u = torch.einsum("csn,cs->cn", Xt, z)
             _, g = _loss_and_grad(instance.loss, u, y)
-            grad = torch.einsum("csn,cn->cs", Xt, g) + 2.0 * lam2 * bt
-            bt = torch.clamp(bt - grad / Lt[:, None], -M, M) * mt
+            grad = torch.einsum("csn,cn->cs", Xt, g) + 2.0 * lam2 * z
+            bp, bt = bt, torch.clamp(z - grad / Lt[:, None], -M, M) * mt
         b[todo] = bt
     u = torch.einsum("csn,cs->cn", Xs, b)
     f, _ = _loss_and_grad(instance.loss, u, y)
@@ -256,8 +259,13 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
     def pruned(bound):
         return bound >= inc_obj - (opts.prune_abs + opts.prune_rel * abs(inc_obj))
 
+    # bounds of nodes closed without being pruned (a leaf whose convex solve
+    # did not reach the incumbent, a node with nothing left to branch on):
+    # they stay in the global bound so the certificate remains sound
+    unresolved: List[float] = []
+
     def glb():
-        return min([inc_obj] + [b for b, _, _, _ in heap])
+        return min([inc_obj] + [b for b, _, _, _ in heap] + unresolved)
 
     while heap:
         if time.perf_counter() - t0 > opts.time_limit:
@@ -280,14 +288,18 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
                 # every free coordinate must stay zero: the node is the convex
                 # problem on its fixed-one support (the relaxation solver's prox
                 # leaves ulp residues there that its envelope rejects, as the
-                # reference's does) -> refit + safe bound, no branching
+                # reference's does) -> refit until its safe bound closes the
+                # node; a node that stays open keeps its bound in glb()
                 explored += 1
-                b, o = _refit(instance, [tuple(node.fixed_one)], opts.refit_iterations)
-                if float(o[0]) < inc_obj:
-                    inc_beta, inc_obj = b[0], float(o[0])
-                lb_leaf = max(bound, safe_lower_bound(instance, b[0], node))
+                b, o, lb_leaf = _solve_leaf(instance, node, bound, opts, inc_obj)
+                if o < inc_obj:
+                    inc_beta, inc_obj = b, o
+                closed = pruned(lb_leaf)
+                if not closed:
+                    unresolved.append(lb_leaf)
                 log.append({"depth": node.depth, "fixed_one": node.fixed_one,
-                            "fixed_zero": node.fixed_zero, "bound": lb_leaf, "decision": "leaf"})
+                            "fixed_zero": node.fixed_zero, "bound": lb_leaf,
+                            "decision": "leaf" if closed else "leaf (open)"})
                 continue
             batch.append((bound, node))
         if not batch:
@@ -326,7 +338,17 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
                 inc_beta, inc_obj = b_node, o_node
             j = select_branching_variable(instance, node, b_node)
             if j is None:
-                entry["decision"] = "complete"
+                # the node's feasible point uses only fixed coordinates: branch
+                # on the relaxation's largest free coordinate instead
+                j = _relaxation_branch(instance, node, rep.beta)
+            if j is None:
+                # nothing free is active: closed only if its bound prunes it
+                # against the (possibly just improved) incumbent
+                if pruned(bound):
+                    entry["decision"] = "complete"
+                else:
+                    unresolved.append(bound)
+                    entry["decision"] = "complete (open)"
                 log.append(entry)
                 continue
             entry["decision"] = f"branch {j}"
@@ -341,7 +363,8 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
             w0[j] = 0.0
             push(bound, NodeState(fixed_one=node.fixed_one, fixed_zero=node.fixed_zero + (j,),
                                   depth=node.depth + 1, parent_bound=bound, warm_start=w0))
-    lb = glb() if heap else inc_obj
+    unresolved[:] = [b for b in unresolved if not pruned(b)]
+    lb = glb()
     if status is None:
         status = CertificateStatus.OPTIMAL
     gap = max(0.0, inc_obj - lb)
@@ -351,6 +374,39 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
     return Certificate(incumbent_beta=inc_beta, incumbent_objective=inc_obj, global_lower_bound=lb,
                        gap_absolute=gap, gap_relative=rel, nodes_explored=explored,
                        wall_time=time.perf_counter() - t0, status=status, log=log)
+
+
+def _solve_leaf(instance: ProblemInstance, node: NodeState, bound: float, opts: BnBOptions,
+                inc_obj: float):
+    """Leaf node: the convex problem on the fixed-one support.  Squared error
+    refits exactly (ridge); other losses (or a binding box) refit by projected
+    gradient with a growing budget until the fp64 safe bound at the refit is
+    within the pruning tolerance of its objective.  Returns (beta, objective,
+    bound); the bound is sound whether or not the refit converged."""
+    S = tuple(node.fixed_one)
+    iters = max(1, opts.refit_iterations)
+    best_b, best_o, best_lb = None, math.inf, bound
+    for _ in range(6):
+        b, o = _refit(instance, [S], iters)
+        if float(o[0]) < best_o:
+            best_b, best_o = b[0], float(o[0])
+        best_lb = max(best_lb, safe_lower_bound(instance, b[0], node))
+        ub = min(inc_obj, best_o)
+        if best_lb >= ub - (opts.prune_abs + opts.prune_rel * abs(ub)):
+            break
+        iters *= 4
+    return best_b, best_o, best_lb
+
+
+def _relaxation_branch(instance: ProblemInstance, node: NodeState, relax_beta) -> Optional[int]:
+    """The free coordinate with the largest |relaxation beta| (None if all zero)."""
+    beta = np.abs(np.asarray(relax_beta, dtype=np.float64))
+    free = np.ones(instance.p, dtype=bool)
+    free[list(node.fixed_one) + list(node.fixed_zero)] = False
+    beta[~free] = 0.0
+    if len(node.fixed_one) >= int(instance.k) or not np.any(beta > 0.0):
+        return None
+    return int(np.argmax(beta))
 
 
 def _is_leaf(instance: ProblemInstance, node: NodeState) -> bool:

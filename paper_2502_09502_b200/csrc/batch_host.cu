@@ -450,8 +450,8 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   if (!(o->gap_tolerance > 0)) return set_error(L0_INVALID, "gap_tolerance must be positive");
   if (o->bound_check_interval < 1) return set_error(L0_INVALID, "bound_check_interval must be >= 1");
   if (o->max_iterations < 1) return set_error(L0_INVALID, "max_iterations must be >= 1");
-  if (!(o->lipschitz > 0) || std::isnan(o->lipschitz))
-    return set_error(L0_INVALID, "lipschitz constant must be provided and positive");
+  if (std::isnan(o->lipschitz))   // fista.py:101: any other L is clamped to >= 1e-12
+    return set_error(L0_INVALID, "lipschitz constant is NaN");
   // ---- per-node classes and parameters (model.py:119-149, perspective.py:36-73) ----
   std::vector<uint8_t> mask((size_t)(B * pv), (uint8_t)FREE);
   std::vector<int> fone((size_t)(B * g.fone_stride), 0);
@@ -608,7 +608,10 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
     r.k3_ms = prof_ms[1];   // slab epilogue + windowed prox
     r.k1_ms = prof_ms[2];   // forward contraction X (beta step)
     r.k1_count = r.k2_count = r.k3_count = prof_n;
-    if (h.err != ST_OK && first_err == ST_OK) { first_err = h.err; err_node = b; }
+    // a window tie overflow has no full-sort re-run in batched mode
+    const int err = h.err == ST_TIE_OVERFLOW ? (int)ST_UNSUPPORTED : h.err;
+    r.status = err;
+    if (err != ST_OK && first_err == ST_OK) { first_err = err; err_node = b; }
   }
   if (first_err != ST_OK)
     return set_error(first_err, "node " + std::to_string(err_node) + " failed (status " +

@@ -21,7 +21,10 @@ namespace l0 {
 enum Loss : int { SQUARED_ERROR = 0, LOGISTIC = 1, SQUARED_HINGE = 2, POISSON = 3, GAMMA = 4 };
 enum Dtype : int { F64 = 0, F32 = 1 };
 enum Status : int {
-  ST_OK = 0, ST_INVALID = 1, ST_NUMERICAL = 2, ST_INFEASIBLE = 3, ST_UNSUPPORTED = 4, ST_CUDA = 5
+  ST_OK = 0, ST_INVALID = 1, ST_NUMERICAL = 2, ST_INFEASIBLE = 3, ST_UNSUPPORTED = 4, ST_CUDA = 5,
+  // internal: the windowed prox met an exact tie group larger than its window
+  // (duplicated columns); the host re-runs the solve on the full key sort
+  ST_TIE_OVERFLOW = 7
 };
 enum Termination : int {
   TERM_CONVERGED = 0, TERM_ITERATION_LIMIT = 1, TERM_TIME_LIMIT = 2,

@@ -85,6 +85,10 @@ struct EngineArgs {
   double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta)
   double* fz_cpart;  // [fz_ncl][8] per-cluster loss, non-finite, F* sums
   int prox_full_sort; // 1: K3 sorts all p keys (reference check path); 0: windowed sort
+  // verification ring of K3 decisions (l0_problem_set_prox_record; nullptr: off):
+  // per iteration kProxRecHead ints (see ProxRec) + the first prox_rec_w sorted ids
+  int* prox_rec;
+  int prox_rec_cap, prox_rec_w;
   // PLAIN-mode vectors
   const double* in_vec;
   double* out_vec;
@@ -114,6 +118,40 @@ __device__ __forceinline__ double momentum(int64_t phi) {
 
 // bound check cadence (fista.py:182)
 __device__ __forceinline__ bool is_check(int64_t t, int bci) { return t == 1 || (t % bci) == 0; }
+
+// K3 decision record (prox.py:101-116 internals the parity tests compare with
+// the oracle's stable argsort and PAVA pool): header fields, then ids
+enum ProxRec : int {
+  PR_ITER = 0,   // iteration whose beta the prox produced (fista.py:159 t)
+  PR_HOW = 1,    // _prox_gstar_core case: 0 copy, 1 elementwise, 2 sort + PAVA
+  PR_POOL = 2,   // 1: a merged pool [a*, c*] exists, 0: none
+  PR_A = 3, PR_C = 4,   // pool bounds in sorted positions of the free coordinates
+  PR_LEN = 5,    // sorted prefix length K3 materialised (all free coords: full sort)
+  PR_PATH = 6,   // 0 window fast path, 1 window extensions, 2 full key sort
+  PR_NFREE = 7,
+  kProxRecHead = 8
+};
+// All threads of the K3 CTA call this after the pool search (a.perm holds the
+// sorted prefix and is visible block-wide).
+__device__ __forceinline__ void record_prox(int* rec, int cap, int w, const int* perm,
+                                            int64_t iter, int how, int pool, int64_t astar,
+                                            int64_t cstar, int64_t len, int path, int64_t nf) {
+  if (rec == nullptr || cap <= 0) return;
+  int* r = rec + (size_t)(iter % cap) * (size_t)(kProxRecHead + w);
+  if (threadIdx.x == 0) {
+    r[PR_ITER] = (int)iter;
+    r[PR_HOW] = how;
+    r[PR_POOL] = pool;
+    r[PR_A] = pool ? (int)astar : -1;
+    r[PR_C] = pool ? (int)cstar : -1;
+    r[PR_LEN] = (int)len;
+    r[PR_PATH] = path;
+    r[PR_NFREE] = (int)nf;
+  }
+  const int64_t m = len < w ? len : w;
+  for (int64_t i = threadIdx.x; i < w; i += blockDim.x)
+    r[kProxRecHead + i] = i < m ? perm[i] : -1;
+}
 
 // Launch helpers (defined in gemv.cu / prox.cu)
 cudaError_t launch_k1(const EngineArgs& a, int mode, cudaStream_t s);

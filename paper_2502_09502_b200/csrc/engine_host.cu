@@ -102,6 +102,8 @@ struct Problem {
   int fused_planned = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  int force_full_sort = 0;      // re-run after a window tie overflow (ST_TIE_OVERFLOW)
+  double trace_delivered = -1;  // ... skipping the trace records already delivered
 };
 
 }  // namespace l0
@@ -443,6 +445,17 @@ int32_t l0_debug_probe(l0_problem* P, int64_t* out16) {
   return ST_OK;
 }
 
+int32_t l0_problem_set_prox_record(l0_problem* P, int32_t* d_ring, int32_t cap, int32_t width) {
+  if (!P) return set_error(ST_INVALID, "null argument");
+  if (d_ring != nullptr && (cap < 1 || width < 0))
+    return set_error(ST_INVALID, "prox record ring needs cap >= 1 and width >= 0");
+  destroy_graphs(*P);   // the ring pointer is baked into the captured K3 launches
+  P->a.prox_rec = d_ring;
+  P->a.prox_rec_cap = d_ring ? cap : 0;
+  P->a.prox_rec_w = d_ring ? width : 0;
+  return ST_OK;
+}
+
 int32_t l0_debug_scratch(l0_problem* P, double* h_out, int64_t count) {
   if (!P || !h_out || !P->ws) return set_error(ST_INVALID, "null argument");
   count = std::min<int64_t>(count, P->a.pv);
@@ -519,8 +532,14 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   if (!(o->gap_tolerance > 0)) return set_error(ST_INVALID, "gap_tolerance must be positive");
   if (o->bound_check_interval < 1) return set_error(ST_INVALID, "bound_check_interval must be >= 1");
   if (o->max_iterations < 1) return set_error(ST_INVALID, "max_iterations must be >= 1");
-  if (!(o->lipschitz > 0) || std::isnan(o->lipschitz))
-    return set_error(ST_INVALID, "lipschitz constant must be provided and positive");
+  // fista.py:101 clamps any L to max(L, 1e-12) (an all-zero X gives L = 0);
+  // only NaN is rejected
+  if (std::isnan(o->lipschitz)) return set_error(ST_INVALID, "lipschitz constant is NaN");
+  // row sharding over NCCL: every rank must replay the same number of chunks
+  // (each holds all-reduces), so no rank may stop on its own host clock
+  if (a.multi && P->comm && std::isfinite(o->time_limit))
+    return set_error(ST_UNSUPPORTED, "time_limit is not available with row sharding over NCCL "
+                                     "(ranks would stop after different chunks)");
 
   std::vector<uint8_t> mask;
   std::vector<int> fone;
@@ -591,8 +610,8 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   // extensions (a PAVA pool spanning much of p, as on C3: K3 0.34 -> 0.19 ms);
   // L0_FULL_SORT=0/1 pins either variant
   const char* full_env = getenv("L0_FULL_SORT");
-  a.prox_full_sort = full_env ? atoi(full_env) : 0;
-  const bool auto_full = full_env == nullptr;
+  a.prox_full_sort = full_env ? atoi(full_env) : P->force_full_sort;
+  const bool auto_full = full_env == nullptr && !P->force_full_sort;
   // the captured graphs always see the node buffers; Params::node_mode gates their use
   a.mask = P->d_mask;
   a.fone = P->d_fone;
@@ -652,7 +671,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   }
   int64_t trace_seen = 0;
   int64_t chunks = 0;
-  bool aborted = false, stop_sent = false;
+  bool aborted = false, stop_sent = false, abort_deferred = false;
   int64_t t_before[2] = {0, 0};
   int64_t t_prev = 0, ext_prev = 0;
   State* last = nullptr;
@@ -701,8 +720,16 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     if (cb && !aborted) {
       for (; trace_seen < h->trace_count; ++trace_seen) {
         const TraceRec& r = h->trace[trace_seen % kTraceCap];
+        if (r.iteration <= P->trace_delivered) continue;   // delivered before a re-run
         l0_trace_record rec{r.iteration, r.primal, r.dual, r.gap, r.restarted};
         if (cb(&rec, user) != 0) {
+          if (a.multi && P->comm) {
+            // sharded: keep replaying in step with the other ranks (their
+            // all-reduces wait for ours); report the abort after the solve
+            abort_deferred = true;
+            cb = nullptr;
+            break;
+          }
           aborted = true;
           break;
         }
@@ -740,6 +767,22 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     ++inflight;
   }
   const State* h = last;
+  if (!aborted && h->err == ST_TIE_OVERFLOW && !a.prox_full_sort) {
+    // an exact tie group larger than the prox window (prox_window.cu select_window):
+    // the same deterministic solve on the full key sort, whose trajectory is
+    // identical (test_k3_variants_agree); trace records already delivered are skipped
+    L0_CUDA_TRY(cudaStreamSynchronize(s));
+    double delivered = -1;
+    for (int64_t i = std::max<int64_t>(0, trace_seen - kTraceCap); i < trace_seen; ++i)
+      delivered = std::max(delivered, h->trace[i % kTraceCap].iteration);
+    P->force_full_sort = 1;
+    P->trace_delivered = cb ? delivered : -1;
+    const int rc2 = l0_fista_solve(P, k, M, lambda2, o, node, d_warm, d_beta_out, rep, cb, user, stream);
+    P->force_full_sort = 0;
+    P->trace_delivered = -1;
+    rep->gpu_launches += launches;
+    return rc2;
+  }
   if (aborted) {
     L0_CUDA_TRY(cudaStreamSynchronize(s));
     rep->status = L0_ABORTED_CODE;
@@ -765,6 +808,10 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   L0_CUDA_TRY(cudaStreamSynchronize(s));
   rep->gpu_launches = launches;
   rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (abort_deferred) {
+    rep->status = L0_ABORTED_CODE;
+    return set_error(L0_ABORTED_CODE, "aborted by the trace callback (after the sharded solve)");
+  }
   if (h->err != ST_OK) {
     if (h->err == ST_NUMERICAL)
       return set_error(ST_NUMERICAL, "composite objective became non-finite at iteration " +
@@ -772,7 +819,9 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
                                          "; the step-size constant is likely too small");
     if (h->err == ST_INVALID) return set_error(ST_INVALID, "u contains non-finite entries");
     if (h->err == ST_UNSUPPORTED)
-      return set_error(ST_UNSUPPORTED, "budget k too large for the on-chip envelope kernel");
+      return set_error(ST_UNSUPPORTED, "budget k exceeds the envelope kernel's top-k capacity (2048)");
+    if (h->err == ST_TIE_OVERFLOW)
+      return set_error(ST_UNSUPPORTED, "exact tie group larger than the prox window (4096 keys)");
     return set_error(h->err, "solve failed");
   }
   return ST_OK;

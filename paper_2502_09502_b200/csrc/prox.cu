@@ -339,6 +339,9 @@ __device__ void prox_post_sort(const PostArgs& q_in, ProxSmem& sm) {
   const int64_t astar = sm.found > 0 ? sm.astar : INT64_MAX;
   const int64_t cstar = sm.found > 0 ? sm.cstar : -1;
   const double vstar = sm.vstar;
+  if (q.rec != nullptr)
+    record_prox(q.rec, q.rec_cap, q.rec_w, q.perm, q.rec_iter, how, sm.found > 0 ? 1 : 0, astar,
+                cstar, how == 2 ? nf : 0, 2, nf);
 
   // scatter
   double total = 0.0, amax = 0.0, rest = 0.0;
@@ -477,6 +480,10 @@ __device__ __forceinline__ PostArgs iter_post_args(const EngineArgs& a) {
   q.want_g = 1;
   q.g_out = &st->g_next;
   q.st = st;
+  q.rec = a.prox_rec;
+  q.rec_cap = a.prox_rec_cap;
+  q.rec_w = a.prox_rec_w;
+  q.rec_iter = st->t + 1;
   return q;
 }
 

@@ -56,6 +56,9 @@ struct PostArgs {
   int want_g;         // also evaluate g(out) into *g_out
   double* g_out;
   State* st;          // diagnostics / error reporting (nullable)
+  int* rec;           // K3 decision ring (EngineArgs::prox_rec; nullptr: off)
+  int rec_cap, rec_w;
+  int64_t rec_iter;
 };
 
 template <int T>

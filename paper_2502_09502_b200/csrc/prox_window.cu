@@ -533,8 +533,8 @@ __device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) 
     bool more = true;
     while (sm.res == 3 && more) {
       select_window(a.key, p, ub, kWinCap, sm);
-      if (sm.sel_state == 2) {
-        if (tid == 0) { atomicExch(&st->err, (int)ST_UNSUPPORTED); st->done = 1; }
+      if (sm.sel_state == 2) {   // tie group > kWinCap: the host falls back to the full sort
+        if (tid == 0) { atomicExch(&st->err, (int)ST_TIE_OVERFLOW); st->done = 1; }
         return 0;
       }
       const unsigned long long lb = sm.sel_lb;
@@ -561,6 +561,8 @@ __device__ int prox_window_body(const EngineArgs& a, ProxSmem& ps, WinSmem& sm) 
   const int64_t astar = (how == 2 && sm.res == 1) ? sm.astar : INT64_MAX;
   const int64_t cstar = (how == 2 && sm.res == 1) ? sm.cstar : -1;
   const double vstar = sm.vstar;
+  record_prox(a.prox_rec, a.prox_rec_cap, a.prox_rec_w, a.perm, st->t + 1, how,
+              (how == 2 && sm.res == 1) ? 1 : 0, astar, cstar, len, dirty ? 1 : 0, nf);
 
   L0_STAMP(st, 6);
   // ---- scatter ----------------------------------------------------------------

@@ -67,14 +67,20 @@ def ar1_rows(n: int, p: int, sigma: float, rng: np.random.Generator,
     X = rng.standard_normal((n, p))
     if sigma != 0.0:
         c = np.sqrt(1.0 - sigma * sigma)
-        col_prev = X[:, 0]
-        tmp = np.empty(n)
-        for j in range(1, p):
-            col = X[:, j]
-            np.multiply(col, c, out=tmp)          # c * w_j
-            np.multiply(col_prev, sigma, out=col)  # sigma * x_{j-1}
-            np.add(col, tmp, out=col)
-            col_prev = col
+        # the recursion is elementwise per row, so blocks of rows run it on a
+        # transposed (column-contiguous) copy: the same roundings, without the
+        # strided column walk over the whole matrix
+        R = 512
+        tmp = np.empty(R)
+        for r0 in range(0, n, R):
+            blk = np.ascontiguousarray(X[r0:r0 + R].T)     # p x rows
+            t = tmp[:blk.shape[1]]
+            for j in range(1, p):
+                col = blk[j]
+                np.multiply(col, c, out=t)                  # c * w_j
+                np.multiply(blk[j - 1], sigma, out=col)     # sigma * x_{j-1}
+                np.add(col, t, out=col)
+            X[r0:r0 + R] = blk.T
     if dtype != np.float64:
         X = X.astype(dtype)
     return X

@@ -129,10 +129,19 @@ class ShardedProblem:
     def p(self) -> int:
         return self.instance.p
 
-    def lipschitz(self) -> float:
-        """curvature * lambda_max(X^T X) * 1.01 over all ranks (model.py:316-327)."""
+    def lipschitz(self, method: str = "power") -> float:
+        """curvature * lambda_max(X^T X) * 1.01 over all ranks (model.py:316-327);
+        ``method="lanczos"``: device Lanczos on the all-reduced X^T X v."""
         from .model import _CURVATURE, LIPSCHITZ_SAFETY
         dp = self.instance.device_problem()
+        if method == "lanczos":
+            from .spectral import engine_normal_op, lanczos_lambda_max
+            red = None
+            if self.world > 1:
+                import torch.distributed as dist
+                red = lambda t: dist.all_reduce(t, group=self.group)
+            lam = lanczos_lambda_max(engine_normal_op(dp), self.p, dp.X.device, allreduce=red)
+            return _CURVATURE[self.instance.loss] * lam * LIPSCHITZ_SAFETY
         v0 = np.random.default_rng(0).standard_normal(self.p)
         v0 /= np.linalg.norm(v0)
         red = _torch_allreduce(self.group) if self.world > 1 else (lambda a: a)

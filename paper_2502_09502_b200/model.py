@@ -247,7 +247,12 @@ class ProblemInstance:
         return self.X.shape[1]
 
     def device_problem(self) -> DeviceProblem:
-        """The HBM-resident copy of (X, y) used by every engine call (built once)."""
+        """The HBM-resident copy of (X, y) used by every engine call (built once).
+
+        X (and y) are treated as immutable after the first engine call, as the
+        reference treats its private float64 copy (model.py:92): in-place
+        edits of the host array are not seen; assign a new array to ``X`` (a
+        new object re-uploads) or call ``release_device()``."""
         if self._dev is None or self._dev_key != id(self.X):
             if not is_solver_grade(self.loss):
                 _engine_loss(self.loss)
@@ -389,10 +394,28 @@ def power_iteration_lambda_max(instance: ProblemInstance, tol=_POWER_TOL,
     return float(lam.value)
 
 
-def lipschitz_constant(instance: ProblemInstance) -> float:
-    """curvature * lambda_max(X^T X) * 1.01 (model.py:316-327)."""
+def lanczos_lambda_max(instance: ProblemInstance, tol: float = 1e-13, max_steps: int = 300) -> float:
+    """lambda_max(X^T X) by device Lanczos with full reorthogonalisation
+    (spectral.py): converges where the reference's 500-step power iteration
+    does not."""
+    from .spectral import engine_normal_op, lanczos_lambda_max as _lanczos
+    dp = instance.device_problem()
+    return _lanczos(engine_normal_op(dp), instance.p, dp.X.device, tol=tol, max_steps=max_steps)
+
+
+def lipschitz_constant(instance: ProblemInstance, *, method: str = "power") -> float:
+    """curvature * lambda_max(X^T X) * 1.01 (model.py:316-327).
+
+    ``method="power"`` (default) is the reference's estimator, failing the same
+    way (NumericalError after 500 steps); ``method="lanczos"`` is the engine's
+    robust extension (same curvature and 1.01 safety factor)."""
     if not is_solver_grade(instance.loss):
         raise UnsupportedOperationError(
             f"{instance.loss.value} has no global gradient Lipschitz constant")
-    lam = power_iteration_lambda_max(instance)
+    if method == "power":
+        lam = power_iteration_lambda_max(instance)
+    elif method == "lanczos":
+        lam = lanczos_lambda_max(instance)
+    else:
+        raise InvalidInputError("method must be 'power' or 'lanczos'")
     return _CURVATURE[instance.loss] * lam * LIPSCHITZ_SAFETY

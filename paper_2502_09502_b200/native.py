@@ -72,6 +72,7 @@ _PROTOS = {
                                ctypes.POINTER(Node), c_vp, c_vp, ctypes.POINTER(Report), TRACE_CB,
                                c_vp, c_vp]),
     "l0_debug_probe": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
+    "l0_problem_set_prox_record": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
     "l0_debug_scratch": (c_i32, [c_vp, c_vp, c_i64]),
     "l0_matvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "l0_rmatvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -70,3 +70,28 @@ def test_certify_matches_enumeration(seed):
     assert tuple(np.flatnonzero(np.abs(cert.incumbent_beta) > 1e-9)) == S
     # soundness: the certified bound never exceeds the true optimum
     assert cert.global_lower_bound <= obj + 1e-7 * abs(obj)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_certify_logistic_matches_enumeration(seed):
+    """Logistic loss: leaf and node refits are iterative (no closed form), so
+    the certificate must stay sound when a refit is inexact: the
+    certified bound never exceeds the enumeration optimum, and an OPTIMAL
+    status comes with the optimal objective."""
+    from oracle.bnb_oracle import best_subset_logistic
+    from paper_2502_09502_b200 import LossKind, ProblemInstance
+    from paper_2502_09502_b200.bnb import BnBOptions, CertificateStatus, certify
+    rng = np.random.default_rng(300 + seed)
+    X = rng.standard_normal((40, 7))
+    bt = np.zeros(7)
+    bt[rng.choice(7, 2, replace=False)] = rng.choice([-1.0, 1.0], 2) * 1.5
+    y = np.where(rng.random(40) < 1.0 / (1.0 + np.exp(-(X @ bt))), 1.0, -1.0)
+    k, M, lam2 = 2, 3.0, 0.2
+    obj, beta, S = best_subset_logistic(X, y, k, lam2, M)
+    inst = ProblemInstance(X, y, LossKind.LOGISTIC, k, M, lam2)
+    cert = certify(inst, BnBOptions(gap_tolerance=1e-6, batch_size=8))
+    assert cert.global_lower_bound <= obj + 1e-7 * abs(obj)
+    assert cert.incumbent_objective >= obj - 1e-7 * abs(obj)     # a feasible point
+    if cert.status is CertificateStatus.OPTIMAL:
+        assert cert.incumbent_objective == pytest.approx(obj, rel=1e-5)
+    assert cert.status in (CertificateStatus.OPTIMAL, CertificateStatus.GAP_LIMIT)

@@ -1,15 +1,21 @@
 """Parity at BASELINE.json's full sizes.
 
-* C2 (16000 x 16000 fp64, 2 GB X): 40 restarted-FISTA iterations on the GPU
-  (the engine `auto` picks: the single-pass kf_fused_s) against the CPU oracle
-  port of the reference solver on the same inputs and the same injected L:
-  objective within 1e-12, bound within 1e-9, iterate within 1e-9 * max|beta|,
-  identical restart count and support, and the trace records at every bound
-  check.
-* C3 (50000 x 20000 fp32 logistic, 4 GB X): size-independent properties where
-  the oracle would need an 8 GB fp64 copy: the single-pass and two-pass engines
-  agree to summation order, weak duality holds at every bound check, and the
-  prox output satisfies the envelope's box and budget constraints.
+Every case runs the production engine path on the GPU against the CPU oracle
+port of the reference solver (oracle/l0_oracle.py, fista.py:76-222) on the
+same inputs and the same injected L: objective within 1e-12, bound within
+1e-9, iterate within 1e-9 * max|beta|, identical restart count, support and
+bound-check trace records.  fp32 configs store X in fp32 and compute in fp64,
+so the oracle runs on the exact fp64 upcast of the same matrix.
+
+* C2 (16000 x 16000 fp64, 2 GB X): 40 iterations on the single-pass kernel.
+* C3 (50000 x 20000 fp32 logistic, 4 GB X; the oracle's fp64 copy is 8 GB):
+  40 iterations on the single-pass fp32 kernel; plus size-independent
+  properties (single pass vs two pass, weak duality, box/budget).
+* C5 leading-row subsample (100000 x 10000 fp32, the first generator block of
+  C5): 40 iterations on the single-pass fp32 kernel.
+L for C3 / C5 comes from the package's device Lanczos
+(``lipschitz_constant(method="lanczos")``); the reference's power iteration
+does not converge on them.
 """
 
 import numpy as np
@@ -32,6 +38,10 @@ def test_c2_full_size_vs_oracle(engine):
     rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
         lipschitz=L_C2, max_iterations=40, gap_tolerance=1e-300, trace_hook=rec.append))
     assert rep.stats["single_pass"]
+    # the injected constant is a valid L: the package's Lanczos (2 x 1.01 x lambda_max)
+    # sits just below it (2.99073e5)
+    L_lz = engine.lipschitz_constant(inst, method="lanczos")
+    assert L_C2 * (1 - 1e-4) <= L_lz <= L_C2
     trace = []
     with threadpoolctl.threadpool_limits(None):
         ref = l0_oracle.fista(cd.X, cd.y, "squared_error", cd.k, cd.M, cd.lambda2, L=L_C2, max_iter=40,
@@ -51,23 +61,65 @@ def test_c2_full_size_vs_oracle(engine):
         assert ours["dual"] == pytest.approx(theirs["dual"], rel=1e-9)
 
 
-def test_c3_full_size_properties(engine):
-    import torch
-
+@pytest.fixture(scope="module")
+def c3(engine):
     cd = mydata.make_config("C3", scale=1.0)
     inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.LOGISTIC, cd.k, cd.M, cd.lambda2,
                                   dtype="fp32")
-    # L from a GPU power iteration (the reference's 500-iteration one does not
-    # converge on C3); any L >= the true constant is valid
-    Xd = torch.from_numpy(cd.X).cuda().double()
-    v = torch.ones(cd.p, device="cuda", dtype=torch.float64)
-    for _ in range(200):
-        w = Xd.T @ (Xd @ v)
-        lam = float(w.norm())
-        v = w / lam
-    del Xd, v, w
-    torch.cuda.empty_cache()
-    L = 0.25 * lam * 1.05
+    L = engine.lipschitz_constant(inst, method="lanczos")
+    yield cd, inst, L
+    inst.release_device()
+
+
+def _vs_oracle(engine, cd, inst, L, iters=40, path="single_pass"):
+    import threadpoolctl
+    from oracle import l0_oracle
+
+    rec = []
+    rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
+        lipschitz=L, max_iterations=iters, gap_tolerance=1e-300, engine_path=path,
+        trace_hook=rec.append))
+    assert rep.stats["single_pass"] == (path == "single_pass")
+    X64 = np.asarray(cd.X, dtype=np.float64)
+    trace = []
+    with threadpoolctl.threadpool_limits(None):
+        ref = l0_oracle.fista(X64, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=iters,
+                              gap_tol=1e-300, trace=trace.append)
+    del X64
+    assert rep.iterations == ref["iterations"] == iters
+    assert rep.restarts == ref["restarts"]
+    assert rep.primal_value == pytest.approx(ref["primal_value"], rel=1e-12)
+    assert rep.dual_bound == pytest.approx(ref["dual_bound"], rel=1e-9)
+    scale = float(np.max(np.abs(ref["beta"])))
+    np.testing.assert_allclose(rep.beta, ref["beta"], rtol=0, atol=1e-9 * scale)
+    thr = 1e-9 * cd.M
+    assert np.array_equal(np.abs(rep.beta) > thr, np.abs(ref["beta"]) > thr)
+    assert len(rec) == len(trace)
+    for ours, theirs in zip(rec, trace):
+        assert ours["iteration"] == theirs["iteration"]
+        assert ours["restarted"] == theirs["restarted"]
+        assert ours["primal"] == pytest.approx(theirs["primal"], rel=1e-12)
+        assert ours["dual"] == pytest.approx(theirs["dual"], rel=1e-9)
+    return rep
+
+
+def test_c3_full_size_vs_oracle(engine, c3):
+    cd, inst, L = c3
+    _vs_oracle(engine, cd, inst, L)
+
+
+def test_c5_subsample_vs_oracle(engine):
+    cd = mydata.make_config("C5", scale=0.1)       # rows 0..99999 of C5 (block [0, 0])
+    assert (cd.n, cd.p) == (100_000, 10_000)
+    inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M,
+                                  cd.lambda2, dtype="fp32")
+    L = engine.lipschitz_constant(inst, method="lanczos")
+    _vs_oracle(engine, cd, inst, L)
+    inst.release_device()
+
+
+def test_c3_full_size_properties(engine, c3):
+    cd, inst, L = c3
     res = {}
     for path in ("two_pass", "single_pass"):
         rec = []
