@@ -2,22 +2,29 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one restarted-FISTA iteration of the perspective relaxation on the
-workload BASELINE.json's metric is quoted on (configs[1] = C2: least squares,
-fp64, n = p = 16000, Toeplitz rho 0.7, k=20, M=2, lambda2=0.1; synthetic data
-from the reference's generator with the paper's protocol).  X is 2.05 GB,
-larger than the 126 MB L2, so every pass streams HBM.
+A step is one restarted-FISTA iteration of the perspective relaxation.
 
-ours       value  = K iterations / device time of a K-iteration solve with X resident
-                    (stop_on_gap=False so exactly K iterations run, bound checks included)
-           e2e    = iterations / time of full solves to the C2 target (relative gap
-                    <= 1e-6) through solve_relaxation on an instance whose X lives
-                    in pinned host memory (H2D of X and y + D2H of beta inside)
-reference  the CPU oracle port of the reference solver (oracle/l0_oracle.py, numpy +
-           C PAVA, all host threads), K iterations of the same workload
-N > 1      node sharding (default): each GPU runs its own branch-and-bound node of C2
-           (independent units, no collective, "weak"); --shard rows splits C2's rows
-           over the ranks with the engine's NCCL all-reduce each iteration ("strong").
+N = 1 (headline): configs[1] = C2, least squares, fp64, n = p = 16000,
+Toeplitz rho 0.7, k=20, M=2, lambda2=0.1, synthetic data from the reference's
+own generator (2.05 GB X, far beyond the 126 MB L2: every pass streams HBM).
+    value  = K iterations / device time of a K-iteration solve, X resident
+             (stop_on_gap=False so exactly K iterations run, bound checks included)
+    e2e    = iterations / time of full solves to the C2 target (relative gap
+             <= 1e-6) through solve_relaxation with X in host memory: the
+             numpy (pageable) call a drop-in user makes, H2D of X and y and D2H
+             of beta inside; the pinned-tensor variant is reported beside it
+  sections on the same line: C5 (10^6 x 10^4 fp32, 40 GB, the row-sharding
+  config) on one GPU with its own roofline and CPU baseline; C4 batched nodes
+  (tcgen05 tensor roofline); C1 and C3.
+N > 1 (torchrun, one rank per GPU, NCCL):
+    --shard rows (default): C5's rows split over the ranks, each rank
+             generating its own rows in HBM; the engine all-reduces the gradient
+             over NCCL every iteration ("strong": fixed total work);
+    --shard nodes: C4's 512 nodes split over the ranks, each rank one batched
+             call on its share (no collective).
+reference  the reference's own CPU solver (baseline/_ref, the unmodified
+           l0cert.fista.solve_relaxation) on the same config, all host threads;
+           the oracle port (oracle/l0_oracle.py) is timed beside it.
 """
 
 import argparse
@@ -34,14 +41,20 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/l0_numba_cache")
 
-WORKLOAD = "C2"
 # injected step constant 2 * 1.01 * lambda_max(X^T X) for C2 (SURVEY.md §8(d):
-# Lanczos 2.99073e5), rounded up so it stays a valid Lipschitz bound
+# Lanczos 2.99073e5), rounded up so it stays a valid Lipschitz bound; the
+# package's own Lanczos reproduces it (tests/test_gpu_fullsize.py)
 L_C2 = 2.9908e5
 REL_GAP = 1e-6
 TF32_DENSE_PEAK = 1100.0   # TFLOP/s, B200 dense TF32 (B200_PROFILING.md)
-METRIC = "FISTA iters/sec (C2 perspective relaxation; N>1: one branch-and-bound node per GPU)"
+METRIC = "FISTA iters/sec (N=1: C2 perspective relaxation; N>1: C5 rows sharded over the GPUs)"
+C2_WORKLOAD = ("C2: least-squares root perspective relaxation, n=p=16000, Toeplitz rho=0.7, "
+               "k=20, M=2, lambda2=0.1, SNR=5, fp64")
+C5_WORKLOAD = ("C5: least-squares root perspective relaxation, n=1e6, p=1e4 fp32 (40 GB), "
+               "Toeplitz rho=0.5, k=25, M=2, lambda2=0.1, SNR=5; rows sharded over the GPUs "
+               "with the engine's NCCL all-reduce of the gradient each iteration")
 
 
 def log(*a):
@@ -55,21 +68,29 @@ def dist_env():
     return world, rank, local
 
 
-def make_inputs(scale):
+def c2_inputs(scale):
     from paper_2502_09502_b200 import data
     t0 = time.time()
-    cd = data.make_config(WORKLOAD, scale=scale)
-    log(f"[bench] generated {WORKLOAD} n={cd.n} p={cd.p} in {time.time() - t0:.1f}s")
+    cd = data.make_config("C2", scale=scale)
+    log(f"[bench] generated C2 n={cd.n} p={cd.p} in {time.time() - t0:.1f}s")
     return cd
 
 
-def base_config(cd, n_gpus):
-    return {"workload": "C2: least-squares root perspective relaxation, n=p=%d, Toeplitz rho=0.7, "
-                        "k=20, M=2, lambda2=0.1, SNR=5" % cd.n,
+def c2_config(cd):
+    return {"workload": C2_WORKLOAD if cd.n == 16000 else C2_WORKLOAD + f" (scaled to n=p={cd.n})",
             "n": cd.n, "p": cd.p, "k": cd.k, "M": cd.M, "lambda2": cd.lambda2,
             "x_bytes": int(cd.X.nbytes), "lipschitz": L_C2,
             "l2_policy": "inputs larger than L2 (X = %.2f GB vs 126 MB)" % (cd.X.nbytes / 1e9),
-            "parallelism": "rows%d" % n_gpus if n_gpus > 1 else "single"}
+            "parallelism": "single"}
+
+
+def c5_config(n, p, world, shard="rows"):
+    return {"workload": C5_WORKLOAD if n == 1_000_000 else C5_WORKLOAD + f" (scaled to n={n})",
+            "n": n, "p": p, "k": 25, "M": 2.0, "lambda2": 0.1, "x_bytes": n * p * 4,
+            "l2_policy": "inputs larger than L2 (X = %.1f GB vs 126 MB)" % (n * p * 4 / 1e9),
+            "parallelism": f"{shard}{world}",
+            "data_generation": "AR(1) rows drawn in HBM per 100k-row block (torch Philox, "
+                               "seeded per block: the same matrix at every world size)"}
 
 
 # ---------------------------------------------------------------------------
@@ -95,6 +116,7 @@ class ClockSampler:
             self.thread.start()
         except Exception:
             self.proc = None
+        time.sleep(0.3)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -131,54 +153,164 @@ def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes (read + write) per launch of each kernel, from the committed ncu
-    --set full captures (profiles/ncu_summary.json)."""
+def ncu_traffic(key):
+    """dram bytes (read + write) per launch of a kernel from the committed ncu
+    --set full captures (profiles/ncu_summary.json), keyed by config/kernel."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return {k: v.get("dram_bytes_per_launch") for k, v in d.get("kernels", {}).items()}
+        ks = d.get("kernels", {})
+        v = ks.get(key)
+        if v is None and key.startswith("C2/"):      # round-1 captures are keyed by kernel
+            v = ks.get(key.split("/", 1)[1])
+        return v.get("dram_bytes_per_launch") if v else None
     except Exception:
-        return {}
+        return None
+
+
+def kf_roofline(st, n, p, s_el, peak, peak_src, traffic_key):
+    """HBM roofline of the single-pass kernel kf_fused_s from the per-launch
+    CUDA-event durations (algorithmic bytes: X once + y, u_{t-1}, u_t, beta)."""
+    avg = lambda k: st[k + "_ms"] / max(1, st[k + "_count"])
+    kf_bytes = n * p * s_el + 8 * (4 * n + p)
+    achieved = kf_bytes / (avg("k2") / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "kf_fused_s", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": ncu_traffic(traffic_key), "algorithmic_bytes_per_launch": kf_bytes,
+            "launch_ms": avg("k2"),
+            "other_kernels": {"kr_reduce_epilogue": {"launch_ms": avg("k1")},
+                              "k3_prox_window": {"launch_ms": avg("k3")}}}
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference solver)
+# CPU baselines: the unmodified reference (baseline/_ref) and the oracle port
 # ---------------------------------------------------------------------------
-def cpu_baseline(cd, iters, warm=2):
+def _reference_module():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "l0cert")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import l0cert.fista as rf
+        import l0cert.model as rm
+        return rf, rm
+    except Exception as exc:   # reported by the caller
+        log(f"[bench] reference import failed: {exc!r}")
+        return None
+
+
+def time_reference(X, y, loss, k, M, lam2, L, iters, warm=2):
+    """The reference's own solve_relaxation (fista.py:76-222), unmodified, on
+    all host threads: K iterations after a warm-up solve (numba compile / cache
+    load).  Returns seconds per iteration or None if the reference is absent."""
+    mods = _reference_module()
+    if mods is None:
+        return None
+    rf, rm = mods
+    import threadpoolctl
+    kind = {"squared_error": rm.LossKind.SQUARED_ERROR, "logistic": rm.LossKind.LOGISTIC}[loss]
+    inst = rm.ProblemInstance(X=X, y=y, loss=kind, k=int(k), M=float(M), lambda2=float(lam2))
+    with threadpoolctl.threadpool_limits(os.cpu_count()):
+        rf.solve_relaxation(inst, opts=rf.FistaOptions(lipschitz=L, max_iterations=warm,
+                                                       gap_tolerance=1e-300))
+        t0 = time.perf_counter()
+        rep = rf.solve_relaxation(inst, opts=rf.FistaOptions(lipschitz=L, max_iterations=iters,
+                                                             gap_tolerance=1e-300))
+        dt = time.perf_counter() - t0
+    return dt / max(1, rep.iterations)
+
+
+def time_port(X, y, loss, k, M, lam2, L, iters, warm=2):
+    """The oracle port (numpy/OpenBLAS + C PAVA) on all host threads."""
     import threadpoolctl
     from oracle import l0_oracle
+    with threadpoolctl.threadpool_limits(os.cpu_count()):
+        l0_oracle.fista(X, y, loss, k, M, lam2, L=L, max_iter=warm, gap_tol=1e-300,
+                        stop_on_gap=False)
+        t0 = time.perf_counter()
+        l0_oracle.fista(X, y, loss, k, M, lam2, L=L, max_iter=iters, gap_tol=1e-300,
+                        stop_on_gap=False)
+        dt = time.perf_counter() - t0
+    return dt / iters
+
+
+def cpu_baseline_c2(cd, iters, warm=2, prefer_reference=True):
     X = cd.X if cd.X.dtype == np.float64 else cd.X.astype(np.float64)
     cores = os.cpu_count()
-    with threadpoolctl.threadpool_limits(cores):
-        l0_oracle.fista(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L_C2, max_iter=warm,
-                        gap_tol=1e-300, stop_on_gap=False)
-        t0 = time.perf_counter()
-        l0_oracle.fista(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L_C2, max_iter=iters,
-                        gap_tol=1e-300, stop_on_gap=False)
-        dt = time.perf_counter() - t0
-    return {"value": iters / dt, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": f"{iters} FISTA iterations of {WORKLOAD} (after {warm} warm-up) with the "
-                      f"numpy/OpenBLAS + C-PAVA oracle port, {cores} threads, {dt:.2f}s"}
+    out = {"unit": "iters/s", "cores": cores}
+    s_ref = time_reference(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L_C2, iters, warm) \
+        if prefer_reference else None
+    s_port = time_port(X, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L_C2, iters, warm)
+    if s_ref is not None:
+        out.update(value=1.0 / s_ref, kind="reference",
+                   sample=f"{iters} FISTA iterations of C2 (after {warm} warm-up) with the "
+                          f"unmodified reference l0cert.fista.solve_relaxation (baseline/_ref), "
+                          f"{cores} threads", port_value=1.0 / s_port)
+    else:
+        out.update(value=1.0 / s_port, kind="port",
+                   sample=f"{iters} FISTA iterations of C2 (after {warm} warm-up) with the "
+                          f"numpy/OpenBLAS + C-PAVA oracle port, {cores} threads")
+    return out
+
+
+def c5_host_sample(rows, device):
+    """The leading `rows` rows of C5 (generator block 0) copied to host fp64,
+    with y: the bounded CPU sample whose per-iteration time scales with n."""
+    from paper_2502_09502_b200 import data
+    X, y = data.c5_shard_device(0, rows, device)
+    return X.double().cpu().numpy(), y.cpu().numpy()
+
+
+def cpu_baseline_c5(n_full, rows, iters, device, L=None):
+    Xh, yh = c5_host_sample(rows, device)
+    if L is None:
+        import scipy.sparse.linalg as sla
+        from scipy.sparse.linalg import LinearOperator
+        op = LinearOperator((Xh.shape[1], Xh.shape[1]), matvec=lambda v: Xh.T @ (Xh @ v),
+                            dtype=np.float64)
+        L = 2.0 * 1.01 * float(sla.eigsh(op, k=1, which="LA", tol=1e-8,
+                                         return_eigenvectors=False)[0])
+    cores = os.cpu_count()
+    s_ref = time_reference(Xh, yh, "squared_error", 25, 2.0, 0.1, L, iters, warm=1)
+    s_port = time_port(Xh, yh, "squared_error", 25, 2.0, 0.1, L, iters, warm=1)
+    s = s_ref if s_ref is not None else s_port
+    scale = rows / n_full           # per-iteration work is linear in n at fixed p
+    return {"value": scale / s, "unit": "iters/s", "cores": cores,
+            "kind": "reference" if s_ref is not None else "port",
+            "sample": f"{iters} FISTA iterations on the leading {rows} rows of C5 (fp64 on host), "
+                      f"{'unmodified reference' if s_ref is not None else 'oracle port'}, "
+                      f"{cores} threads; rate extrapolated x{rows}/{n_full} to the full n",
+            "port_value": scale / s_port}
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cd = make_inputs(args.scale)
-    cb = cpu_baseline(cd, args.steps, warm=args.warmup)
-    line = {"metric": METRIC, "value": cb["value"],
-            "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
-            "config": base_config(cd, 1), "impl": "reference", "cpu_baseline": cb,
+    if world > 1 and args.shard == "rows":
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        n = int(1_000_000 * args.c5_scale)
+        cb = cpu_baseline_c5(n, args.c5_cpu_rows, max(1, min(args.steps, 5)), dev)
+        cfg = c5_config(n, 10_000, world)
+        dtype = "f64"
+    else:
+        cd = c2_inputs(args.scale)
+        cb = cpu_baseline_c2(cd, args.steps, warm=min(args.warmup, 2))
+        cfg = c2_config(cd)
+        dtype = "f64"
+    line = {"metric": METRIC, "value": cb["value"], "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / cb["value"],
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded, see config)",
+            "config": cfg, "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -218,20 +350,26 @@ def tf32_peak(seconds=1.5):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+def c4_setup(args, nodes_total):
+    import paper_2502_09502_b200 as eng
+    from paper_2502_09502_b200 import data
+    t0 = time.time()
+    cd = data.make_config("C4", scale=args.c4_scale, nodes=nodes_total)
+    inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2,
+                               dtype="fp32")
+    nodes = [None] + [eng.NodeState(fixed_one=f1, fixed_zero=f0)
+                      for f0, f1 in cd.nodes[:nodes_total - 1]]
+    L = eng.lipschitz_constant(inst, method="lanczos")
+    log(f"[bench] C4 generated + L in {time.time() - t0:.1f}s")
+    return cd, inst, nodes, L
+
+
 def run_batched(args):
     """C4: 512 node relaxations (n=20000, p=5000 fp32) advanced together; the two
     X passes per iteration are tcgen05 3xTF32 contractions."""
     import torch
     import paper_2502_09502_b200 as eng
-    from paper_2502_09502_b200 import data
-    t0 = time.time()
-    cd = data.make_config("C4", scale=args.c4_scale, nodes=args.c4_nodes)
-    inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2,
-                               dtype="fp32")
-    nodes = [None] + [eng.NodeState(fixed_one=f1, fixed_zero=f0)
-                      for f0, f1 in cd.nodes[:args.c4_nodes - 1]]
-    L = eng.lipschitz_constant(inst)
-    log(f"[bench] C4 generated + L in {time.time() - t0:.1f}s")
+    cd, inst, nodes, L = c4_setup(args, args.c4_nodes)
     B, n, p, K = len(nodes), cd.n, cd.p, args.c4_steps
     opts = lambda it, prof: eng.FistaOptions(lipschitz=L, max_iterations=it, stop_on_gap=False,
                                              profile=prof)
@@ -240,7 +378,6 @@ def run_batched(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(0)
     clocks.start()
-    time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     reps = eng.solve_relaxation_batched(inst, nodes, opts=opts(K, False), return_device=True)
@@ -260,11 +397,11 @@ def run_batched(args):
     tensor_t = 3 * useful_t / (gt / 1e3) / 1e12
     cpu = None
     if not args.no_cpu:
+        X64 = cd.X.astype(np.float64)
+        nd = nodes[1]
         import threadpoolctl
         from oracle import l0_oracle
-        X64 = cd.X.astype(np.float64)
         cores = os.cpu_count()
-        nd = nodes[1]
         with threadpoolctl.threadpool_limits(cores):
             l0_oracle.fista(X64, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=1,
                             fixed_one=nd.fixed_one, fixed_zero=nd.fixed_zero, stop_on_gap=False)
@@ -297,6 +434,53 @@ def run_batched(args):
             "cpu_baseline": cpu}
 
 
+# ---------------------------------------------------------------------------
+# C5 on one GPU (the row-sharding config at N=1)
+# ---------------------------------------------------------------------------
+def run_c5_single(args):
+    import torch
+    import paper_2502_09502_b200 as eng
+    from paper_2502_09502_b200 import data
+    n, p = int(data.C5_N * args.c5_scale), data.C5_P
+    t0 = time.time()
+    X, y = data.c5_shard_device(0, n, torch.device("cuda", 0), n=n)
+    inst = eng.ProblemInstance(X, y.cpu().numpy(), eng.LossKind.SQUARED_ERROR, 25, 2.0, 0.1,
+                               dtype="fp32")
+    inst.device_problem()
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    t0 = time.time()
+    L = eng.lipschitz_constant(inst, method="lanczos")
+    l_s = time.time() - t0
+    log(f"[bench] C5 n={n} generated in {gen_s:.1f}s, Lanczos L={L:.6g} in {l_s:.1f}s")
+    K = args.c5_steps
+    o = lambda k, prof: eng.FistaOptions(lipschitz=L, max_iterations=k, gap_tolerance=1e-300,
+                                         stop_on_gap=False, profile=prof)
+    eng.solve_relaxation(inst, opts=o(3, False), return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep = eng.solve_relaxation(inst, opts=o(K, False), return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    assert rep.iterations == K
+    st = eng.solve_relaxation(inst, opts=o(K, True), return_device=True).stats
+    peak, src = measured_peak()
+    roof = kf_roofline(st, n, p, 4, peak, src, "C5/kf_fused_s") if st.get("single_pass") else None
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline_c5(n, args.c5_cpu_rows, 3, "cuda", L=L)
+    del inst, X
+    torch.cuda.empty_cache()
+    return {"workload": C5_WORKLOAD.split(";")[0] + "; one GPU", "n": n, "p": p,
+            "value": K / (ms / 1e3), "unit": "iters/s", "steps": K, "ms_per_step": ms / K,
+            "engine_path": "single_pass" if st.get("single_pass") else "two_pass",
+            "cluster_size": st.get("cluster_size"), "lipschitz": L, "lipschitz_method": "lanczos",
+            "setup_s": {"generate": gen_s, "lanczos": l_s}, "roofline": roof, "cpu_baseline": cpu,
+            "restarts": rep.restarts, "primal": rep.primal_value, "dual": rep.dual_bound}
+
+
 def run_config(name, iters):
     """One more BASELINE config on one GPU (C1: L2-resident fp64; C3: fp32
     logistic): K fixed iterations un-instrumented (iterations/s), then again
@@ -307,22 +491,11 @@ def run_config(name, iters):
     t0 = time.time()
     cd = data.make_config(name, scale=1.0)
     inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype=cd.dtype)
-    # L: the reference's power iteration stops at 500 iterations without converging
-    # on C3; 300 power iterations on the GPU, x 1.05
-    Xd = torch.from_numpy(cd.X).cuda().double()
-    v = torch.randn(Xd.shape[1], device="cuda", dtype=torch.float64, generator=torch.Generator("cuda").manual_seed(0))
-    for _ in range(300):
-        w = Xd.T @ (Xd @ v)
-        lam = float(w.norm())
-        v = w / lam
-    del Xd, v, w
-    torch.cuda.empty_cache()
-    L = {"squared_error": 2.0, "logistic": 0.25}[cd.loss] * lam * 1.05
+    L = eng.lipschitz_constant(inst, method="lanczos")
     gen_s = time.time() - t0
     o = lambda k, prof: eng.FistaOptions(lipschitz=L, max_iterations=k, gap_tolerance=1e-300,
                                          stop_on_gap=False, profile=prof)
     eng.solve_relaxation(inst, opts=o(5, False), return_device=True)
-    eng.solve_relaxation(inst, opts=o(5, True), return_device=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -348,7 +521,7 @@ def run_config(name, iters):
         for k in ("k1_forward", "k2_transpose"):
             kern[k]["frac"] = kern[k]["achieved_gbs"] / peak
     out = {"config": name, "n": n, "p": p, "dtype": cd.dtype, "loss": cd.loss, "k": cd.k, "M": cd.M,
-           "lambda2": cd.lambda2, "lipschitz": L, "iterations": iters,
+           "lambda2": cd.lambda2, "lipschitz": L, "lipschitz_method": "lanczos", "iterations": iters,
            "value": iters / (ms / 1e3), "unit": "iters/s", "ms_per_iteration": ms / iters,
            "engine_path": "single_pass" if st.get("single_pass") else "two_pass",
            "x_bytes": xb, "l2_resident": xb < 100e6, "kernels": kern, "peak_gbs": peak,
@@ -360,8 +533,32 @@ def run_config(name, iters):
 
 
 # ---------------------------------------------------------------------------
-# ours
+# ours, N = 1
 # ---------------------------------------------------------------------------
+def e2e_solves(eng, cd, make_x, solves, engine):
+    """Full solves to the C2 target through the public API from host X."""
+    import torch
+    iters, secs, reps = 0, 0.0, []
+    for i in range(solves + 1):
+        warm = i == 0          # one untimed warm-up call (process-level one-time costs)
+        X = make_x()
+        inst_h = eng.ProblemInstance(X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = eng.solve_relaxation(inst_h, opts=eng.FistaOptions(
+            lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP, engine_path=engine))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if not warm:
+            iters += r.iterations
+            secs += dt
+        reps.append({"iterations": r.iterations, "seconds": dt, "rel_gap": r.gap / abs(r.primal_value),
+                     "termination": r.termination.value, "warmup": warm})
+        inst_h.release_device()
+        del inst_h
+    return (iters / secs if secs > 0 else None), reps
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -370,7 +567,7 @@ def run_ours(args):
     torch.cuda.set_device(0)
     import paper_2502_09502_b200 as eng
     eng.native.load()
-    cd = make_inputs(args.scale)
+    cd = c2_inputs(args.scale)
     inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
     t0 = time.time()
     inst.device_problem()
@@ -382,13 +579,14 @@ def run_ours(args):
         return eng.FistaOptions(lipschitz=L_C2, max_iterations=iters, gap_tolerance=1e-300,
                                 stop_on_gap=False, profile=profile, engine_path=args.engine)
 
-    # warm-up: W iterations (graph capture, caches)
+    # warm-up: W iterations with the same options as the timed run (graph
+    # capture, caches), then the profiled variant (its graphs are kept apart)
+    eng.solve_relaxation(inst, opts=fixed(W, False), return_device=True)
     eng.solve_relaxation(inst, opts=fixed(W, True), return_device=True)
     torch.cuda.synchronize()
     # timed region: exactly K iterations, CUDA events, clocks sampled
     clocks = ClockSampler(0)
     clocks.start()
-    time.sleep(0.3)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()
@@ -398,126 +596,101 @@ def run_ours(args):
     ms = start.elapsed_time(end)
     assert rep.iterations == K, rep.iterations
     value = K / (ms / 1e3)
+    launches = int(rep.stats["gpu_launches"])
     # the same K iterations again with CUDA events around every kernel inside the
     # graphs (on the engine's stream): the per-launch durations behind the
     # roofline.  The events add ~10 us of graph nodes per iteration, so the
     # headline value above comes from the un-instrumented run.
     start.record()
-    rep = eng.solve_relaxation(inst, opts=fixed(K, True), return_device=True)
+    rep_p = eng.solve_relaxation(inst, opts=fixed(K, True), return_device=True)
     end.record()
     torch.cuda.synchronize()
     ms_prof = start.elapsed_time(end)
     clk = clocks.stop()
-    assert rep.iterations == K, rep.iterations
-    st = rep.stats
+    st = rep_p.stats
     log(f"[bench] {K} its in {ms:.2f} ms -> {value:.1f} it/s; k1 {st['k1_ms'] / max(1, st['k1_count']):.4f} "
         f"ms k2 {st['k2_ms'] / max(1, st['k2_count']):.4f} ms k3 {st['k3_ms'] / max(1, st['k3_count']):.4f} ms")
-
-    # roofline of the dominant kernel (algorithmic bytes / measured launch time)
     peak, peak_src = measured_peak()
-    s = 8
     n, p = cd.n, cd.p
-    k1_avg = st["k1_ms"] / max(1, st["k1_count"])
-    k2_avg = st["k2_ms"] / max(1, st["k2_count"])
-    k3_avg = st["k3_ms"] / max(1, st["k3_count"])
     single = bool(st.get("single_pass"))
-    traffic = ncu_traffic()
     if single:
-        # KF reads X once: both gradient candidates, X^T zeta and u_t from one pass
-        kf_bytes = n * p * s + 8 * (4 * n + p)        # X, y, u_{t-1}, u_t (write), beta slice
-        dom, dom_bytes, dom_ms = "kf_fused_s", kf_bytes, k2_avg
-        others = {"kr_reduce_epilogue": {"launch_ms": k1_avg},
-                  "k3_prox_window": {"launch_ms": k3_avg}}
+        roofline = kf_roofline(st, n, p, 8, peak, peak_src, "C2/kf_fused_s")
     else:
-        k2_bytes = n * p * s + 8 * (3 * n + 5 * p)     # X, u_t, u_t-1, y, beta_t, beta_t-1, gamma, key
-        k1_bytes = n * p * s + 8 * (p + 2 * n)          # X, beta, y, u
-        dom = "k2_transpose" if st["k2_ms"] >= st["k1_ms"] else "k1_forward"
-        dom_bytes, dom_ms = (k2_bytes, k2_avg) if dom == "k2_transpose" else (k1_bytes, k1_avg)
-        others = {"k1_forward": {"launch_ms": k1_avg, "achieved_gbs": k1_bytes / (k1_avg / 1e3) / 1e9,
-                                 "frac": k1_bytes / (k1_avg / 1e3) / 1e9 / peak},
-                  "k2_transpose": {"launch_ms": k2_avg, "achieved_gbs": k2_bytes / (k2_avg / 1e3) / 1e9,
-                                   "frac": k2_bytes / (k2_avg / 1e3) / 1e9 / peak},
-                  "k3_prox_pava_envelope": {"launch_ms": k3_avg}}
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": traffic.get(dom), "algorithmic_bytes_per_launch": dom_bytes,
-                "launch_ms": dom_ms, "launch_ms_source": "CUDA events around each kernel inside the graphs, "
-                "second timed run of the same K iterations (instrumented ms/step %.4f)" % (ms_prof / K),
-                "engine": "single pass (X read once per iteration)" if single
-                else "two pass", "other_kernels": others,
-                "iteration_bytes_2pass": 2 * n * p * s,
-                "iteration_rate_vs_2pass_roofline": (2 * n * p * s) / (ms / 1e3 / K) / 1e9 / peak,
-                "note": "iteration_rate_vs_2pass_roofline > 1 is possible only because the "
-                        "single-pass engine reads X once per iteration" if single else ""}
-    # end to end through the public API with host-resident X (pinned)
-    Xpin = torch.from_numpy(cd.X).pin_memory()
-    e2e_iters, e2e_time = 0, 0.0
+        avg = lambda k: st[k + "_ms"] / max(1, st[k + "_count"])
+        k2_bytes = n * p * 8 + 8 * (3 * n + 5 * p)
+        achieved = k2_bytes / (avg("k2") / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k2_transpose", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                    "traffic": ncu_traffic("C2/k2_transpose"),
+                    "algorithmic_bytes_per_launch": k2_bytes, "launch_ms": avg("k2")}
+    roofline.update({
+        "launch_ms_source": "CUDA events around each kernel inside the graphs (engine stream), "
+                            "second run of the same K iterations (instrumented ms/step %.4f)" % (ms_prof / K),
+        "engine": "single pass (X read once per iteration)" if single else "two pass",
+        "iteration_bytes_2pass": 2 * n * p * 8,
+        "iteration_rate_vs_2pass_roofline": (2 * n * p * 8) / (ms / 1e3 / K) / 1e9 / peak,
+        "note": "iteration_rate_vs_2pass_roofline > 1 is possible only because the single-pass "
+                "engine reads X once per iteration" if single else ""})
+    # end to end through the public API with host-resident X: numpy (pageable,
+    # the drop-in call) is the headline; a pinned torch tensor is reported beside
     h2d = cd.X.nbytes + cd.y.nbytes
     d2h = cd.p * 8
-    e2e_reps = []
-    for i in range(args.e2e_solves + (1 if args.e2e_solves > 0 else 0)):
-        warm = i == 0          # one untimed warm-up call (process-level one-time costs)
-        inst_h = eng.ProblemInstance(Xpin, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = eng.solve_relaxation(inst_h, opts=eng.FistaOptions(
-            lipschitz=L_C2, gap_tolerance=1e-300, gap_tolerance_rel=REL_GAP, engine_path=args.engine))
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if not warm:
-            e2e_iters += r.iterations
-            e2e_time += dt
-        e2e_reps.append({"iterations": r.iterations, "seconds": dt, "rel_gap": r.gap / abs(r.primal_value),
-                         "termination": r.termination.value, "warmup": warm})
-        inst_h.release_device()
-        del inst_h
-    e2e = {"value": e2e_iters / e2e_time if e2e_time > 0 else None, "unit": "iters/s",
-           "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h,
-           "step": "one solve_relaxation call to relative gap 1e-6 from host (pinned) X",
-           "solves": e2e_reps}
-    log(f"[bench] e2e {e2e['value']} it/s {e2e_reps}")
-
-    cb = cpu_baseline(cd, args.cpu_iters) if not args.no_cpu else None
+    e2e_np, reps_np = e2e_solves(eng, cd, lambda: cd.X, args.e2e_solves, args.engine)
+    Xpin = torch.from_numpy(cd.X).pin_memory()
+    e2e_pin, reps_pin = e2e_solves(eng, cd, lambda: Xpin, args.e2e_solves, args.engine)
+    del Xpin
+    e2e = {"value": e2e_np, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "step": "one solve_relaxation call to relative gap 1e-6 from a host numpy X (pageable; "
+                   "staged by the engine's multi-threaded pinned ring, l0_upload_rows)",
+           "solves": reps_np, "pinned_tensor_value": e2e_pin, "pinned_tensor_solves": reps_pin}
+    log(f"[bench] e2e numpy {e2e_np} it/s, pinned {e2e_pin} it/s")
+    cb = cpu_baseline_c2(cd, args.cpu_iters) if not args.no_cpu else None
     del inst
     torch.cuda.empty_cache()
+    sections = {}
+    if args.c5_steps > 0:
+        try:
+            sections["c5"] = run_c5_single(args)
+            log(f"[bench] C5 {sections['c5']['value']:.1f} it/s")
+        except Exception as exc:   # reported, never silently dropped
+            sections["c5"] = {"error": repr(exc)}
     batched = None
     if args.c4_nodes > 0:
         try:
             batched = run_batched(args)
             log(f"[bench] C4 {batched['value']:.0f} node-it/s {batched['ms_per_iteration_split']}")
-        except Exception as exc:   # reported, never silently dropped
+        except Exception as exc:
             batched = {"error": repr(exc)}
     others = []
     for name in [c for c in args.configs.split(",") if c and c != "none"]:
         try:
             others.append(run_config(name, args.config_steps))
             log(f"[bench] {name} {others[-1]['value']:.1f} it/s {others[-1]['kernels']}")
-        except Exception as exc:   # reported, never silently dropped
+        except Exception as exc:
             others.append({"config": name, "error": repr(exc)})
     line = {"metric": METRIC,
             "value": value, "unit": "iters/s", "n_gpus": 1, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True,
-            "scaling": "strong" if args.shard == "rows" else "weak",
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
-            "config": base_config(cd, 1), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-            "gpu_launches": int(st["gpu_launches"]), "clocks": clk,
+            "config": c2_config(cd), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
             "engine_path": "single_pass" if single else "two_pass",
             "restarts": rep.restarts, "final_gap": rep.gap,
             "prox_full_passes": st.get("prox_full_passes"), "topk_fallbacks": st.get("topk_fallbacks"),
-            "batched_nodes": batched, "other_configs": others}
+            "c5_single_gpu": sections.get("c5"), "batched_nodes": batched, "other_configs": others}
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# ours, N > 1
+# ---------------------------------------------------------------------------
 def run_ours_sharded(args, world, rank, local):
-    """N > 1.  Default (--shard nodes): node sharding, the path's independent
-    units: every rank holds C2's X and runs K iterations of
-    its own branch-and-bound node (rank 0 the root, the others seeded
-    fixed-zero/fixed-one sets), no data-path collective; value = node
-    iterations of all ranks / max-over-ranks device time ("weak").
-    --shard rows: C2's rows split over the ranks with the engine's NCCL
-    all-reduce of the gradient each iteration ("strong")."""
+    """--shard rows (default): C5's rows over the ranks, each rank generating
+    its own rows in HBM; the engine all-reduces [X_r^T r | X_r^T zeta | F*]
+    and the loss over NCCL inside its CUDA graphs every iteration ("strong").
+    --shard nodes: C4's 512 nodes over the ranks, one batched call per rank on
+    its share (no collective).  value = all ranks' units / max-over-ranks
+    device time."""
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
@@ -526,47 +699,82 @@ def run_ours_sharded(args, world, rank, local):
     import paper_2502_09502_b200 as eng
     from paper_2502_09502_b200 import data
     eng.native.load()
-    cd = make_inputs(args.scale)
     K, W = args.steps, args.warmup
-    opts = lambda it: eng.FistaOptions(lipschitz=L_C2, max_iterations=it, gap_tolerance=1e-300,
-                                       stop_on_gap=False, engine_path=args.engine)
+    dev = torch.device("cuda", local)
+    red = lambda t: dist.all_reduce(t)
+    e2e = None
     if args.shard == "rows":
-        r0, r1 = shard.row_range(cd.n, world, rank)
-        inst = shard.ShardedProblem(cd.X[r0:r1], cd.y[r0:r1], eng.LossKind.SQUARED_ERROR, cd.k,
-                                    cd.M, cd.lambda2, n_global=cd.n)
-        solve = lambda it: shard.solve_relaxation_sharded(inst, opts=opts(it))
-        scaling, units_per_step, par = "strong", 1, "rows%d" % world
+        n, p = int(data.C5_N * args.c5_scale), data.C5_P
+        r0, r1 = shard.row_range(n, world, rank)
+        t0 = time.time()
+        X, y = data.c5_shard_device(r0, r1, dev, n=n, allreduce=red)
+        sp = shard.ShardedProblem(X, y.cpu().numpy(), eng.LossKind.SQUARED_ERROR, 25, 2.0, 0.1,
+                                  n_global=n, dtype="fp32")
+        L = sp.lipschitz(method="lanczos")
+        log(f"[bench] rank {rank}: rows [{r0}, {r1}) generated + L={L:.6g} in {time.time() - t0:.1f}s")
+        opts = lambda it: eng.FistaOptions(lipschitz=L, max_iterations=it, gap_tolerance=1e-300,
+                                           stop_on_gap=False)
+        solve = lambda it: shard.solve_relaxation_sharded(sp, opts=opts(it))
+        units, cfg, unit_name = 1, c5_config(n, p, world), "iters/s"
     else:
-        inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind.SQUARED_ERROR, cd.k, cd.M, cd.lambda2)
-        sets = data.random_nodes(cd.p, world, seed=1)
-        node = None if rank == 0 else eng.NodeState(fixed_one=sets[rank][1], fixed_zero=sets[rank][0])
-        solve = lambda it: eng.solve_relaxation(inst, node, opts=opts(it), return_device=True)
-        scaling, units_per_step, par = "weak", world, "nodes%d" % world
+        cd, inst, nodes, L = c4_setup(args, args.c4_nodes)
+        mine = shard.shard_nodes(nodes, world, rank)
+        my_nodes = [nodes[i] for i in mine]
+        opts = lambda it: eng.FistaOptions(lipschitz=L, max_iterations=it, stop_on_gap=False)
+        solve = lambda it: eng.solve_relaxation_batched(inst, my_nodes, opts=opts(it),
+                                                        return_device=True)[0]
+        units, unit_name = len(nodes), "node-iters/s"
+        cfg = {"workload": f"C4: {len(nodes)} node relaxations (n={cd.n}, p={cd.p} fp32) split over "
+                           f"the GPUs, one batched tcgen05 call per rank", "nodes": len(nodes),
+               "parallelism": f"nodes{world}"}
     solve(W)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
     start.record()
     rep = solve(K)
     end.record()
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
-    ms = torch.tensor([start.elapsed_time(end)], device="cuda")
+    clk = clocks.stop() if clocks else None
+    ms = torch.tensor([start.elapsed_time(end)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    launches = torch.tensor([float(rep.stats["gpu_launches"])], device="cuda")
+    launches = torch.tensor([float(rep.stats["gpu_launches"])], device=dev)
     dist.all_reduce(launches)
+    if args.shard == "rows" and args.e2e_solves > 0:
+        # end to end: this rank's rows from pinned host memory, uploaded and
+        # solved K iterations per call (H2D of X_r, y_r and D2H of beta inside)
+        Xh = X.cpu().pin_memory()
+        yh = y.cpu().numpy()
+        del sp
+        torch.cuda.empty_cache()
+        dist.barrier()
+        t0 = time.perf_counter()
+        sp2 = shard.ShardedProblem(Xh, yh, eng.LossKind.SQUARED_ERROR, 25, 2.0, 0.1,
+                                   n_global=n, dtype="fp32")
+        r2 = shard.solve_relaxation_sharded(sp2, opts=opts(K))
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": K / float(dt.item()), "unit": "iters/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4 + yh.size * 8) * world,
+               "d2h_bytes_per_step": int(p * 8) * world,
+               "step": f"per rank: its C5 rows from pinned host memory -> ShardedProblem + "
+                       f"{K}-iteration solve (max over ranks, host wall clock)"}
     if rank == 0:
-        cfg = base_config(cd, world)
-        cfg["parallelism"] = par
-        line = {"metric": METRIC,
-                "value": units_per_step * K / (ms / 1e3), "unit": "iters/s", "n_gpus": world,
+        line = {"metric": METRIC if args.shard == "rows" else
+                "node FISTA iterations/s (C4 nodes sharded over the GPUs)",
+                "value": units * K / (ms / 1e3), "unit": unit_name, "n_gpus": world,
                 "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-                "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (reference generator, seed 0)", "config": cfg,
-                "gpu_launches": int(launches.item()),
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 X / f64 arithmetic", "data": "synthetic (seeded, see config)",
+                "config": cfg, "gpu_launches": int(launches.item()), "clocks": clk, "e2e": e2e,
                 "engine_path": "single_pass" if rep.stats.get("single_pass") else "two_pass"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -584,8 +792,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", default="auto", choices=["auto", "two_pass", "single_pass"])
     ap.add_argument("--force-dist", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--shard", default="nodes", choices=["nodes", "rows"],
-                    help="N > 1: independent node relaxations per GPU (weak) or C2's rows (strong)")
+    ap.add_argument("--shard", default="rows", choices=["rows", "nodes"],
+                    help="N > 1: C5 rows over the GPUs (default) or C4 nodes over the GPUs")
+    ap.add_argument("--c5-steps", type=int, default=100, help="C5 section at N=1 (0: skip)")
+    ap.add_argument("--c5-scale", type=float, default=1.0, help="shrink C5's n (testing only)")
+    ap.add_argument("--c5-cpu-rows", type=int, default=20000)
     ap.add_argument("--c4-nodes", type=int, default=512, help="batched-node section (0: skip)")
     ap.add_argument("--c4-steps", type=int, default=100)
     ap.add_argument("--c4-scale", type=float, default=1.0)

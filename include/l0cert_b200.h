@@ -155,6 +155,16 @@ int32_t l0_problem_set_prox_record(l0_problem* prob, int32_t* d_ring, int32_t ca
  * the single-pass kernel in L0_PROBE builds) */
 int32_t l0_debug_scratch(l0_problem* prob, double* h_out, int64_t count);
 
+/* ---- ingest ------------------------------------------------------------------
+ * Copy `rows` rows of `row_bytes` from host memory (pitch h_pitch; pageable is
+ * fine, e.g. a numpy array) to device rows of pitch d_pitch, through a ring of
+ * pinned staging slots filled by `threads` host threads while the copy engine
+ * drains the previous slot.  Synchronous (returns after the data is in HBM).
+ * Replaces the host copy ProblemInstance makes of X (model.py:92) on the way
+ * to the device. */
+int32_t l0_upload_rows(void* d_dst, int64_t d_pitch, const void* h_src, int64_t h_pitch,
+                       int64_t row_bytes, int64_t rows, int32_t threads, void* stream);
+
 /* ---- hot path ----------------------------------------------------------------- */
 int32_t l0_fista_solve(l0_problem* prob, int64_t k, double M, double lambda2,
                        const l0_fista_opts* opts, const l0_node* node /* nullable */,

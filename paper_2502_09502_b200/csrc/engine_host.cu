@@ -98,7 +98,8 @@ struct Problem {
   State* h_st[2] = {nullptr, nullptr};  // pinned mirrors (double-buffered chunks)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_chunk[2] = {nullptr, nullptr};
-  Graph graph[2];
+  Graph graphs[2][2];   // [profile][double-buffer slot]: both variants stay captured
+  Graph* graph = graphs[0];
   int fused_planned = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -205,11 +206,12 @@ static uint64_t carve(Problem& P, char* base) {
 }
 
 static void destroy_graphs(Problem& P) {
-  for (auto& g : P.graph) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (auto e : g.ev) cudaEventDestroy(e);
-    g = Graph{};
-  }
+  for (auto& set : P.graphs)
+    for (auto& g : set) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      for (auto e : g.ev) cudaEventDestroy(e);
+      g = Graph{};
+    }
 }
 
 static int fused_tail(Problem& P, int mode, cudaStream_t s) {
@@ -665,6 +667,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   // ---- chunked iteration: graph replays, double-buffered state mirrors ------
   const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100)
                                         : auto_chunk(*P, o->bound_check_interval);
+  P->graph = P->graphs[o->profile ? 1 : 0];
   for (int w = 0; w < 2; ++w) {
     rc = build_graph(*P, w, G, o->profile ? 1 : 0);
     if (rc) return rc;

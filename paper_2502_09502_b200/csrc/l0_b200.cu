@@ -7,6 +7,7 @@
 #include "ops.cu"
 #include "engine_host.cu"
 #include "abi_ops.cu"
+#include "upload.cu"
 #include "tc_gemm.cu"
 #include "batch.cu"
 #include "batch_host.cu"

@@ -454,3 +454,58 @@ def make_config(name: str, scale: float = 1.0, **kw) -> ConfigData:
     """Build config ``name`` (C1, C1-literal, C2, C3, C4, C5) at ``scale``
     (scale < 1 shrinks n and p proportionally for parity tests)."""
     return CONFIGS[name](scale=scale, **kw) if kw else CONFIGS[name](scale=scale)
+
+
+# ---------------------------------------------------------------------------
+# C5 on the device (bench): AR(1) rows generated in HBM, sharded by rows
+# ---------------------------------------------------------------------------
+C5_N, C5_P, C5_BLOCK = 1_000_000, 10_000, 100_000
+
+
+def ar1_block_device(b: int, rows: int, p: int, sigma: float, device, seed: int = 0):
+    """Rows of generator block ``b`` of an AR(1) design (Toeplitz sigma^|i-j|
+    correlation, N(0, 1) marginals; the recursion of data.py:76-85) drawn on
+    the device from torch's Philox generator seeded (seed, b), fp32, as a
+    (p, rows) column-major block.  Blocks are independent of how rows are
+    later sharded, so every world size sees the same matrix."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed((seed << 32) + b)
+    W = torch.randn((p, rows), generator=g, device=device, dtype=torch.float32)
+    if sigma != 0.0:
+        c = math.sqrt(1.0 - sigma * sigma)
+        for j in range(1, p):
+            W[j].mul_(c).add_(W[j - 1], alpha=sigma)
+    return W
+
+
+def c5_shard_device(r0: int, r1: int, device, n: int = C5_N, p: int = C5_P, k_true: int = 25,
+                    sigma: float = 0.5, snr: float = 5.0, block: int = C5_BLOCK, allreduce=None):
+    """Rows [r0, r1) of C5 (n x p fp32, Toeplitz 0.5, k=25 evenly spaced ones,
+    SNR 5) built on ``device``: X (rows x p, row-major fp32) and y (fp64).
+    The noise scale needs ||X beta*|| over all n rows: ``allreduce`` sums a
+    1-element CUDA tensor over the ranks (None on one rank)."""
+    import torch
+    rows = r1 - r0
+    X = torch.empty((rows, p), dtype=torch.float32, device=device)
+    for b in range(r0 // block, (r1 - 1) // block + 1):
+        b0, b1 = b * block, min(n, (b + 1) * block)
+        lo, hi = max(r0, b0), min(r1, b1)
+        W = ar1_block_device(b, b1 - b0, p, sigma, device)
+        X[lo - r0:hi - r0].copy_(W[:, lo - b0:hi - b0].T)
+        del W
+    support = torch.from_numpy(true_support(p, k_true)).to(device)
+    sig = X.index_select(1, support).to(torch.float64).sum(1)        # X beta* (beta* = 1 on S)
+    sq = (sig * sig).sum().reshape(1)
+    if allreduce is not None:
+        allreduce(sq)
+    std = math.sqrt(math.sqrt(float(sq.item())) / snr)                # data.py:97-99 "variance"
+    eps = torch.empty(rows, dtype=torch.float64, device=device)
+    for b in range(r0 // block, (r1 - 1) // block + 1):
+        b0, b1 = b * block, min(n, (b + 1) * block)
+        lo, hi = max(r0, b0), min(r1, b1)
+        g = torch.Generator(device=device)
+        g.manual_seed((1 << 40) + b)
+        e = torch.randn(b1 - b0, generator=g, device=device, dtype=torch.float64) * std
+        eps[lo - r0:hi - r0] = e[lo - b0:hi - b0]
+    return X, sig + eps

@@ -177,24 +177,32 @@ def solve_relaxation_sharded(problem: ShardedProblem, node=None, warm_start=None
     return solve_relaxation(problem.instance, node=node, warm_start=warm_start, opts=opts)
 
 
-def solve_nodes_sharded(instance, nodes: Sequence, opts=None, group=None):
+def solve_nodes_sharded(instance, nodes: Sequence, opts=None, group=None, batched: bool = True):
     """Node sharding: this rank solves its round-robin share of ``nodes`` on
-    the replicated X; returns {node index: report} gathered on every rank."""
+    the replicated X -- as ONE batched call (``solve_relaxation_batched``: the
+    share's X passes run as tcgen05 contractions), or node by node with
+    ``batched=False``.  Returns {node index: report} on this rank plus, gathered
+    from every rank, {node index: (primal, dual, gap, iterations, restarts,
+    termination)} as the second element."""
     import torch.distributed as dist
-    from .fista import solve_relaxation
+    from .fista import solve_relaxation, solve_relaxation_batched
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    idx = shard_nodes(nodes, world, rank)
     mine = {}
-    for i in shard_nodes(nodes, world, rank):
-        rep = solve_relaxation(instance, node=nodes[i], opts=opts)
-        mine[i] = rep
+    if idx and batched:
+        reps = solve_relaxation_batched(instance, [nodes[i] for i in idx], opts=opts)
+        mine = dict(zip(idx, reps))
+    else:
+        for i in idx:
+            mine[i] = solve_relaxation(instance, node=nodes[i], opts=opts)
+    summary = {i: (r.primal_value, r.dual_bound, r.gap, r.iterations, r.restarts,
+                   r.termination.value) for i, r in mine.items()}
     if world == 1:
-        return mine
+        return mine, summary
     gathered = [None] * world
-    dist.all_gather_object(gathered, {i: (r.primal_value, r.dual_bound, r.gap, r.iterations,
-                                          r.restarts, r.termination.value)
-                                      for i, r in mine.items()}, group=group)
+    dist.all_gather_object(gathered, summary, group=group)
     out = {}
     for part in gathered:
         out.update(part)
-    return out
+    return mine, out

@@ -20,6 +20,7 @@ UnsupportedOperationError.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import weakref
 from dataclasses import dataclass, field
@@ -102,6 +103,23 @@ def _check_labels(loss: LossKind, y: np.ndarray) -> None:
             raise InvalidInputError("multinomial labels must be one-hot rows")
 
 
+def _padded_finite(Xt, lib) -> bool:
+    """All n x stride(0) elements under a strided device view are finite
+    (the engine reads the padding columns with beta = 0 there)."""
+    import torch
+    from . import _device
+    if Xt.stride(0) == Xt.shape[1]:
+        return True
+    full = Xt.as_strided((Xt.shape[0], Xt.stride(0)), (Xt.stride(0), 1))
+    buf, nb = _device.ops_workspace(1)
+    ok = ctypes.c_int32()
+    code = native.F64 if Xt.dtype == torch.float64 else native.F32
+    native.check(lib.l0_all_finite(full.data_ptr(), code, full.shape[0], full.shape[1],
+                                   full.stride(0), ctypes.byref(ok), buf.data_ptr(), nb,
+                                   _device.stream_handle()))
+    return bool(ok.value)
+
+
 class DeviceProblem:
     """X, y resident in HBM plus the engine's problem handle and workspace."""
 
@@ -118,7 +136,23 @@ class DeviceProblem:
         n, p = Xt.shape
         align = 32
         ld = ((p + align - 1) // align) * align
-        if ld == p and Xt.dtype == tdt and Xt.is_contiguous():
+        if not isinstance(X, torch.Tensor) and Xt.dtype == tdt:
+            # pageable host array: multi-threaded pinned staging overlapped with the DMA
+            es = Xt.element_size()
+            Xd = (torch.empty if ld == p else torch.zeros)((n, ld), dtype=tdt, device=dev)
+            native.check(lib.l0_upload_rows(Xd.data_ptr(), ld * es, Xt.data_ptr(), p * es, p * es,
+                                            n, min(16, os.cpu_count() or 8),
+                                            _device.stream_handle()))
+        elif (Xt.device.type == "cuda" and Xt.dtype == tdt and Xt.dim() == 2 and Xt.stride(1) == 1
+              and Xt.stride(0) >= p and Xt.stride(0) % align == 0 and n > 0
+              and (Xt.storage_offset() + n * Xt.stride(0)) * Xt.element_size()
+              <= Xt.untyped_storage().nbytes()
+              and _padded_finite(Xt, lib)):
+            # a device view whose rows already carry finite padding (e.g. the
+            # [:, :p] view of an (n, ld) buffer): used in place, no copy
+            ld = int(Xt.stride(0))
+            Xd = Xt.as_strided((n, ld), (ld, 1))
+        elif ld == p and Xt.dtype == tdt and Xt.is_contiguous():
             Xd = Xt.to(dev, non_blocking=Xt.is_pinned()) if Xt.device.type != "cuda" else Xt
         else:
             Xd = torch.zeros((n, ld), dtype=tdt, device=dev)

@@ -73,6 +73,7 @@ _PROTOS = {
                                c_vp, c_vp]),
     "l0_debug_probe": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
     "l0_problem_set_prox_record": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
+    "l0_upload_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp]),
     "l0_debug_scratch": (c_i32, [c_vp, c_vp, c_i64]),
     "l0_matvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "l0_rmatvec": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -76,13 +76,22 @@ def test_prox_permutation_pool_values(engine, oracle, p):
         out, perm, gpool = prox_engine(mu, rho, k, M, 0, want_perm=True)
         if k < p:
             assert np.array_equal(perm.cpu().numpy(), order), "sorted permutation differs"
-            # pools may only differ on an exact value tie (then the values agree)
-            pool_mismatch += (gpool if gpool[0] >= 0 else None) != pool
+            # pools may only differ on an exact value tie of the pool value and
+            # the boundary singleton (then the outputs agree); report the margin
+            gp = tuple(int(v) for v in gpool) if gpool[0] >= 0 else None
+            if gp != pool:
+                from tests.test_gpu_prox_trajectory import _pool_margin
+                keys = np.abs(mu)[order]
+                ref_pool, other = (pool, gp) if pool is not None else (gp, pool)
+                margin = _pool_margin(keys, ref_pool, other, k, rho, M)
+                print(f"p={p} trial={trial}: pool {gp} vs oracle {pool}, tie margin {margin:.3e}")
+                assert margin <= 1e-12, (gp, pool, margin)
+                pool_mismatch += 1
         _close(out.cpu().numpy(), ref)
         # g-mode through the Moreau identity
         gam = mu / rho
         _close(engine.prox_g(gam, rho, k, M), oracle.prox_g(gam, rho, k, M))
-    assert pool_mismatch <= 1
+    assert pool_mismatch <= 2      # each one an exact tie (margin checked above)
 
 
 def test_prox_spec_examples(engine):

@@ -140,7 +140,9 @@ def test_c1_prox_identity(engine, oracle, monkeypatch, full_sort):
         monkeypatch.setenv("L0_FULL_SORT", full_sort)
     cd = mydata.make_config("C1")
     L = 2.0 * 1.01 * _lmax(cd.X)
-    _, recs = _run(engine, oracle, cd, L, "fp64", iters=60)
+    # C1 reaches the round-off plateau early (relative gap ~1e-15 by t ~ 40),
+    # where restart decisions compare ulp-equal objectives: stay before it
+    _, recs = _run(engine, oracle, cd, L, "fp64", iters=30)
     paths = set(int(x) for x in recs[:, 6] if x >= 0)
     assert paths <= ({0, 1} if full_sort == "auto" else {2})
 
