@@ -665,8 +665,17 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   }
 
   // ---- chunked iteration: graph replays, double-buffered state mirrors ------
-  const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100)
-                                        : auto_chunk(*P, o->bound_check_interval);
+  // iterations that can ever run: max_iterations plus one bound-only pass
+  // (fista.py:208-209); no chunk is launched past them, and the chunk size is
+  // trimmed so that they tile into whole chunks (no trailing empty launches)
+  const int64_t need = o->max_iterations + 1;
+  int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100)
+                                  : auto_chunk(*P, o->bound_check_interval);
+  if (o->chunk_iterations <= 0 && need < (int64_t)G * 64) {
+    const int64_t nch = (need + G - 1) / G;
+    G = (int)std::max<int64_t>(1, (need + nch - 1) / nch);
+  }
+  int64_t launched_its = 0;
   P->graph = P->graphs[o->profile ? 1 : 0];
   for (int w = 0; w < 2; ++w) {
     rc = build_graph(*P, w, G, o->profile ? 1 : 0);
@@ -683,10 +692,11 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   auto launch_chunk = [&](int w) -> int {
     L0_CUDA_TRY(cudaGraphLaunch(P->graph[w].exec, s));
     L0_CUDA_TRY(cudaEventRecord(P->ev_chunk[w], s));
+    launched_its += G;
     return ST_OK;
   };
   // keep two chunks in flight
-  for (int w = 0; w < 2; ++w) {
+  for (int w = 0; w < 2 && launched_its < need; ++w) {
     rc = launch_chunk(w);
     if (rc) return rc;
     ++inflight;
@@ -761,6 +771,9 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
       }
       stop_sent = true;
     }
+    // nothing left that could run (the in-flight chunk finishes the solve);
+    // with nothing in flight a chunk is launched anyway (never strand a solve)
+    if (launched_its >= need && !stop_sent && inflight > 0) continue;
     if (P->graph[w].full_sort != a.prox_full_sort) {
       rc = build_graph(*P, w, G, o->profile ? 1 : 0);
       if (rc) return rc;
