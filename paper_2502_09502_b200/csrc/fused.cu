@@ -28,6 +28,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "control.cuh"
 #include "engine.cuh"
@@ -116,6 +117,7 @@ template <> struct FzVec<double> {
   using T = double2;
   static constexpr int N = 2;
   __device__ __forceinline__ static void widen(const T& v, double* o) { o[0] = v.x; o[1] = v.y; }
+  __device__ __forceinline__ static void widen_s(const T& v, double* o) { widen(v, o); }
 };
 template <> struct FzVec<float> {
   using T = float4;
@@ -123,8 +125,24 @@ template <> struct FzVec<float> {
   __device__ __forceinline__ static void widen(const T& v, double* o) {
     o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
   }
+  // x * 2^-896 exactly, for every finite x (normals, zeros and subnormals):
+  // the fp32 exponent field lands in the low 8 bits of the fp64 one, so the
+  // fp64 bias 1023 reads the fp32 bias 127 as 127 + 896; an fp32 subnormal
+  // becomes the fp64 subnormal of the same mantissa.  Three integer ops
+  // (shift, mask, shift) instead of an F2F.F64.F32 on the XU pipe.  Paired
+  // with the other factor scaled by 2^896, fma(x', b', acc) == fma(x, b, acc)
+  // bit for bit as long as b * 2^896 is finite.
+  __device__ __forceinline__ static double rebias(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = (uint32_t)((int32_t)u >> 3) & 0x8fffffffu;
+    return __hiloint2double((int)hi, (int)(u << 29));
+  }
+  __device__ __forceinline__ static void widen_s(const T& v, double* o) {
+    o[0] = rebias(v.x); o[1] = rebias(v.y); o[2] = rebias(v.z); o[3] = rebias(v.w);
+  }
 };
 
+constexpr double kRebias = 0x1p896;                // scale paired with FzVec<float>::rebias
 constexpr int kFzFwdWarps = 4;                      // forward warps
 constexpr int kFzTrWarps = 8;                       // accumulate warps
 constexpr int kFzTr = kFzTrWarps * 32;              // 256 accumulate threads
@@ -402,48 +420,68 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
         const int64_t col = c0 + qc + (j * 32 + lane) * VE + e;
         bq[j * VE + e] = col < a.p ? bsrc[col] : 0.0;
       }
-    int buf = 0, q = 0;
-    uint32_t ph = 0;
-    for (int k = 0; k < mytiles; ++k) {
-      const int rows = tile_rows(k);
-      if (tid == 0) FZ_STAMP(a, k, 0);
-      mbar_wait(&sh.full[buf], ph);
-      if (tid == 0) FZ_STAMP(a, k, 1);
-      const TX* tl = tiles + (int64_t)buf * R * W;
-      double d[R];
+    // fp32 X: widen by integer rebias against beta * 2^896 (all of this
+    // warp's beta finite after scaling; |beta| <= M keeps that true unless M
+    // is within 2^-896 of the fp64 range)
+    bool fint = sizeof(TX) == 4 && (a.fz_widen & 1);
+    if (fint) {
+      bool ok = true;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double d0 = 0.0, d1 = 0.0;
-        if (r < rows) {
+      for (int i = 0; i < FV * VE; ++i) ok = ok && isfinite(bq[i] * kRebias);
+      fint = __all_sync(0xffffffffu, ok);
+      if (fint)
 #pragma unroll
-          for (int j = 0; j < FV; ++j) {   // columns >= wvalid are zero in every stage
-            const int col = qc + (j * 32 + lane) * VE;
-            double x[VE];
-            V::widen(*reinterpret_cast<const typename V::T*>(tl + r * W + col), x);
+        for (int i = 0; i < FV * VE; ++i) bq[i] *= kRebias;
+    }
+    auto fwd_loop = [&](auto INT) {
+      constexpr bool kInt = decltype(INT)::value;
+      int buf = 0, q = 0;
+      uint32_t ph = 0;
+      for (int k = 0; k < mytiles; ++k) {
+        const int rows = tile_rows(k);
+        if (tid == 0) FZ_STAMP(a, k, 0);
+        mbar_wait(&sh.full[buf], ph);
+        if (tid == 0) FZ_STAMP(a, k, 1);
+        const TX* tl = tiles + (int64_t)buf * R * W;
+        double d[R];
 #pragma unroll
-            for (int e = 0; e < VE; ++e) {
-              if (((j * VE + e) & 1) == 0) d0 = fma(x[e], bq[j * VE + e], d0);
-              else d1 = fma(x[e], bq[j * VE + e], d1);
+        for (int r = 0; r < R; ++r) {
+          double d0 = 0.0, d1 = 0.0;
+          if (r < rows) {
+#pragma unroll
+            for (int j = 0; j < FV; ++j) {   // columns >= wvalid are zero in every stage
+              const int col = qc + (j * 32 + lane) * VE;
+              double x[VE];
+              const typename V::T xv = *reinterpret_cast<const typename V::T*>(tl + r * W + col);
+              if (kInt) V::widen_s(xv, x);
+              else V::widen(xv, x);
+#pragma unroll
+              for (int e = 0; e < VE; ++e) {
+                if (((j * VE + e) & 1) == 0) d0 = fma(x[e], bq[j * VE + e], d0);
+                else d1 = fma(x[e], bq[j * VE + e], d1);
+              }
             }
           }
+          d[r] = d0 + d1;
         }
-        d[r] = d0 + d1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < R; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+        if (lane < cs) {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r < rows)
+              st_async_f64(part + (((size_t)q * cs + crank) * kFzFwdWarps + warp) * R + r, &sh.xb[q],
+                           (uint32_t)lane, d[r]);
+        }
+        if (tid == 0) FZ_STAMP(a, k, 2);
+        if (++buf == S) { buf = 0; ph ^= 1u; }
+        if (++q == NS) q = 0;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int r = 0; r < R; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
-      if (lane < cs) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (r < rows)
-            st_async_f64(part + (((size_t)q * cs + crank) * kFzFwdWarps + warp) * R + r, &sh.xb[q],
-                         (uint32_t)lane, d[r]);
-      }
-      if (tid == 0) FZ_STAMP(a, k, 2);
-      if (++buf == S) { buf = 0; ph ^= 1u; }
-      if (++q == NS) q = 0;
-    }
+    };
+    if (fint) fwd_loop(std::true_type{});
+    else fwd_loop(std::false_type{});
   } else if (warp < kFsGatherWarp + G) {
     // ===================== gather =====================
     const int gw = warp - kFsGatherWarp;
@@ -538,7 +576,19 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       mbar_wait(&sh.rfull[buf], ph);
       mbar_wait(&sh.full[buf], ph);
       const TX* tl = tiles + (int64_t)buf * R * W + lt * VE;
-      if (rows == R) {
+      // fp32 X: integer-rebias widening against residuals * 2^896 when they
+      // all stay finite after scaling (warp-uniform: every lane reads them)
+      bool aint = false;
+      if (sizeof(TX) == 4 && (a.fz_widen & 2) && rows == R) {
+        aint = true;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          aint = aint && isfinite(sh.rr[buf][0][r] * kRebias) && isfinite(sh.rr[buf][1][r] * kRebias) &&
+                 (!want_z || isfinite(sh.rr[buf][2][r] * kRebias));
+      }
+      auto acc_full = [&](auto INT) {
+        constexpr bool kInt = decltype(INT)::value;
+        const double sc = kInt ? kRebias : 1.0;
         // rows in pairs: a pair's loads are issued before its FMAs
         constexpr int RP = R >= 2 ? 2 : 1;
 #pragma unroll
@@ -552,12 +602,13 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
 #pragma unroll
           for (int h = 0; h < RP; ++h) {
             const int r = r0 + h;
-            const double rR = sh.rr[buf][0][r], rN = sh.rr[buf][1][r];
-            const double rZ = want_z ? sh.rr[buf][2][r] : 0.0;
+            const double rR = sh.rr[buf][0][r] * sc, rN = sh.rr[buf][1][r] * sc;
+            const double rZ = want_z ? sh.rr[buf][2][r] * sc : 0.0;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               double x[VE];
-              V::widen(xv[h][v], x);
+              if (kInt) V::widen_s(xv[h][v], x);
+              else V::widen(xv[h][v], x);
 #pragma unroll
               for (int e = 0; e < VE; ++e) {
                 accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
@@ -570,6 +621,11 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
             }
           }
         }
+      };
+      if (aint) {
+        acc_full(std::true_type{});
+      } else if (rows == R) {
+        acc_full(std::false_type{});
       } else {
         // the last, partial tile of the grid: rows past n hold stale data
         for (int r = 0; r < rows; ++r) {
@@ -757,6 +813,9 @@ int fused_plan(EngineArgs& a, int sms) {
     if (getenv("L0_FZ_S")) S = std::min(S, atoi(getenv("L0_FZ_S")));
     if (S < 2) continue;
     a.fz_slots = 2 * S;
+    // fp32 X: widen by integer rebias (bit 0 forward warps, bit 1 accumulate
+    // warps) instead of F2F on the XU pipe; L0_FZ_WIDEN overrides
+    a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : 3;
     a.fz_cs = cs;
     a.fz_w = W;
     a.fz_nv = nv;
