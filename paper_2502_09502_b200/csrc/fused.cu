@@ -159,7 +159,8 @@ __device__ __forceinline__ double gtimer() {
 #define FZ_STAMP(a, slotk, which)                                                           \
   do {                                                                                     \
     const int _c = (blockIdx.x == 0) ? 0 : ((int)blockIdx.x == a.fz_cs - 1 ? 1 : -1);     \
-    if (_c >= 0 && (slotk) < 1000) a.scratch[(_c * 1000 + (slotk)) * 6 + (which)] = gtimer(); \
+    if (_c >= 0 && (slotk) < 1000 && (_c * 1000 + (slotk)) * 6 + 6 <= a.pv)                 \
+      a.scratch[(_c * 1000 + (slotk)) * 6 + (which)] = gtimer();                            \
   } while (0)
 #else
 #define FZ_STAMP(a, slotk, which) do { } while (0)
@@ -500,53 +501,65 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
         for (int j = lane + 32; j < np; j += 32) v += part[((size_t)q * np + j) * R + r];
         us[r] = v;
       }
+      // butterfly that halves the live rows each round while more than one
+      // is left: afterwards every lane of the group lane / (32 / R) holds the
+      // cluster total u of that row (2R - 2 + 5 - log2 R shuffles, not 5R)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+      for (int o = 16; o > 0; o >>= 1) {
+        const int nl = (R * o / 16) > 1 ? R * o / 16 : 1;   // live rows before this round
+        if (nl > 1) {
+          const bool up = (lane & o) != 0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) us[r] += __shfl_xor_sync(0xffffffffu, us[r], o);
+          for (int i = 0; i < nl / 2; ++i) {
+            const double keep = up ? us[i + nl / 2] : us[i];
+            const double send = up ? us[i] : us[i + nl / 2];
+            us[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        } else {
+          us[0] += __shfl_xor_sync(0xffffffffu, us[0], o);
+        }
+      }
       __syncwarp();
       if (lane == 0 && k + NS < mytiles) mbar_arrive_expect(&sh.xb[q], slot_bytes(k + NS));
-      if (lane < R) {
-        const int r = lane;
-        double u = us[0];
-#pragma unroll
-        for (int i = 1; i < R; ++i)
-          if (r == i) u = us[i];
-        double gR = 0.0, gN = 0.0, gZ = 0.0;
-        if (r < rows) {
-          const int64_t row = tile_of(k) * R + r;
-          double yi, up;
-          if (side(k)) {
-            yi = sh.sy[buf][r];
-            up = (mode == MODE_ITER) ? sh.su[buf][r] : u;
-          } else {
-            yi = a.y[row];
-            up = (mode == MODE_ITER) ? uprev[row] : u;
-          }
-          const double dlt = dsub(u, up);
-          const double ugR = dadd(u, dmul(cR, dlt));   // X gamma for the two momenta (fista.py:161-162)
-          const double ugN = dadd(u, dmul(cN, dlt));
-          if (!isfinite(ugR)) gbad_R = 1;
-          if (!isfinite(ugN)) gbad_N = 1;
-          gR = loss_grad(a.loss, ugR, yi);
-          gN = loss_grad(a.loss, ugN, yi);
-          const double z = -loss_grad(a.loss, u, yi);     // zeta_t = -grad F(u_t) (fista.py:152)
-          gZ = z;
-          if (crank == 0) {
-            if (mode == MODE_ITER) {
-              a.u[ring(t) * n + row] = u;
-            } else {
-              a.u[row] = u;
-              a.u[2 * n + row] = u;
-            }
-            if (!isfinite(u)) bad = 1;
-            loss_acc += loss_term(a.loss, u, yi);
-            if (want_z) conj_accumulate(a.loss, z, yi, f_acc);
-          }
+      // four lanes per row, one loss evaluation each (the logistic ones are
+      // exp / log1p chains; spreading them over lanes cuts the gather's
+      // issue slots, which it shares with the forward and accumulate warps):
+      //   f = 0: r_R = grad F(u + cR dlt)   f = 1: r_N = grad F(u + cN dlt)
+      //   f = 2: zeta = -grad F(u) (+ F*(-zeta) terms)   f = 3: F(u), u out
+      constexpr int GL = 32 / R;
+      const int r = lane / GL, f = lane % GL;
+      if (f < 4 && r < rows) {
+        const double u = us[0];
+        const int64_t row = tile_of(k) * R + r;
+        double yi, up;
+        if (side(k)) {
+          yi = sh.sy[buf][r];
+          up = (mode == MODE_ITER) ? sh.su[buf][r] : u;
+        } else {
+          yi = a.y[row];
+          up = (mode == MODE_ITER) ? uprev[row] : u;
         }
-        sh.rr[buf][0][r] = gR;
-        sh.rr[buf][1][r] = gN;
-        sh.rr[buf][2][r] = gZ;
+        if (f < 3) {
+          const double dlt = dsub(u, up);
+          // X gamma for the two momenta (fista.py:161-162); zeta_t = -grad F(u_t) (fista.py:152)
+          const double arg = f == 0 ? dadd(u, dmul(cR, dlt)) : (f == 1 ? dadd(u, dmul(cN, dlt)) : u);
+          if (f == 0 && !isfinite(arg)) gbad_R = 1;
+          if (f == 1 && !isfinite(arg)) gbad_N = 1;
+          const double g = loss_grad(a.loss, arg, yi);
+          sh.rr[buf][f][r] = f == 2 ? -g : g;
+          if (f == 2 && crank == 0 && want_z) conj_accumulate(a.loss, -g, yi, f_acc);
+        } else if (crank == 0) {
+          if (mode == MODE_ITER) {
+            a.u[ring(t) * n + row] = u;
+          } else {
+            a.u[row] = u;
+            a.u[2 * n + row] = u;
+          }
+          if (!isfinite(u)) bad = 1;
+          loss_acc += loss_term(a.loss, u, yi);
+        }
+      } else if (f < 4 && f < 3) {
+        sh.rr[buf][f][r] = 0.0;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.rfull[buf]);
