@@ -80,7 +80,8 @@ struct EngineArgs {
   int fz_cs, fz_ncl, fz_nv, fz_rows;   // cluster size, clusters, vectors/thread, rows/tile
   int fz_stages;     // shared-memory tile ring depth
   int fz_slots;      // partial-slot ring depth
-  int fz_widen;      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
+  int fz_widen;
+  uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)
   int64_t fz_tiles;  // row tiles
   double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta)

@@ -50,14 +50,19 @@ __device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+// The waits carry a suspend-time hint: a warp whose phase is not complete
+// sleeps until the phase completes (or the hint expires) instead of retrying
+// every ~50 cycles -- ncu on C5 counted ~150M retries per launch (accumulate
+// warps on rfull, producer on empty, gather on the partial slots), issue slots
+// taken from the warps doing the work on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase, uint32_t ns) {
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(saddr(bar)), "r"(phase)
+        : "r"(saddr(bar)), "r"(phase), "r"(ns)
         : "memory");
   }
 }
@@ -65,14 +70,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // complete_tx of a remote st.async is a release at cluster scope, so the wait
 // acquires at cluster scope (one L1 invalidation per completed wait; measured
 // free next to the CTA-scope form on C2).
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase, uint32_t ns) {
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(saddr(bar)), "r"(phase)
+        : "r"(saddr(bar)), "r"(phase), "r"(ns)
         : "memory");
   }
 }
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       for (int k = 0; k < mytiles; ++k) {
         const int rows = tile_rows(k);
         if (tid == 0) FZ_STAMP(a, k, 0);
-        mbar_wait(&sh.full[buf], ph);
+        mbar_wait(&sh.full[buf], ph, a.fz_sleep);
         if (tid == 0) FZ_STAMP(a, k, 1);
         const TX* tl = tiles + (int64_t)buf * R * W;
         double d[R];
@@ -491,8 +496,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       const int buf = k % S, q = k % NS;
       const uint32_t ph = (uint32_t)((k / S) & 1), qph = (uint32_t)((k / NS) & 1);
       const int rows = tile_rows(k);
-      mbar_wait_cluster(&sh.xb[q], qph);
-      mbar_wait(&sh.full[buf], ph);            // y / u_{t-1} of the stage
+      mbar_wait_cluster(&sh.xb[q], qph, a.fz_sleep);
+      mbar_wait(&sh.full[buf], ph, a.fz_sleep);            // y / u_{t-1} of the stage
       if (lane == 0) FZ_STAMP(a, k, 3);
       double us[R];
 #pragma unroll
@@ -570,7 +575,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       int buf = 0;
       uint32_t ph = 0;
       for (int k = 0; k + S < mytiles; ++k) {
-        mbar_wait(&sh.empty[buf], ph);
+        mbar_wait(&sh.empty[buf], ph, a.fz_sleep);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(k + S, buf);
         if (lane == 0) FZ_STAMP(a, k, 5);
@@ -586,8 +591,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
     uint32_t ph = 0;
     for (int k = 0; k < mytiles; ++k) {
       const int rows = tile_rows(k);
-      mbar_wait(&sh.rfull[buf], ph);
-      mbar_wait(&sh.full[buf], ph);
+      mbar_wait(&sh.rfull[buf], ph, a.fz_sleep);
+      mbar_wait(&sh.full[buf], ph, a.fz_sleep);
       const TX* tl = tiles + (int64_t)buf * R * W + lt * VE;
       // fp32 X: integer-rebias widening against residuals * 2^896 when they
       // all stay finite after scaling (warp-uniform: every lane reads them)
@@ -830,6 +835,8 @@ int fused_plan(EngineArgs& a, int sms) {
     // warps) instead of F2F on the XU pipe; L0_FZ_WIDEN overrides
     a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : 3;
     a.fz_cs = cs;
+    // suspend-time hint of the role waits (ns); L0_FZ_SLEEP overrides
+    a.fz_sleep = getenv("L0_FZ_SLEEP") ? (uint32_t)atoi(getenv("L0_FZ_SLEEP")) : 1000u;
     a.fz_w = W;
     a.fz_nv = nv;
     a.fz_rows = R;
