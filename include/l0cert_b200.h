@@ -14,9 +14,12 @@
  *   l0_g_value            perspective.py:114-132   g_value
  *   l0_g_conjugate        perspective.py:143-159   g_conjugate
  *   l0_safe_lower_bound   perspective.py:162-190   safe_lower_bound
+ *   l0_safe_lower_bound_batched  perspective.py:162-190, once per node of a
+ *                                branch-and-bound batch (SPEC.md:330 bounding)
  *   l0_loss_value         model.py:159-181 / :208-218  loss_value, loss_gradient
  *   l0_loss_conjugate     model.py:226-280          loss_conjugate_at_neg
  *   l0_power_iteration    model.py:283-306          _power_iteration_lambda_max
+ *   l0_standardize_stats / l0_standardize_apply  data.py:224-242  standardize
  *   l0_matvec/rmatvec     the numpy X @ v / X.T @ r call sites fista.py:141,156,162,165,209
  *
  * Conventions
@@ -180,6 +183,24 @@ int32_t l0_power_iteration(l0_problem* prob, const double* d_v0, double tol, int
 int32_t l0_safe_lower_bound(l0_problem* prob, const double* d_beta, int64_t k_free, double M,
                             double lambda2, const uint8_t* d_node_class /* nullable */,
                             double* h_out, void* stream);
+/* The same bound for nb nodes in one call (fp64 throughout): d_betas is nb x p
+ * (node-major), h_k_free[j] the free budget of node j, d_node_class nb x p
+ * (node-major, nullable: every coordinate free), h_out[nb] the bounds (-inf
+ * where F*(-zeta) is +inf).  Each X tile is read once per pass for all nodes.
+ * Workspace (device, caller-owned) from l0_safe_lower_bound_batched_workspace. */
+int32_t l0_safe_lower_bound_batched_workspace(l0_problem* prob, int64_t nb, uint64_t* bytes);
+int32_t l0_safe_lower_bound_batched(l0_problem* prob, const double* d_betas, int64_t nb,
+                                    const int64_t* h_k_free, double M, double lambda2,
+                                    const uint8_t* d_node_class /* nullable */, double* h_out,
+                                    void* d_ws, uint64_t ws_bytes, void* stream);
+
+/* ---- instance ingest (data.py:224-242 standardize), bit-identical to numpy ---- */
+/* d_X row-major fp64 (n x ld); per-column mean, centred norm and max |x| (p each) */
+int32_t l0_standardize_stats(const double* d_X, int64_t n, int64_t p, int64_t ld, double* d_mean,
+                             double* d_norm, double* d_scale, void* stream);
+/* d_out (n x m, row-major) = (X[:, kept] - mean[kept]) / norm[kept] */
+int32_t l0_standardize_apply(const double* d_X, int64_t n, int64_t ld, const int64_t* d_kept, int64_t m,
+                             const double* d_mean, const double* d_norm, double* d_out, void* stream);
 
 int32_t l0_ops_workspace_bytes(int64_t len, uint64_t* bytes);
 /* g_mode=0: out = prox_{rho g*}(in) (prox_gstar[_node]); g_mode=1: out =

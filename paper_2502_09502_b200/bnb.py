@@ -40,7 +40,7 @@ import numpy as np
 from .errors import InfeasibleNodeError, UnsupportedOperationError
 from .fista import FistaOptions, Termination, solve_relaxation_batched
 from .model import LossKind, NodeState, ProblemInstance, is_solver_grade, lipschitz_constant
-from .perspective import safe_lower_bound
+from .perspective import safe_lower_bound, safe_lower_bound_batched
 
 __all__ = ["BnBOptions", "Certificate", "CertificateStatus", "beam_search_incumbent",
            "select_branching_variable", "certify"]
@@ -318,12 +318,14 @@ def certify(instance: ProblemInstance, opts: Optional[BnBOptions] = None) -> Cer
         nodes += [nodes[-1]] * (max(opts.batch_size, 1) - len(nodes))
         reps = solve_relaxation_batched(instance, nodes, opts=ropts)[:len(batch)]
         explored += len(batch)
-        for (pbound, node), rep in zip(batch, reps):
-            # the certificate uses the fp64 Fenchel bound at the node's final
-            # iterate (two fp64 X passes, perspective.py:162-190): the batched
-            # engine's own bound carries 3xTF32 rounding and only steers its
-            # stopping tests
-            safe = safe_lower_bound(instance, rep.beta, node)
+        # the certificate uses the fp64 Fenchel bound at each node's final
+        # iterate (perspective.py:162-190), all nodes of the batch in one
+        # engine call (two fp64 multi-right-hand-side X passes): the batched
+        # engine's own bound carries 3xTF32 rounding and only steers its
+        # stopping tests
+        safes = safe_lower_bound_batched(instance, np.stack([rep.beta for rep in reps]),
+                                         [node for _, node in batch])
+        for (pbound, node), rep, safe in zip(batch, reps, safes):
             bound = max(pbound, safe) if math.isfinite(safe) else pbound
             entry = {"depth": node.depth, "fixed_one": node.fixed_one, "fixed_zero": node.fixed_zero,
                      "bound": bound, "termination": rep.termination.value}

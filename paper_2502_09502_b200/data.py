@@ -133,22 +133,31 @@ def standardize(X):
     except ImportError:  # pragma: no cover
         on_gpu = False
     if on_gpu:
-        Xd = X.to(torch.float64)
-        if Xd.ndim != 2 or Xd.shape[0] < 2:
+        # hand-written kernels (csrc/standardize.cu), bit-identical to the
+        # numpy branch below: sequential column sums over rows, as numpy
+        # reduces a C-contiguous matrix over axis 0
+        import ctypes
+        from . import _device, native
+        if X.ndim != 2 or X.shape[0] < 2:
             raise InvalidInputError("standardize needs a 2-d matrix with n >= 2")
-        means = Xd.mean(dim=0)
-        cen = Xd - means
-        norms = torch.linalg.vector_norm(cen, dim=0)
-        scale = Xd.abs().amax(dim=0)
-        keep = norms > 1e-12 * torch.clamp(scale, min=1.0)
-        if not bool(keep.any()):
+        Xd = X.to(torch.float64).contiguous()
+        n, p = Xd.shape
+        lib = native.load()
+        stats = torch.empty((3, p), dtype=torch.float64, device=Xd.device)
+        st = _device.stream_handle()
+        native.check(lib.l0_standardize_stats(Xd.data_ptr(), n, p, p, stats[0].data_ptr(),
+                                              stats[1].data_ptr(), stats[2].data_ptr(), st))
+        means, norms, scale = stats.cpu().numpy()
+        keep = norms > 1e-12 * np.maximum(1.0, scale)
+        if not keep.any():
             raise InvalidInputError("all columns are constant")
-        kept = torch.nonzero(keep).flatten()
-        out = cen[:, kept] / norms[kept]
-        kh = kept.cpu().numpy()
-        return out, StandardizeTransform(kept=kh, dropped=np.flatnonzero(~keep.cpu().numpy()),
-                                         means=means[kept].cpu().numpy(),
-                                         norms=norms[kept].cpu().numpy())
+        kept = np.nonzero(keep)[0]
+        kd = torch.from_numpy(kept.astype(np.int64)).to(Xd.device)
+        out = torch.empty((n, kept.size), dtype=torch.float64, device=Xd.device)
+        native.check(lib.l0_standardize_apply(Xd.data_ptr(), n, p, kd.data_ptr(), kept.size,
+                                              stats[0].data_ptr(), stats[1].data_ptr(), out.data_ptr(), st))
+        return out, StandardizeTransform(kept=kept, dropped=np.nonzero(~keep)[0],
+                                         means=means[kept], norms=norms[kept])
     X = np.asarray(X, dtype=np.float64)
     if X.ndim != 2 or X.shape[0] < 2:
         raise InvalidInputError("standardize needs a 2-d matrix with n >= 2")

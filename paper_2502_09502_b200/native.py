@@ -81,6 +81,11 @@ _PROTOS = {
                                    ctypes.POINTER(c_i64), c_vp]),
     "l0_safe_lower_bound": (c_i32, [c_vp, c_vp, c_i64, c_f64, c_f64, c_vp,
                                     ctypes.POINTER(c_f64), c_vp]),
+    "l0_safe_lower_bound_batched_workspace": (c_i32, [c_vp, c_i64, ctypes.POINTER(c_u64)]),
+    "l0_safe_lower_bound_batched": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_f64, c_f64, c_vp, c_vp, c_vp,
+                                            c_u64, c_vp]),
+    "l0_standardize_stats": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "l0_standardize_apply": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "l0_ops_workspace_bytes": (c_i32, [c_i64, ctypes.POINTER(c_u64)]),
     "l0_prox": (c_i32, [c_vp, c_i64, c_f64, c_i64, c_f64, c_vp, c_i32, c_vp, c_vp,
                         ctypes.POINTER(c_i64), c_vp, c_u64, c_vp]),

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
-from typing import Optional, Tuple
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -18,7 +18,7 @@ from . import native
 from .errors import InfeasibleNodeError, InvalidInputError, UnsupportedOperationError
 from .model import LossKind, NodeState, ProblemInstance
 
-__all__ = ["EnvelopeParams", "g_value", "g_conjugate", "safe_lower_bound"]
+__all__ = ["EnvelopeParams", "g_value", "g_conjugate", "safe_lower_bound", "safe_lower_bound_batched"]
 
 _FEAS_RTOL = 1e-9   # perspective.py:23
 _ZERO_ATOL = 1e-9   # perspective.py:25
@@ -136,3 +136,56 @@ def safe_lower_bound(instance: ProblemInstance, beta_hat, node: Optional[NodeSta
                                                   _device.ptr(cls), ctypes.byref(out),
                                                   _device.stream_handle()))
     return float(out.value)
+
+
+_bb_ws = None
+
+
+def safe_lower_bound_batched(instance: ProblemInstance, betas, nodes: Sequence[Optional[NodeState]]):
+    """safe_lower_bound (perspective.py:162-190) of len(nodes) search nodes in
+    one engine call: row j of ``betas`` (len(nodes) x p) is node j's point.
+    fp64 throughout (l0_safe_lower_bound_batched); each value equals the
+    per-node bound up to the summation order of the two X passes.  Returns a
+    list of floats (-inf where F*(-zeta) is +inf)."""
+    global _bb_ws
+    if instance.loss is LossKind.MULTINOMIAL:
+        raise UnsupportedOperationError("multinomial instances have no vector-coefficient bound")
+    if instance.loss not in (LossKind.SQUARED_ERROR, LossKind.LOGISTIC, LossKind.SQUARED_HINGE,
+                             LossKind.POISSON, LossKind.GAMMA):
+        raise UnsupportedOperationError(
+            f"{instance.loss.value}: the B200 engine evaluates bounds for vector GLM losses")
+    nodes = list(nodes)
+    nb = len(nodes)
+    if nb == 0:
+        return []
+    from . import _device
+    import torch
+    bd = _device.to_cuda_f64(betas)
+    if bd.ndim != 2 or bd.shape[0] != nb or bd.shape[1] != instance.p:
+        raise InvalidInputError(f"betas must be {nb} x {instance.p}")
+    if not bool(torch.isfinite(bd).all()):
+        raise InvalidInputError("beta_hat contains non-finite entries")
+    params = [EnvelopeParams.for_instance(instance, nd) for nd in nodes]
+    kf = np.array([pr.k_remaining if pr.restricted else pr.k for pr in params], dtype=np.int64)
+    cls = None
+    if any(pr.restricted for pr in params):
+        host = np.zeros((nb, instance.p), dtype=np.uint8)
+        for j, pr in enumerate(params):
+            if pr.fixed_one:
+                host[j, np.asarray(pr.fixed_one, dtype=np.int64)] = native.FIXED_ONE
+            if pr.fixed_zero:
+                host[j, np.asarray(pr.fixed_zero, dtype=np.int64)] = native.FIXED_ZERO
+        cls = torch.from_numpy(host).to(_device.device())
+    dp = instance.device_problem()
+    lib = native.lib()
+    need = ctypes.c_uint64()
+    native.check(lib.l0_safe_lower_bound_batched_workspace(dp.handle, nb, ctypes.byref(need)))
+    if _bb_ws is None:
+        _bb_ws = _device.Workspace()
+    ws = _bb_ws.get(need.value)
+    out = np.empty(nb, dtype=np.float64)
+    native.check(lib.l0_safe_lower_bound_batched(
+        dp.handle, bd.data_ptr(), nb, kf.ctypes.data_as(ctypes.c_void_p), float(instance.M),
+        float(instance.lambda2), _device.ptr(cls), out.ctypes.data_as(ctypes.c_void_p),
+        ws.data_ptr(), need.value, _device.stream_handle()))
+    return [float(v) for v in out]
