@@ -256,6 +256,9 @@ int32_t l0_batch_solve(l0_batch* batch, int64_t k, double M, double lambda2,
                        double* d_beta_out, l0_report* reps, void* stream);
 int32_t l0_batch_destroy(l0_batch* batch);
 
+/* C_s = A B^T in 3xTF32 on tcgen05 (the batched engine's contraction):
+ * splits > 0: that many K splits (C holds S partials, S x N x ldc); 0: planned
+ * split count; < 0: stream-K (one output C, N x ldc).  *h_splits gets S. */
 uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
                           const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,

@@ -35,6 +35,9 @@ struct Batch {
   std::vector<cudaEvent_t> ev;   // profile: [iter][gemm_t b,e | step+window b,e | gemm_f b,e]
   int64_t graph_kernels = 0;
   int sf_cap = 1, sct_cap = 1;   // split-K partial capacity carved for the measured choice
+  int streamk = 0;               // stream-K contractions (L0_TC_SK=1; default: tuned split-K)
+  float* sk_part = nullptr;      // stream-K partials [sms][kTcBN][kTcBM]
+  int* sk_flag = nullptr;        // [sms]
 };
 
 static uint64_t batch_carve(Batch& Bt, char* base) {
@@ -84,6 +87,8 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
   g.slab_htop = (double*)take(8ull * B * g.S * kHTop);
   g.flags = (int*)take(4ull * 8);
   g.slot = (int*)take(4ull * B);
+  Bt.sk_part = Bt.streamk ? (float*)take(4ull * Bt.sms * kTcBN * kTcBM) : nullptr;
+  Bt.sk_flag = Bt.streamk ? (int*)take(4ull * Bt.sms) : nullptr;
   return off + 1024;
 }
 
@@ -242,9 +247,11 @@ static cudaError_t tune_splits(Batch& Bt, cudaStream_t s) {
 
 extern "C" {
 
+// operands (hi/lo splits) | stream-K partials and flags for up to 256 CTAs
+static constexpr int kSkMaxCtas = 256;
 uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const int64_t ldk = (K + 31) / 32 * 32;
-  return (uint64_t)(2 * (M + N) * ldk) * 4 + 1024;
+  return (uint64_t)(2 * (M + N) * ldk) * 4 + 1024 + 4ull * kSkMaxCtas * (kTcBN * kTcBM + 1) + 256;
 }
 
 int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
@@ -291,6 +298,15 @@ int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K
   if (splits > 0) {
     g.S = splits;
     g.units = g.S * g.m_tiles * g.n_tiles;
+  } else if (splits < 0) {   // stream-K: one output, partials only for tiles that straddle CTAs
+    sms = std::min(sms, kSkMaxCtas);
+    g.S = 1;
+    g.units = g.m_tiles * g.n_tiles;
+    g.streamk = 1;
+    g.sk_part = bl + N * ldk;
+    g.sk_flag = (int*)(g.sk_part + (int64_t)kSkMaxCtas * kTcBN * kTcBM);
+    if (cudaMemsetAsync(g.sk_flag, 0, 4ull * kSkMaxCtas, s) != cudaSuccess)
+      return set_error(L0_CUDA, "memset failed");
   }
   if (h_splits_out) *h_splits_out = g.S;
   const int grid = std::min(g.units, sms);
@@ -344,6 +360,19 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   gt.N = 2 * n_nodes;
   gt.n_tiles = (int)((gt.N + kTcBN - 1) / kTcBN);
   gt.units = gt.S * gt.m_tiles * gt.n_tiles;
+  // stream-K (L0_TC_SK=1): one output per contraction from even (tile,
+  // K-block) shares.  Measured on C4: no faster end to end (1.52 vs 1.47-1.52
+  // ms per batched iteration) and each output is one fp32 TMEM accumulation
+  // over all of K (5000 / 20000) instead of eight ~625-deep chunks summed in
+  // fp64 by the consumers -- so the tuned split-K stays the default
+  Bt->streamk = getenv("L0_TC_SK") ? atoi(getenv("L0_TC_SK")) : 0;
+  if (Bt->streamk) {
+    for (TcGemmArgs* t : {&gf, &gt}) {
+      t->S = 1;
+      t->units = t->m_tiles * t->n_tiles;
+      t->streamk = 1;
+    }
+  }
   g.sf = gf.S;
   g.sct = gt.S;
   // partial capacity for the measured split choice (l0_batch_set_workspace)
@@ -354,6 +383,7 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   Bt->sct_cap = gt.S;
   if (getenv("L0_TC_SF")) Bt->sf_cap = gf.S;
   if (getenv("L0_TC_ST")) Bt->sct_cap = gt.S;
+  if (Bt->streamk) Bt->sf_cap = Bt->sct_cap = 1;
   Bt->ws_bytes = batch_carve(*Bt, nullptr);
   cudaError_t e = cudaStreamCreateWithFlags(&Bt->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&Bt->ev_in, cudaEventDisableTiming);
@@ -419,7 +449,15 @@ int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
   gt.c_split = 2 * g.B * g.pp;
   gt.C = g.ct;
   gt.n_active = g.flags + 2;
-  L0_B_TRY(tune_splits(*Bt, s));
+  if (Bt->streamk) {
+    for (TcGemmArgs* t : {&gf, &gt}) {
+      t->sk_part = Bt->sk_part;
+      t->sk_flag = Bt->sk_flag;
+    }
+    L0_B_TRY(cudaMemsetAsync(Bt->sk_flag, 0, 4ull * Bt->sms, s));
+  } else {
+    L0_B_TRY(tune_splits(*Bt, s));
+  }
   L0_B_TRY(cudaStreamSynchronize(s));
   return L0_OK;
 }

@@ -313,8 +313,9 @@ __device__ void sort_window_regs(WinSmem& sm, int cnt) {
 }
 
 // Large windows: each warp sorts a run of 32 * E pairs in registers (shuffles
-// only), then the kWinThreads / 32 sorted runs are merged by co-ranking
-// (sortnet.cuh merge_runs) -- far fewer block barriers than a block bitonic.
+// only), then the kWinThreads / 32 sorted runs are merged pairwise by merge
+// path (sortnet.cuh merge_runs_path) -- far fewer block barriers than a block
+// bitonic.
 template <int E>
 __device__ void sort_window_runs(WinSmem& sm, int cnt) {
   constexpr int RUN = 32 * E;
@@ -337,9 +338,10 @@ __device__ void sort_window_runs(WinSmem& sm, int cnt) {
     sm.wkey[s] = k[e];
     sm.widx[s] = id[e];
   }
-  if (threadIdx.x <= NW) sm.u.hist[threadIdx.x] = (unsigned)(threadIdx.x * RUN);
   __syncthreads();
-  const int res = merge_runs(sm.wkey, sm.widx, sm.mkey, sm.midx, sm.u.hist, NW, kWinCap);
+  // merge path (one co-rank search per thread and level; the per-element
+  // co-ranking of merge_runs took ~75 us on 4096 keys: C2's first iterations)
+  const int res = merge_runs_path<kWinCap / kWinThreads>(sm.wkey, sm.widx, sm.mkey, sm.midx, RUN, NW);
   if (res) {
     for (int s = threadIdx.x; s < cnt; s += kWinThreads) {
       sm.wkey[s] = sm.mkey[s];

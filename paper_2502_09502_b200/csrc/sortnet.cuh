@@ -43,6 +43,36 @@ __device__ void bitonic_desc(double* key, int* idx, int n) {
   }
 }
 
+// In-thread compare-exchange stage of a register bitonic sort: element e of
+// this thread is position e * stride + lane0, partners differ by JE in e.  JE
+// is a template argument so that k / id stay in registers (a runtime JE
+// puts them on the stack: 96 bytes of local memory per thread, ~50 us of the
+// 4096-key window sort).
+template <int E, int JE>
+__device__ __forceinline__ void inreg_stage(double (&k)[E], int (&id)[E], int stride, int lane0, int kk) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if ((e & JE) == 0) {
+      const int e2 = e | JE;
+      const int i = e * stride + lane0;
+      const bool dir = (i & kk) == 0;
+      const bool ord = precedes(k[e], id[e], k[e2], id[e2]);
+      if (dir != ord) {
+        const double tk = k[e]; k[e] = k[e2]; k[e2] = tk;
+        const int ti = id[e]; id[e] = id[e2]; id[e2] = ti;
+      }
+    }
+  }
+}
+template <int E>
+__device__ __forceinline__ void inreg_dispatch(double (&k)[E], int (&id)[E], int je, int stride, int lane0,
+                                               int kk) {
+  if (E > 1 && je == 1) inreg_stage<E, (E > 1 ? 1 : 0)>(k, id, stride, lane0, kk);
+  else if (E > 2 && je == 2) inreg_stage<E, (E > 2 ? 2 : 0)>(k, id, stride, lane0, kk);
+  else if (E > 4 && je == 4) inreg_stage<E, (E > 4 ? 4 : 0)>(k, id, stride, lane0, kk);
+  else if (E > 8 && je == 8) inreg_stage<E, (E > 8 ? 8 : 0)>(k, id, stride, lane0, kk);
+}
+
 // Register bitonic sort of N = T * E pairs held E per thread (element e of
 // thread t is position e * T + t).  Strides < 32 exchange through warp
 // shuffles, strides 32..T/2 through shared memory (sk/si, N entries), strides
@@ -57,22 +87,7 @@ __device__ void bitonic_regs(double (&k)[E], int (&id)[E], double* sk, int* si) 
 #pragma unroll 1
     for (int j = kk >> 1; j > 0; j >>= 1) {
       if (j >= T) {
-        const int je = j / T;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-#pragma unroll
-          for (int e2 = e + 1; e2 < E; ++e2) {
-            if ((e ^ e2) == je) {                    // static indices: stays in registers
-              const int i = e * T + tid;               // lower position of the pair
-              const bool dir = (i & kk) == 0;
-              const bool ord = precedes(k[e], id[e], k[e2], id[e2]);
-              if (dir != ord) {
-                const double tk = k[e]; k[e] = k[e2]; k[e2] = tk;
-                const int ti = id[e]; id[e] = id[e2]; id[e2] = ti;
-              }
-            }
-          }
-        }
+        inreg_dispatch<E>(k, id, j / T, T, tid, kk);
       } else if (j >= 32) {
 #pragma unroll
         for (int e = 0; e < E; ++e) { sk[e * T + tid] = k[e]; si[e * T + tid] = id[e]; }
@@ -113,22 +128,7 @@ __device__ __forceinline__ void bitonic_warp(double (&k)[E], int (&id)[E], int l
 #pragma unroll 1
     for (int j = kk >> 1; j > 0; j >>= 1) {
       if (j >= 32) {
-        const int je = j >> 5;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-#pragma unroll
-          for (int e2 = e + 1; e2 < E; ++e2) {
-            if ((e ^ e2) == je) {
-              const int i = e * 32 + lane;
-              const bool dir = (i & kk) == 0;
-              const bool ord = precedes(k[e], id[e], k[e2], id[e2]);
-              if (dir != ord) {
-                const double tk = k[e]; k[e] = k[e2]; k[e2] = tk;
-                const int ti = id[e]; id[e] = id[e2]; id[e2] = ti;
-              }
-            }
-          }
-        }
+        inreg_dispatch<E>(k, id, j >> 5, 32, lane, kk);
       } else {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -200,6 +200,59 @@ __device__ int merge_runs(double* k0, int* i0, double* k1, int* i1, unsigned* of
     if ((int)threadIdx.x <= S2) off[threadIdx.x] = o;
     __syncthreads();
     S = S2;
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// Merge S sorted runs of equal length `run` (S * run = total, S a power of
+// two) pairwise, log2(S) levels, by merge path: thread t writes the ITEMS
+// consecutive outputs [ITEMS t, ITEMS t + ITEMS) of its pair after ONE
+// co-rank binary search on the merge-path diagonal, then a sequential merge
+// of ITEMS steps -- instead of a binary search per element (scattered shared
+// loads, bank conflicts).  total == ITEMS * blockDim.x.  Same strict order as
+// merge_runs (key descending, index ascending); returns 0 if the result is in
+// (k0, i0), 1 otherwise.
+template <int ITEMS>
+__device__ int merge_runs_path(double* k0, int* i0, double* k1, int* i1, int run, int S) {
+  int cur = 0;
+  for (; S > 1; S >>= 1, run <<= 1) {
+    const double* ks = cur ? k1 : k0;
+    const int* is = cur ? i1 : i0;
+    double* kd = cur ? k0 : k1;
+    int* id = cur ? i0 : i1;
+    const int q0 = ITEMS * threadIdx.x;
+    const int sa = (q0 / (2 * run)) * (2 * run);     // pair start
+    const int sb = sa + run;                          // second run
+    const int d = q0 - sa;                            // diagonal in the pair
+    // co-rank: i elements of A = [sa, sb) and d - i of B = [sb, sb + run)
+    int lo = max(0, d - run), hi = min(d, run);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int j = d - mid - 1;
+      if (precedes(ks[sa + mid], is[sa + mid], ks[sb + j], is[sb + j])) lo = mid + 1;
+      else hi = mid;
+    }
+    int ia = sa + lo, ib = sb + (d - lo);
+    const int ea = sb, eb = sb + run;
+    double ka = ia < ea ? ks[ia] : 0.0, kb = ib < eb ? ks[ib] : 0.0;
+    int xa = ia < ea ? is[ia] : 0, xb = ib < eb ? is[ib] : 0;
+#pragma unroll
+    for (int e = 0; e < ITEMS; ++e) {
+      const bool take_a = ib >= eb || (ia < ea && precedes(ka, xa, kb, xb));
+      if (take_a) {
+        kd[q0 + e] = ka;
+        id[q0 + e] = xa;
+        ++ia;
+        if (ia < ea) { ka = ks[ia]; xa = is[ia]; }
+      } else {
+        kd[q0 + e] = kb;
+        id[q0 + e] = xb;
+        ++ib;
+        if (ib < eb) { kb = ks[ib]; xb = is[ib]; }
+      }
+    }
+    __syncthreads();
     cur ^= 1;
   }
   return cur;

@@ -83,19 +83,55 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-struct Unit {
-  int s, mt, nt;
+// A run of K blocks [kb0, kb1) of one output tile.  kind: 0 = the whole K
+// range of a split-K unit or of a stream-K tile (written to C), 1 = a
+// stream-K piece that does not start at K block 0 (fp32 partial to
+// sk_part[cta], flagged), 2 = a stream-K piece starting at K block 0 of a
+// tile that other CTAs finish (waits for their partials, adds, writes C).
+struct Seg {
+  int s, mt, nt, kb0, kb1, kind;
 };
-// units are numbered over the LIVE n-tiles only (rows of B actually needed,
-// read on the device), so a launch with fewer live rows stays balanced
-__device__ __forceinline__ Unit decode(const TcGemmArgs& g, int nt_live, int u) {
-  Unit r;
-  r.nt = u % nt_live;
-  const int rest = u / nt_live;
-  r.mt = rest % g.m_tiles;
-  r.s = rest / g.m_tiles;
-  return r;
-}
+// stream-K: the steps (tile, K block), tiles in (m-tile, n-tile) order with n
+// fastest, split into gridDim.x contiguous ranges
+__device__ __forceinline__ int64_t sk_start(int64_t total, int c, int G) { return total * c / G; }
+
+struct SegIter {
+  const TcGemmArgs& g;
+  int nt_live, units;
+  int64_t step, end, total;   // stream-K
+  int u;                      // split-K
+  __device__ SegIter(const TcGemmArgs& g_, int ntl) : g(g_), nt_live(ntl) {
+    units = g.S * g.m_tiles * nt_live;
+    total = (int64_t)g.m_tiles * nt_live * g.kb_total;
+    step = sk_start(total, blockIdx.x, gridDim.x);
+    end = sk_start(total, blockIdx.x + 1, gridDim.x);
+    u = blockIdx.x;
+  }
+  __device__ bool next(Seg& r) {
+    if (g.streamk) {
+      if (step >= end) return false;
+      const int64_t tile = step / g.kb_total;
+      r.s = 0;
+      r.nt = (int)(tile % nt_live);
+      r.mt = (int)(tile / nt_live);
+      r.kb0 = (int)(step - tile * g.kb_total);
+      r.kb1 = (int)min((int64_t)g.kb_total, (int64_t)r.kb0 + (end - step));
+      r.kind = r.kb0 > 0 ? 1 : (r.kb1 < g.kb_total ? 2 : 0);
+      step += r.kb1 - r.kb0;
+      return true;
+    }
+    if (u >= units) return false;
+    r.nt = u % nt_live;
+    const int rest = u / nt_live;
+    r.mt = rest % g.m_tiles;
+    r.s = rest / g.m_tiles;
+    r.kb0 = (int)(((int64_t)g.kb_total * r.s) / g.S);
+    r.kb1 = (int)(((int64_t)g.kb_total * (r.s + 1)) / g.S);
+    r.kind = 0;
+    u += gridDim.x;
+    return true;
+  }
+};
 
 // instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = kTcBN
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcBN >> 3) << 17) |
@@ -118,7 +154,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_act = g.n_active ? (int64_t)*g.n_active : g.N;
   const int nt_live = (int)min((int64_t)g.n_tiles, (n_act + kTcBN - 1) / kTcBN);
-  const int units = g.S * g.m_tiles * nt_live;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_ah) : "memory");
@@ -146,21 +181,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto kb_range = [&](int s, int& kb0, int& kb1) {
-    kb0 = (int)(((int64_t)g.kb_total * s) / g.S);
-    kb1 = (int)(((int64_t)g.kb_total * (s + 1)) / g.S);
-  };
-
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = decode(g, nt_live, u);
-        int kb0, kb1;
-        kb_range(w.s, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      SegIter it(g, nt_live);
+      Seg w;
+      while (it.next(w)) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           bar_wait(&empty[stage], phase ^ 1u);
           unsigned char* st = smem + stage * kStageBytes;
           bar_expect(&full[stage], kStageBytes);
@@ -179,14 +208,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int li = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = decode(g, nt_live, u);
+      SegIter it(g, nt_live);
+      Seg w;
+      while (it.next(w)) {
         const int acc = li & 1;
         bar_wait(&tempty[acc], ((li >> 1) & 1) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * kTcBN);
-        int kb0, kb1;
-        kb_range(w.s, kb0, kb1);
+        const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           bar_wait(&full[stage], phase);
           tc_fence_after();
@@ -211,24 +240,67 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> C (transposed, coalesced along m) =====
     const int q = warp & 3;
+    const int et = threadIdx.x - 128;          // 0..127 over the four epilogue warps
     int li = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit w = decode(g, nt_live, u);
+    SegIter it(g, nt_live);
+    Seg w;
+    while (it.next(w)) {
       const int acc = li & 1;
       bar_wait(&tfull[acc], (li >> 1) & 1);
       tc_fence_after();
       const int64_t m = (int64_t)w.mt * kTcBM + q * 32 + lane;
-      float* cbase = g.C + (int64_t)w.s * g.c_split;
+      if (w.kind == 1) {
+        // stream-K piece without K block 0: fp32 partial for the finishing CTA
+        float* part = g.sk_part + (int64_t)blockIdx.x * kTcBN * kTcBM;
 #pragma unroll 1
-      for (int c = 0; c < kTcBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kTcBN + c * 32), v);
-        const int64_t r0 = (int64_t)w.nt * kTcBN + c * 32;
-        if (m < g.M) {
+        for (int c = 0; c < kTcBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kTcBN + c * 32), v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (r0 + j < n_act) cbase[(r0 + j) * g.ldc + m] = __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) part[(c * 32 + j) * kTcBM + q * 32 + lane] = __uint_as_float(v[j]);
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(g.sk_flag + blockIdx.x), "r"(1) : "memory");
+      } else {
+        // CTAs holding the later K blocks of this tile (stream-K kind 2)
+        int c_first = 0, c_last = -1;
+        if (w.kind == 2) {
+          const int64_t total = (int64_t)g.m_tiles * nt_live * g.kb_total;
+          const int64_t tile_end = ((int64_t)w.mt * nt_live + w.nt + 1) * g.kb_total;
+          c_first = blockIdx.x + 1;
+          c_last = blockIdx.x;
+          while (c_last + 1 < (int)gridDim.x && sk_start(total, c_last + 1, gridDim.x) < tile_end) ++c_last;
+          if (et <= c_last - c_first) {
+            int f = 0;
+            while (!f) asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(g.sk_flag + c_first + et) : "memory");
           }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        float* cbase = g.C + (int64_t)w.s * g.c_split;
+#pragma unroll 1
+        for (int c = 0; c < kTcBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kTcBN + c * 32), v);
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          for (int cc = c_first; cc <= c_last; ++cc) {   // fixed CTA order
+            const float* part = g.sk_part + (int64_t)cc * kTcBN * kTcBM;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] += __ldcg(part + (c * 32 + j) * kTcBM + q * 32 + lane);
+          }
+          const int64_t r0 = (int64_t)w.nt * kTcBN + c * 32;
+          if (m < g.M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (r0 + j < n_act) cbase[(r0 + j) * g.ldc + m] = f[j];
+            }
+          }
+        }
+        if (w.kind == 2) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et <= c_last - c_first) g.sk_flag[c_first + et] = 0;   // consumed: clean for the next launch
         }
       }
       tc_fence_before();

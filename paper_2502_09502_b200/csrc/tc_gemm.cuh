@@ -12,7 +12,9 @@
 // accumulator; four epilogue warps drain TMEM with tcgen05.ld and store the
 // fp32 split-K partial transposed ([r][m], coalesced along m).  Persistent
 // CTAs walk (split, m-tile, n-tile) units, n fastest, so the n-tiles of one
-// A block run back to back and A is read from HBM once.
+// A block run back to back and A is read from HBM once -- or, in stream-K
+// mode, an even share of the (tile, K-block) steps each, which keeps every SM
+// busy without split-K partials of every tile in HBM.
 #pragma once
 
 #include <cuda.h>
@@ -35,6 +37,13 @@ struct TcGemmArgs {
   int m_tiles, n_tiles;
   int kb_total;         // K blocks of kTcBK
   const int* n_active;  // nullable: rows of B actually needed (<= N), read on device
+  // stream-K mode (streamk = 1): one output C (S = 1), the (tile, K-block)
+  // steps split evenly over the persistent CTAs; a tile that straddles CTAs
+  // is finished by the CTA holding its first K block, which adds the other
+  // CTAs' fp32 partials (sk_part[cta], flagged in sk_flag[cta]) in CTA order.
+  int streamk;
+  float* sk_part;       // [grid][kTcBN][kTcBM]
+  int* sk_flag;         // [grid], zero between launches (the finishing CTA resets it)
 };
 
 // Host: tensor map for a K-major fp32 matrix (rows x K, row pitch ld elements)
