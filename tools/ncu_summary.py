@@ -1,10 +1,12 @@
 """Build profiles/ncu_summary.json from ncu --set full reports:
-python tools/ncu_summary.py out.json rep1.ncu-rep [rep2 ...]"""
+python tools/ncu_summary.py out.json [CFG=]rep1.ncu-rep [[CFG=]rep2 ...]
+(CFG= prefixes the kernel keys, e.g. C2=prof.ncu-rep -> "C2/kf_fused_s")"""
 import csv, json, re, subprocess, sys
 
 SHORT = [("kf_fused_s", "kf_fused_s"), ("kf_fused", "kf_fused"), ("k1_forward", "k1_forward"), ("k2_transpose", "k2_transpose"),
          ("k3_prox_window", "k3_prox_window"), ("kr_reduce", "kr_reduce"), ("tc_gemm_kernel", "tc_gemm_kernel"),
-         ("kb_window", "kb_window"), ("kb_step", "kb_step"), ("kb_obj", "kb_obj"), ("kb_rhs", "kb_rhs")]
+         ("kb_window", "kb_window"), ("kb_step", "kb_step"), ("kb_obj", "kb_obj"), ("kb_rhs", "kb_rhs"),
+         ("k_mrhs", "k_mrhs"), ("k_std_stats", "k_std_stats")]
 METRICS = {"gpu__time_duration.sum": ("duration_us", 1.0), "dram__bytes_read.sum": ("dram_read_bytes", None),
            "dram__bytes_write.sum": ("dram_write_bytes", None),
            "dram__throughput.avg.pct_of_peak_sustained_elapsed": ("dram_pct_of_ncu_peak", 1.0),
@@ -17,7 +19,8 @@ METRICS = {"gpu__time_duration.sum": ("duration_us", 1.0), "dram__bytes_read.sum
            "launch__block_size": ("block", 1.0)}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1.0, "ms": 1e3, "ns": 1e-3}
 out = {"source": "ncu --set full --clock-control none (B200), tools/profile_round.sh", "kernels": {}}
-for rep in sys.argv[2:]:
+for arg in sys.argv[2:]:
+    cfg, rep = arg.split("=", 1) if "=" in arg else ("", arg)
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     if len(rows) < 3:
@@ -28,6 +31,8 @@ for rep in sys.argv[2:]:
         short = next((s for k, s in SHORT if k in name), None)
         if short is None:
             continue
+        if cfg:
+            short = f"{cfg}/{short}"
         rec = {"name": name, "report": rep}
         for m, (key, _) in METRICS.items():
             if m in h:
