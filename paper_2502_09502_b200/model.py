@@ -254,6 +254,7 @@ class ProblemInstance:
             raise InvalidInputError("lambda2 must be a positive finite real")
         _check_labels(self.loss, self.y)
         self._dev = None
+        self._dev_src = None
 
     def _x_finite(self) -> bool:
         if isinstance(self.X, np.ndarray):
@@ -287,15 +288,18 @@ class ProblemInstance:
         reference treats its private float64 copy (model.py:92): in-place
         edits of the host array are not seen; assign a new array to ``X`` (a
         new object re-uploads) or call ``release_device()``."""
-        if self._dev is None or self._dev_key != id(self.X):
+        # keyed by the array object itself (a reference, not its id: a new
+        # array cannot reuse a freed id while the old one is held here)
+        if self._dev is None or self._dev_src is not self.X:
             if not is_solver_grade(self.loss):
                 _engine_loss(self.loss)
             self._dev = DeviceProblem(self.X, self.y, self.loss, self.dtype)
-            self._dev_key = id(self.X)
+            self._dev_src = self.X
         return self._dev
 
     def release_device(self) -> None:
         self._dev = None
+        self._dev_src = None
 
 
 @dataclass
