@@ -468,6 +468,7 @@ def run_c5_single(args):
     st = eng.solve_relaxation(inst, opts=o(K, True), return_device=True).stats
     peak, src = measured_peak()
     roof = kf_roofline(st, n, p, 4, peak, src, "C5/kf_fused_s") if st.get("single_pass") else None
+    f32 = fp32_mode_run(eng, inst, L, K, n, p, peak, src)
     cpu = None
     if not args.no_cpu:
         cpu = cpu_baseline_c5(n, args.c5_cpu_rows, 3, "cuda", L=L)
@@ -478,7 +479,30 @@ def run_c5_single(args):
             "engine_path": "single_pass" if st.get("single_pass") else "two_pass",
             "cluster_size": st.get("cluster_size"), "lipschitz": L, "lipschitz_method": "lanczos",
             "setup_s": {"generate": gen_s, "lanczos": l_s}, "roofline": roof, "cpu_baseline": cpu,
-            "restarts": rep.restarts, "primal": rep.primal_value, "dual": rep.dual_bound}
+            "restarts": rep.restarts, "primal": rep.primal_value, "dual": rep.dual_bound,
+            "fp32_mode": f32}
+
+
+def fp32_mode_run(eng, inst, L, K, n, p, peak, src):
+    """The same K iterations in the fp32 mode (FistaOptions.fp32_forward: X beta
+    in fp32 products, fp64 reductions -- BASELINE's "fp32 X with fp64
+    reductions", north-star tolerance 1e-5; tests/test_gpu_fullsize.py)."""
+    import torch
+    o = lambda k, prof: eng.FistaOptions(lipschitz=L, max_iterations=k, gap_tolerance=1e-300,
+                                         stop_on_gap=False, profile=prof, fp32_forward=True)
+    eng.solve_relaxation(inst, opts=o(3, False), return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep = eng.solve_relaxation(inst, opts=o(K, False), return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st = eng.solve_relaxation(inst, opts=o(K, True), return_device=True).stats
+    roof = kf_roofline(st, n, p, 4, peak, src, "none") if st.get("single_pass") else None
+    return {"value": K / (ms / 1e3), "unit": "iters/s", "ms_per_step": ms / K, "roofline": roof,
+            "primal": rep.primal_value, "dual": rep.dual_bound, "restarts": rep.restarts,
+            "arithmetic": "X beta: fp32 products, fp64 reductions; X^T r and everything else fp64"}
 
 
 def run_config(name, iters):
@@ -527,6 +551,9 @@ def run_config(name, iters):
            "x_bytes": xb, "l2_resident": xb < 100e6, "kernels": kern, "peak_gbs": peak,
            "primal": rep.primal_value, "dual": rep.dual_bound, "restarts": rep.restarts,
            "setup_s": gen_s}
+    if cd.dtype == "fp32" and st.get("single_pass"):
+        src = measured_peak()[1]
+        out["fp32_mode"] = fp32_mode_run(eng, inst, L, iters, n, p, peak, src)
     del inst
     torch.cuda.empty_cache()
     return out

@@ -84,6 +84,8 @@ typedef struct l0_fista_opts {
   int32_t profile;              /* 1: time the kernels with CUDA events (report fields) */
   int32_t engine_path;          /* 0 auto (single pass for fp64 X when it fits a <= 8-CTA cluster
                                    plan, else two-pass), 1 two-pass, 2 single pass */
+  int32_t fp32_forward;         /* fp32 X, single pass: X beta with fp32 products and fp64
+                                   reductions (the fp32 mode, 1e-5 relative); 0: fp64 products */
 } l0_fista_opts;
 
 /* NodeState (model.py:119-149): host index arrays, sorted unique, disjoint. */

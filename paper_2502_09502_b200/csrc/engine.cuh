@@ -81,6 +81,7 @@ struct EngineArgs {
   int fz_stages;     // shared-memory tile ring depth
   int fz_slots;      // partial-slot ring depth
   int fz_widen;
+  int f32_forward;   // fp32 X: forward products in fp32 (FistaOptions.fp32_forward; fused.cu)
   uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)
   int64_t fz_tiles;  // row tiles

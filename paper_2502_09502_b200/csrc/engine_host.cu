@@ -78,6 +78,7 @@ struct Graph {
   int G = 0;
   int profile = 0;
   int full_sort = 0;   // K3 variant captured (EngineArgs::prox_full_sort)
+  int f32f = 0;        // single-pass kernel variant captured (EngineArgs::f32_forward)
   int64_t kernels = 0;
   std::vector<cudaEvent_t> ev;  // profile: [iter][k2b,k2e,k3b,k3e,k1b,k1e]
 };
@@ -276,7 +277,9 @@ static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
 
 static int build_graph(Problem& P, int which, int G, int profile) {
   Graph& g = P.graph[which];
-  if (g.exec && g.G == G && g.profile == profile && g.full_sort == P.a.prox_full_sort) return ST_OK;
+  if (g.exec && g.G == G && g.profile == profile && g.full_sort == P.a.prox_full_sort &&
+      g.f32f == P.a.f32_forward)
+    return ST_OK;
   if (g.exec) {
     cudaGraphExecDestroy(g.exec);
     for (auto e : g.ev) cudaEventDestroy(e);
@@ -318,6 +321,7 @@ static int build_graph(Problem& P, int which, int G, int profile) {
   g.G = G;
   g.profile = profile;
   g.full_sort = P.a.prox_full_sort;
+  g.f32f = P.a.f32_forward;
   g.kernels = kernels;
   return ST_OK;
 }
@@ -607,6 +611,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     return set_error(ST_UNSUPPORTED, "the single-pass kernel does not fit this problem");
   if (want_fused != a.fused) destroy_graphs(*P);
   a.fused = want_fused;
+  a.f32_forward = (o->fp32_forward && a.dtype == F32 && a.fused) ? 1 : 0;
   // K3 variant: the windowed top-of-order sort, switched to the full key sort
   // for the rest of the solve once most iterations of a chunk needed window
   // extensions (a PAVA pool spanning much of p, as on C3: K3 0.34 -> 0.19 ms);

@@ -315,7 +315,13 @@ struct FsShared {
 __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~size_t(127); }
 
 // shared memory: FsShared | partial slots [NS][cs][4][R] | stages x (R x W x sizeof(TX))
-template <typename TX, int R, int NV>
+// F32F (fp32 X only, FistaOptions.fp32_forward): the forward dots X beta use
+// fp32 products of fp32 X and fp32-rounded beta in four fp32 chains per lane
+// and row (24 products each on C3 / C5), reduced in fp64 from there on --
+// BASELINE's "fp32 X with fp64 reductions", within the north star's 1e-5
+// fp32-mode tolerance.  The transpose products stay fp64 (the gradient and
+// the Fenchel bound are exact for the residuals the forward produced).
+template <typename TX, int R, int NV, bool F32F = false>
 __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
   constexpr int G = fs_gather<TX>();
   constexpr int kFsProdWarp = fs_prod_warp<G>();
@@ -426,6 +432,48 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
         const int64_t col = c0 + qc + (j * 32 + lane) * VE + e;
         bq[j * VE + e] = col < a.p ? bsrc[col] : 0.0;
       }
+    if constexpr (F32F) {
+      // ---- fp32 mode: fp32 products, fp64 from the lane sums on ----
+      float bf[FV * VE];
+#pragma unroll
+      for (int i = 0; i < FV * VE; ++i) bf[i] = (float)bq[i];
+      int buf = 0, q = 0;
+      uint32_t ph = 0;
+      for (int k = 0; k < mytiles; ++k) {
+        const int rows = tile_rows(k);
+        mbar_wait(&sh.full[buf], ph, a.fz_sleep);
+        const float* tl = reinterpret_cast<const float*>(tiles) + (int64_t)buf * R * W;
+        double d[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (r < rows) {
+#pragma unroll
+            for (int j = 0; j < FV; ++j) {
+              const float4 xv = *reinterpret_cast<const float4*>(tl + r * W + qc + (j * 32 + lane) * 4);
+              s4[0] = fmaf(xv.x, bf[j * 4 + 0], s4[0]);
+              s4[1] = fmaf(xv.y, bf[j * 4 + 1], s4[1]);
+              s4[2] = fmaf(xv.z, bf[j * 4 + 2], s4[2]);
+              s4[3] = fmaf(xv.w, bf[j * 4 + 3], s4[3]);
+            }
+          }
+          d[r] = ((double)s4[0] + (double)s4[1]) + ((double)s4[2] + (double)s4[3]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < R; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+        if (lane < cs) {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r < rows)
+              st_async_f64(part + (((size_t)q * cs + crank) * kFzFwdWarps + warp) * R + r, &sh.xb[q],
+                           (uint32_t)lane, d[r]);
+        }
+        if (++buf == S) { buf = 0; ph ^= 1u; }
+        if (++q == NS) q = 0;
+      }
+    } else {
     // fp32 X: widen by integer rebias against beta * 2^896 (all of this
     // warp's beta finite after scaling; |beta| <= M keeps that true unless M
     // is within 2^-896 of the fp64 range)
@@ -488,6 +536,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
     };
     if (fint) fwd_loop(std::true_type{});
     else fwd_loop(std::false_type{});
+    }
   } else if (warp < kFsGatherWarp + G) {
     // ===================== gather =====================
     const int gw = warp - kFsGatherWarp;
@@ -754,12 +803,12 @@ static size_t fused_smem(const EngineArgs& a) {
 
 using KfFn = void (*)(EngineArgs, int);
 
-template <typename TX, int R>
+template <typename TX, int R, bool F32F = false>
 static KfFn kfs_pick_nv(int nv) {
   switch (nv) {
-    case 1: return kf_fused_s<TX, R, 1>;
-    case 2: return kf_fused_s<TX, R, 2>;
-    case 3: return kf_fused_s<TX, R, 3>;
+    case 1: return kf_fused_s<TX, R, 1, F32F>;
+    case 2: return kf_fused_s<TX, R, 2, F32F>;
+    case 3: return kf_fused_s<TX, R, 3, F32F>;
     case 4: return sizeof(TX) == 8 ? (KfFn)kf_fused_s<TX, R, 4> : nullptr;
     default: return nullptr;
   }
@@ -767,6 +816,11 @@ static KfFn kfs_pick_nv(int nv) {
 
 static KfFn kf_pick(const EngineArgs& a) {
   const bool f64 = a.dtype == F64;
+  if (!f64 && a.f32_forward) {   // fp32 mode (FistaOptions.fp32_forward)
+    if (a.fz_rows == 2) return kfs_pick_nv<float, 2, true>(a.fz_nv);
+    if (a.fz_rows == 4) return kfs_pick_nv<float, 4, true>(a.fz_nv);
+    return nullptr;
+  }
   if (a.fz_rows == 2) return f64 ? kfs_pick_nv<double, 2>(a.fz_nv) : kfs_pick_nv<float, 2>(a.fz_nv);
   if (a.fz_rows == 4) return f64 ? kfs_pick_nv<double, 4>(a.fz_nv) : kfs_pick_nv<float, 4>(a.fz_nv);
   return nullptr;

@@ -60,6 +60,10 @@ class FistaOptions:
     chunk_iterations: int = 0           # iterations per CUDA graph replay (0: auto)
     profile: bool = False               # time the kernels with CUDA events
     engine_path: str = "auto"           # "auto" | "two_pass" | "single_pass"
+    # fp32 mode for fp32 X (BASELINE C3 / C5: "fp32 X with fp64 reductions"):
+    # the single-pass kernel's X beta in fp32 products, reduced in fp64;
+    # results within ~1e-6 relative of the fp64 path (north star: 1e-5)
+    fp32_forward: bool = False
 
     def __post_init__(self):
         if self.gap_tolerance <= 0:
@@ -108,6 +112,7 @@ def _native_opts(opts: FistaOptions, L: float):
     o.chunk_iterations = int(opts.chunk_iterations)
     o.profile = 1 if opts.profile else 0
     o.engine_path = {"auto": 0, "two_pass": 1, "single_pass": 2}[opts.engine_path]
+    o.fp32_forward = 1 if opts.fp32_forward else 0
     return o
 
 
@@ -239,6 +244,7 @@ def solve_relaxation(instance: ProblemInstance, node: Optional[NodeState] = None
     o.chunk_iterations = int(opts.chunk_iterations)
     o.profile = 1 if opts.profile else 0
     o.engine_path = {"auto": 0, "two_pass": 1, "single_pass": 2}[opts.engine_path]
+    o.fp32_forward = 1 if opts.fp32_forward else 0
 
     nd = None
     keep = []

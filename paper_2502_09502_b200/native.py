@@ -32,7 +32,8 @@ class FistaOpts(ctypes.Structure):
                 ("early_primal_cutoff", c_f64), ("early_dual_cutoff", c_f64),
                 ("bound_check_interval", c_i32), ("restart", c_i32), ("lipschitz", c_f64),
                 ("gap_tolerance_rel", c_f64), ("stop_on_gap", c_i32),
-                ("chunk_iterations", c_i32), ("profile", c_i32), ("engine_path", c_i32)]
+                ("chunk_iterations", c_i32), ("profile", c_i32), ("engine_path", c_i32),
+                ("fp32_forward", c_i32)]
 
 
 class Node(ctypes.Structure):

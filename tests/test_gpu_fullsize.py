@@ -71,14 +71,16 @@ def c3(engine):
     inst.release_device()
 
 
-def _vs_oracle(engine, cd, inst, L, iters=40, path="single_pass"):
+def _vs_oracle(engine, cd, inst, L, iters=40, path="single_pass", fp32_forward=False):
+    """fp32_forward: the fp32 mode (X beta in fp32 products, fp64 reductions),
+    checked at the north star's fp32-mode tolerance 1e-5 relative."""
     import threadpoolctl
     from oracle import l0_oracle
 
     rec = []
     rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
         lipschitz=L, max_iterations=iters, gap_tolerance=1e-300, engine_path=path,
-        trace_hook=rec.append))
+        trace_hook=rec.append, fp32_forward=fp32_forward))
     assert rep.stats["single_pass"] == (path == "single_pass")
     X64 = np.asarray(cd.X, dtype=np.float64)
     trace = []
@@ -86,35 +88,44 @@ def _vs_oracle(engine, cd, inst, L, iters=40, path="single_pass"):
         ref = l0_oracle.fista(X64, cd.y, cd.loss, cd.k, cd.M, cd.lambda2, L=L, max_iter=iters,
                               gap_tol=1e-300, trace=trace.append)
     del X64
+    tp, td, tb = (1e-5, 1e-5, 1e-5) if fp32_forward else (1e-12, 1e-9, 1e-9)
     assert rep.iterations == ref["iterations"] == iters
-    assert rep.restarts == ref["restarts"]
-    assert rep.primal_value == pytest.approx(ref["primal_value"], rel=1e-12)
-    assert rep.dual_bound == pytest.approx(ref["dual_bound"], rel=1e-9)
+    if not fp32_forward:
+        # fp32 mode: restart tests compare objectives whose fp32-product noise
+        # (~1e-7 relative) exceeds their difference near the plateau, so the
+        # restart decisions may differ while every value stays within 1e-5
+        assert rep.restarts == ref["restarts"]
+    assert rep.primal_value == pytest.approx(ref["primal_value"], rel=tp)
+    assert rep.dual_bound == pytest.approx(ref["dual_bound"], rel=td)
     scale = float(np.max(np.abs(ref["beta"])))
-    np.testing.assert_allclose(rep.beta, ref["beta"], rtol=0, atol=1e-9 * scale)
-    thr = 1e-9 * cd.M
+    np.testing.assert_allclose(rep.beta, ref["beta"], rtol=0, atol=tb * scale)
+    thr = tb * cd.M
     assert np.array_equal(np.abs(rep.beta) > thr, np.abs(ref["beta"]) > thr)
     assert len(rec) == len(trace)
     for ours, theirs in zip(rec, trace):
         assert ours["iteration"] == theirs["iteration"]
-        assert ours["restarted"] == theirs["restarted"]
-        assert ours["primal"] == pytest.approx(theirs["primal"], rel=1e-12)
-        assert ours["dual"] == pytest.approx(theirs["dual"], rel=1e-9)
+        assert fp32_forward or ours["restarted"] == theirs["restarted"]
+        assert ours["primal"] == pytest.approx(theirs["primal"], rel=tp)
+        assert ours["dual"] == pytest.approx(theirs["dual"], rel=td)
+    if fp32_forward:   # the fp32 mode really ran and really differs from the fp64 products
+        assert rep.primal_value != ref["primal_value"]
     return rep
 
 
-def test_c3_full_size_vs_oracle(engine, c3):
+@pytest.mark.parametrize("fp32_forward", [False, True], ids=["fp64", "fp32mode"])
+def test_c3_full_size_vs_oracle(engine, c3, fp32_forward):
     cd, inst, L = c3
-    _vs_oracle(engine, cd, inst, L)
+    _vs_oracle(engine, cd, inst, L, fp32_forward=fp32_forward)
 
 
-def test_c5_subsample_vs_oracle(engine):
+@pytest.mark.parametrize("fp32_forward", [False, True], ids=["fp64", "fp32mode"])
+def test_c5_subsample_vs_oracle(engine, fp32_forward):
     cd = mydata.make_config("C5", scale=0.1)       # rows 0..99999 of C5 (block [0, 0])
     assert (cd.n, cd.p) == (100_000, 10_000)
     inst = engine.ProblemInstance(cd.X, cd.y, engine.LossKind.SQUARED_ERROR, cd.k, cd.M,
                                   cd.lambda2, dtype="fp32")
     L = engine.lipschitz_constant(inst, method="lanczos")
-    _vs_oracle(engine, cd, inst, L)
+    _vs_oracle(engine, cd, inst, L, fp32_forward=fp32_forward)
     inst.release_device()
 
 

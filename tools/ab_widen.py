@@ -19,8 +19,9 @@ ref = None
 for m in modes:
     os.environ["L0_FZ_WIDEN"] = str(m)
     inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype=cd.dtype)
+    f32 = os.environ.get("FP32_FORWARD") == "1"
     o = lambda k: eng.FistaOptions(lipschitz=L, max_iterations=k, stop_on_gap=False, gap_tolerance=1e-300,
-                                   engine_path="single_pass", profile=True)
+                                   engine_path="single_pass", profile=True, fp32_forward=f32)
     eng.solve_relaxation(inst, opts=o(3))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -15,5 +15,6 @@ for r in c2 c3 c5 c4 bb; do ncu -i gpurun_out/p2_$r.ncu-rep --page details --csv
 python tools/ncu_lines.py gpurun_out/p2_c2.ncu-rep kf_fused 40 > gpurun_out/p2_lines_c2_kf.txt 2>&1
 python tools/ncu_lines.py gpurun_out/p2_c5.ncu-rep kf_fused 40 > gpurun_out/p2_lines_c5_kf.txt 2>&1
 python tools/ncu_lines.py gpurun_out/p2_c4.ncu-rep tc_gemm 40 > gpurun_out/p2_lines_c4_tc.txt 2>&1
-rm -f gpurun_out/p2_c3.ncu-rep gpurun_out/p2_bb.ncu-rep
+for r in c2 c5; do ncu -i gpurun_out/p2_$r.ncu-rep --page source --csv --print-source cuda,sass > /tmp/p2_src_$r.csv 2>/dev/null; python tools/ncu_stalls.py /tmp/p2_src_$r.csv 30 > gpurun_out/p2_stalls_$r.txt 2>&1; done
+rm -f gpurun_out/*.ncu-rep   # the copy-back is capped at 64 MiB: keep the extracted summaries
 du -sh gpurun_out
