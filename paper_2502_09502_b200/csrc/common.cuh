@@ -91,6 +91,21 @@ __device__ __forceinline__ double loss_grad(int loss, double u, double y) {
   return dmul(dmul(-2.0, y), m);
 }
 
+// fp32-mode loss evaluations (single-pass kernel with fp32_forward): the
+// logistic exp / log1p chains in single precision (relative error ~1e-7, the
+// fp32 mode's budget is 1e-5); every other loss keeps its fp64 formula.  The
+// bound stays safe: F*(-zeta) is evaluated in fp64 for the zeta produced.
+__device__ __forceinline__ double loss_grad_f32m(int loss, double u, double y) {
+  if (loss != LOGISTIC) return loss_grad(loss, u, y);
+  const float t = (float)(y * u);                  // expit(-y u) = 1 / (1 + exp(y u))
+  return -y * (double)(1.0f / (1.0f + __expf(t)));
+}
+__device__ __forceinline__ double loss_term_f32m(int loss, double u, double y) {
+  if (loss != LOGISTIC) return loss_term(loss, u, y);
+  const float t = (float)(-y * u);                 // logaddexp(0, t)
+  return (double)(fmaxf(t, 0.0f) + log1pf(__expf(-fabsf(t))));
+}
+
 // xlogy(r, r) with 0 log 0 = 0
 __device__ __forceinline__ double xlogx(double r) { return r == 0.0 ? 0.0 : dmul(r, log(r)); }
 

@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
           const double arg = f == 0 ? dadd(u, dmul(cR, dlt)) : (f == 1 ? dadd(u, dmul(cN, dlt)) : u);
           if (f == 0 && !isfinite(arg)) gbad_R = 1;
           if (f == 1 && !isfinite(arg)) gbad_N = 1;
-          const double g = loss_grad(a.loss, arg, yi);
+          const double g = F32F ? loss_grad_f32m(a.loss, arg, yi) : loss_grad(a.loss, arg, yi);
           sh.rr[buf][f][r] = f == 2 ? -g : g;
           if (f == 2 && crank == 0 && want_z) conj_accumulate(a.loss, -g, yi, f_acc);
         } else if (crank == 0) {
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
             a.u[2 * n + row] = u;
           }
           if (!isfinite(u)) bad = 1;
-          loss_acc += loss_term(a.loss, u, yi);
+          loss_acc += F32F ? loss_term_f32m(a.loss, u, yi) : loss_term(a.loss, u, yi);
         }
       } else if (f < 4 && f < 3) {
         sh.rr[buf][f][r] = 0.0;
