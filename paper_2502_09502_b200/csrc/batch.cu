@@ -101,6 +101,18 @@ __global__ void kb_warm(BatchArgs g, const double* warm) {
   }
 }
 
+// per-node classes from a compact list (node b: entries [off[b], off[b+1]),
+// its fixed-one indices first, ascending): the mask rows were memset to FREE
+__global__ void kb_fill_nodes(BatchArgs g, const int64_t* off, const int* idx, const uint8_t* cls) {
+  const int64_t b = blockIdx.x;
+  const int64_t e0 = off[b], e1 = off[b + 1];
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int j = idx[e];
+    g.mask[b * g.pv + j] = cls[e];
+    if (cls[e] == FIXED_ONE) g.fone[b * g.fone_stride + (e - e0)] = j;
+  }
+}
+
 __global__ void kb_state_init(BatchArgs g, const double* g0) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.B) return;

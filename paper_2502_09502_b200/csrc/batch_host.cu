@@ -480,6 +480,14 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   if (!Bt->ws) return set_error(L0_INVALID, "batch has no workspace (l0_batch_set_workspace)");
   BatchArgs& g = Bt->g;
   const int64_t p = g.p, B = g.B, pv = g.pv;
+  const bool dbg = getenv("L0_DEBUG") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!dbg) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  batch_solve %-28s %8.3f ms\n", what, std::chrono::duration<double>(now - tq).count() * 1e3);
+    tq = now;
+  };
   std::memset(reps, 0, sizeof(l0_report) * (size_t)B);
   if (g.loss > SQUARED_HINGE) return set_error(L0_UNSUPPORTED, "bound-grade loss: the relaxation solver needs a solver-grade loss");
   if (!(k >= 1 && k <= p)) return set_error(L0_INVALID, "k must satisfy 1 <= k <= p");
@@ -491,36 +499,47 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   if (std::isnan(o->lipschitz))   // fista.py:101: any other L is clamped to >= 1e-12
     return set_error(L0_INVALID, "lipschitz constant is NaN");
   // ---- per-node classes and parameters (model.py:119-149, perspective.py:36-73) ----
-  std::vector<uint8_t> mask((size_t)(B * pv), (uint8_t)FREE);
-  std::vector<int> fone((size_t)(B * g.fone_stride), 0);
+  // compact per-node index lists (fixed-one ascending, then fixed-zero); the
+  // device expands them into the [B][pv] class rows (kb_fill_nodes) -- no
+  // B x p host arrays to build and upload per solve
+  std::vector<int64_t> off((size_t)B + 1, 0);
+  std::vector<int> idx;
+  std::vector<uint8_t> cls;
   std::vector<Params> prm((size_t)B);
+  std::vector<uint8_t> seen((size_t)p, 0);
   for (int64_t b = 0; b < B; ++b) {
     const l0_node* nd = nodes ? &nodes[b] : nullptr;
     int64_t n1 = 0, n0 = 0;
     double parent = -INFINITY;
-    uint8_t* mk = mask.data() + b * pv;
-    std::vector<int> f1;
+    const size_t first = idx.size();
     if (nd) {
       parent = nd->parent_bound;
       n1 = nd->n_fixed_one;
       n0 = nd->n_fixed_zero;
-      for (int64_t i = 0; i < n1; ++i) {
+      int err = ST_OK;
+      std::string msg;
+      for (int64_t i = 0; i < n1 && !err; ++i) {
         const int64_t j = nd->h_fixed_one[i];
-        if (j < 0 || j >= p) return set_error(L0_INVALID, "fixed_one index out of range");
-        if (mk[j] != FREE) return set_error(L0_INVALID, "duplicate fixed index");
-        mk[j] = FIXED_ONE;
-        f1.push_back((int)j);
+        if (j < 0 || j >= p) { err = L0_INVALID; msg = "fixed_one index out of range"; break; }
+        if (seen[j]) { err = L0_INVALID; msg = "duplicate fixed index"; break; }
+        seen[j] = 1;
+        idx.push_back((int)j);
+        cls.push_back((uint8_t)FIXED_ONE);
       }
-      for (int64_t i = 0; i < n0; ++i) {
+      std::sort(idx.begin() + first, idx.end());
+      for (int64_t i = 0; i < n0 && !err; ++i) {
         const int64_t j = nd->h_fixed_zero[i];
-        if (j < 0 || j >= p) return set_error(L0_INVALID, "fixed_zero index out of range");
-        if (mk[j] != FREE) return set_error(L0_INVALID, "fixed_one and fixed_zero must be disjoint");
-        mk[j] = FIXED_ZERO;
+        if (j < 0 || j >= p) { err = L0_INVALID; msg = "fixed_zero index out of range"; break; }
+        if (seen[j]) { err = L0_INVALID; msg = "fixed_one and fixed_zero must be disjoint"; break; }
+        seen[j] = 1;
+        idx.push_back((int)j);
+        cls.push_back((uint8_t)FIXED_ZERO);
       }
+      for (size_t e = first; e < idx.size(); ++e) seen[(size_t)idx[e]] = 0;
+      if (err) return set_error(err, msg);
     }
+    off[(size_t)b + 1] = (int64_t)idx.size();
     if (n1 > k) return set_error(L0_INFEASIBLE, "|fixed_one| exceeds the budget k (node " + std::to_string(b) + ")");
-    std::sort(f1.begin(), f1.end());
-    std::copy(f1.begin(), f1.end(), fone.begin() + b * g.fone_stride);
     const int64_t nfree = p - n1 - n0;
     Params& hp = prm[(size_t)b];
     hp = Params{};
@@ -545,15 +564,29 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
     hp.node_mode = (n1 + n0) > 0 ? 1 : 0;
     hp.loss = g.loss;
   }
+  tick("host node lists + params");
   auto t0 = std::chrono::steady_clock::now();
   cudaStream_t user_s = (cudaStream_t)stream;
   cudaStream_t s = Bt->stream;
   L0_B_TRY(cudaEventRecord(Bt->ev_in, user_s));
   L0_B_TRY(cudaStreamWaitEvent(s, Bt->ev_in, 0));
   L0_B_TRY(cudaMemcpyAsync(g.prm, prm.data(), sizeof(Params) * B, cudaMemcpyHostToDevice, s));
-  L0_B_TRY(cudaMemcpyAsync(g.mask, mask.data(), (size_t)(B * pv), cudaMemcpyHostToDevice, s));
-  L0_B_TRY(cudaMemcpyAsync(g.fone, fone.data(), 4ull * B * g.fone_stride, cudaMemcpyHostToDevice, s));
   int64_t launches = 0;
+  L0_B_TRY(cudaMemsetAsync(g.mask, (int)FREE, (size_t)(B * pv), s));
+  if (!idx.empty()) {
+    // the list rides in the (not yet used) candidate-index scratch: off | idx | cls
+    char* lst = reinterpret_cast<char*>(g.cand_idx);
+    const size_t ob = 8 * off.size(), ib = 4 * idx.size();
+    if (ob + ib + cls.size() > 4ull * B * pv) return set_error(L0_INVALID, "node lists exceed the scratch");
+    L0_B_TRY(cudaMemcpyAsync(lst, off.data(), ob, cudaMemcpyHostToDevice, s));
+    L0_B_TRY(cudaMemcpyAsync(lst + ob, idx.data(), ib, cudaMemcpyHostToDevice, s));
+    L0_B_TRY(cudaMemcpyAsync(lst + ob + ib, cls.data(), cls.size(), cudaMemcpyHostToDevice, s));
+    kb_fill_nodes<<<(unsigned)B, 128, 0, s>>>(g, reinterpret_cast<const int64_t*>(lst),
+                                              reinterpret_cast<const int*>(lst + ob),
+                                              reinterpret_cast<const uint8_t*>(lst + ob + ib));
+    L0_B_TRY(cudaGetLastError());
+    ++launches;
+  }
   if (d_warm && !h_g0) return set_error(L0_INVALID, "warm starts need g(beta_0) per node (h_g0)");
   double* d_g0 = nullptr;
   if (h_g0) {
@@ -580,13 +613,15 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   kb_obj<<<dim3((unsigned)g.rblocks, (unsigned)B), kRowThreads, 0, s>>>(g, MODE_INIT);
   L0_B_TRY(cudaGetLastError());
   launches += 2;
+  tick("uploads + init launches");
   const int G = o->chunk_iterations > 0 ? std::min(o->chunk_iterations, 100) : 10;
   int rc = batch_build_graph(*Bt, G, o->profile ? 1 : 0);
   if (rc) return rc;
+  tick("graph (cached or built)");
   int64_t chunks = 0;
   bool stop_sent = false;
-  double prof_ms[3] = {0.0, 0.0, 0.0};
-  int64_t prof_n = 0;
+  double prof_ms[3] = {0.0, 0.0, 0.0}, prof_gap[3] = {0.0, 0.0, 0.0};
+  int64_t prof_n = 0, prof_gn = 0;
   for (;;) {
     L0_B_TRY(cudaGraphLaunch(Bt->exec, s));
     L0_B_TRY(cudaEventRecord(Bt->ev_chunk, s));
@@ -598,6 +633,17 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
         for (int k2 = 0; k2 < 3; ++k2)
           if (cudaEventElapsedTime(&ms, Bt->ev[(size_t)i * 6 + 2 * k2], Bt->ev[(size_t)i * 6 + 2 * k2 + 1]) == cudaSuccess)
             prof_ms[k2] += ms;
+        // gaps: transpose end -> prox begin, prox end -> forward begin, and
+        // forward end -> next transpose begin (kb_obj, kb_compact, kb_rhs, kb_plan)
+        if (cudaEventElapsedTime(&ms, Bt->ev[(size_t)i * 6 + 1], Bt->ev[(size_t)i * 6 + 2]) == cudaSuccess)
+          prof_gap[0] += ms;
+        if (cudaEventElapsedTime(&ms, Bt->ev[(size_t)i * 6 + 3], Bt->ev[(size_t)i * 6 + 4]) == cudaSuccess)
+          prof_gap[1] += ms;
+        if (i + 1 < G &&
+            cudaEventElapsedTime(&ms, Bt->ev[(size_t)i * 6 + 5], Bt->ev[(size_t)(i + 1) * 6]) == cudaSuccess) {
+          prof_gap[2] += ms;
+          ++prof_gn;
+        }
         ++prof_n;
       }
     }
@@ -611,9 +657,16 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
     }
   }
   launches += chunks * Bt->graph_kernels;
+  tick("chunks (device)");
+  if (o->profile && getenv("L0_DEBUG") && prof_n > 0)
+    fprintf(stderr, "batch profile (ms per iteration): gemm_t %.4f | gap %.4f | prox %.4f | gap %.4f | gemm_f %.4f | "
+            "obj+compact+rhs+plan %.4f\n", prof_ms[0] / prof_n, prof_gap[0] / prof_n, prof_ms[1] / prof_n,
+            prof_gap[1] / prof_n, prof_ms[2] / prof_n, prof_gn ? prof_gap[2] / prof_gn : 0.0);
   // ---- reports and iterates ----------------------------------------------------
+  // the report fields only (the states' probe stamps and trace rings are not read)
   std::vector<State> hs((size_t)B);
-  L0_B_TRY(cudaMemcpyAsync(hs.data(), g.st, sizeof(State) * B, cudaMemcpyDeviceToHost, s));
+  L0_B_TRY(cudaMemcpy2DAsync(hs.data(), sizeof(State), g.st, sizeof(State), offsetof(State, probe), (size_t)B,
+                             cudaMemcpyDeviceToHost, s));
   kb_gather_beta<<<dim3((unsigned)std::min<int64_t>((p + 255) / 256, 64), (unsigned)B), 256, 0, s>>>(g, d_beta_out);
   L0_B_TRY(cudaGetLastError());
   ++launches;
@@ -623,6 +676,7 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   cudaStreamWaitEvent(user_s, ev_out, 0);
   L0_B_TRY(cudaStreamSynchronize(s));
   cudaEventDestroy(ev_out);
+  tick("state D2H + beta gather");
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   int first_err = ST_OK;
   int64_t err_node = -1;

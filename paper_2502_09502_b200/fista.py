@@ -144,22 +144,22 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
     dp = instance.device_problem()
     handle, _ws, _fin = dp.batch(len(nodes))
     o = _native_opts(opts, L)
+    # every node's index lists in one int64 buffer; the Node structs point into it
     arr = (native.Node * len(nodes))()
-    keep = []
-    for i, nd in enumerate(nodes):
-        if nd is None:
-            arr[i].n_fixed_one = 0
-            arr[i].n_fixed_zero = 0
-            arr[i].parent_bound = -math.inf
-            continue
-        f1 = np.ascontiguousarray(nd.fixed_one, dtype=np.int64)
-        f0 = np.ascontiguousarray(nd.fixed_zero, dtype=np.int64)
-        keep += [f1, f0]
-        arr[i].h_fixed_one = f1.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
-        arr[i].n_fixed_one = f1.size
-        arr[i].h_fixed_zero = f0.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
-        arr[i].n_fixed_zero = f0.size
-        arr[i].parent_bound = float(nd.parent_bound)
+    lists = [(tuple(nd.fixed_one), tuple(nd.fixed_zero)) if nd is not None else ((), ()) for nd in nodes]
+    flat = np.fromiter((j for f1, f0 in lists for j in (*f1, *f0)), dtype=np.int64,
+                       count=sum(len(f1) + len(f0) for f1, f0 in lists))
+    keep = [flat]
+    base = flat.ctypes.data
+    pos = 0
+    for i, (nd, (f1, f0)) in enumerate(zip(nodes, lists)):
+        a = arr[i]
+        a.h_fixed_one = ctypes.cast(base + 8 * pos, ctypes.POINTER(ctypes.c_int64))
+        a.n_fixed_one = len(f1)
+        a.h_fixed_zero = ctypes.cast(base + 8 * (pos + len(f1)), ctypes.POINTER(ctypes.c_int64))
+        a.n_fixed_zero = len(f0)
+        a.parent_bound = float(nd.parent_bound) if nd is not None else -math.inf
+        pos += len(f1) + len(f0)
     p = instance.p
     # warm starts (NodeState.warm_start; fista.py:130-137): beta_0 per node and
     # g(beta_0) for the initial objective; cold nodes start at 0 with g = 0
@@ -188,7 +188,7 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
         raise NumericalError(native.last_error(),
                              iteration=int(bad.error_iteration) if bad is not None else None)
     native.check(rc)
-    betas = beta_out if return_device else beta_out.cpu().numpy()
+    betas = beta_out.unbind(0) if return_device else beta_out.cpu().numpy()
     out = []
     for i, r in enumerate(reps):
         out.append(RelaxationReport(

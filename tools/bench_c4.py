@@ -34,3 +34,7 @@ print(f"C4 scale={scale} nodes={count} iters={iters}: {dt*1e3:.1f} ms  "
       f"{count*iters/dt:.0f} node-it/s  {dt/iters*1e3:.3f} ms/batched-iteration", flush=True)
 print("gaps", np.percentile([r.gap for r in reps], [0, 50, 100]), "restarts",
       np.mean([r.restarts for r in reps]))
+
+if __import__("os").environ.get("L0_DEBUG"):
+    solve_relaxation_batched(inst, nodes, opts=FistaOptions(max_iterations=iters, stop_on_gap=False,
+                                                            lipschitz=L, profile=True))
