@@ -204,6 +204,13 @@ int32_t l0_standardize_stats(const double* d_X, int64_t n, int64_t p, int64_t ld
 int32_t l0_standardize_apply(const double* d_X, int64_t n, int64_t ld, const int64_t* d_kept, int64_t m,
                              const double* d_mean, const double* d_norm, double* d_out, void* stream);
 
+/* ---- branch and bound: batched exact ridge refits ---------
+ * C supports of width s <= 48 (device int32, -1 = padding): d_beta (C x s) =
+ * (X_S^T X_S + lambda2 I)^{-1} X_S^T y and d_obj (C) = |y - X_S b|^2 +
+ * lambda2 |b|^2 (yty = y^T y), squared-error refits without the box. */
+int32_t l0_refit_ridge(l0_problem* prob, const int32_t* d_supports, int64_t C, int32_t s, double lambda2,
+                       double yty, double* d_beta, double* d_obj, void* stream);
+
 int32_t l0_ops_workspace_bytes(int64_t len, uint64_t* bytes);
 /* g_mode=0: out = prox_{rho g*}(in) (prox_gstar[_node]); g_mode=1: out =
  * prox_{g/rho}(in) = in - prox_{rho g*}(rho in)/rho (prox_g[_node]).  k is the

@@ -40,6 +40,7 @@ import numpy as np
 from .errors import InfeasibleNodeError, UnsupportedOperationError
 from .fista import FistaOptions, Termination, solve_relaxation_batched
 from .model import LossKind, NodeState, ProblemInstance, is_solver_grade, lipschitz_constant
+from . import native
 from .perspective import safe_lower_bound, safe_lower_bound_batched
 
 __all__ = ["BnBOptions", "Certificate", "CertificateStatus", "beam_search_incumbent",
@@ -103,9 +104,53 @@ def _loss_and_grad(loss: LossKind, u, y):
     raise UnsupportedOperationError(f"{loss.value} is not solver-grade")
 
 
+_REFIT_MAX_S = 48   # csrc/refit.cu kRefitMaxS
+
+
 def _refit(instance: ProblemInstance, supports: Sequence[Tuple[int, ...]], iters: int):
+    """min F(X_S b) + l2 |b|^2, |b| <= M, for every support at once: squared
+    error solves the ridge problems exactly on the device (l0_refit_ridge:
+    batched Gram + Cholesky, one launch) and keeps them where the box does not
+    bind; the rest (binding box, other losses) runs accelerated projected
+    gradient.  Returns (list of dense betas, objectives)."""
+    import torch
+    dp = _dev(instance)
+    p = instance.p
+    C = len(supports)
+    s = max(1, max(len(S) for S in supports))
+    if instance.loss is LossKind.SQUARED_ERROR and s <= _REFIT_MAX_S:
+        from . import _device
+        sup = np.full((C, s), -1, dtype=np.int32)
+        for c, S in enumerate(supports):
+            sup[c, :len(S)] = S
+        sup_d = torch.from_numpy(sup).to(dp.X.device)
+        bd = torch.empty((C, s), dtype=torch.float64, device=dp.X.device)
+        od = torch.empty(C, dtype=torch.float64, device=dp.X.device)
+        if getattr(dp, "_yty", None) is None:
+            dp._yty = float(torch.dot(dp.y, dp.y))
+        native.check(native.lib().l0_refit_ridge(dp.handle, sup_d.data_ptr(), C, s, float(instance.lambda2),
+                                                 dp._yty, bd.data_ptr(), od.data_ptr(),
+                                                 _device.stream_handle()))
+        bh, objs = bd.cpu().numpy(), od.cpu().numpy()
+        viol = [c for c in range(C) if np.any(np.abs(bh[c]) > float(instance.M))]
+        betas = []
+        for c, S in enumerate(supports):
+            beta = np.zeros(p)
+            if S:
+                beta[list(S)] = bh[c, :len(S)]
+            betas.append(beta)
+        if viol:   # the box binds: projected gradient from the clamped ridge point
+            vb, vo = _refit_pg(instance, [supports[c] for c in viol], iters,
+                               start=[np.clip(bh[c], -float(instance.M), float(instance.M)) for c in viol])
+            for i, c in enumerate(viol):
+                betas[c], objs[c] = vb[i], vo[i]
+        return betas, objs
+    return _refit_pg(instance, supports, iters)
+
+
+def _refit_pg(instance: ProblemInstance, supports: Sequence[Tuple[int, ...]], iters: int, start=None):
     """Projected gradient descent of min F(X_S b) + l2 |b|^2, |b| <= M, for
-    every support at once.  Returns (list of dense betas, objectives)."""
+    every support at once (squared error: exact ridge first, as the start)."""
     import torch
     dp = _dev(instance)
     p = instance.p
@@ -125,7 +170,10 @@ def _refit(instance: ProblemInstance, supports: Sequence[Tuple[int, ...]], iters
     L = _CURV[instance.loss] * (Xs * Xs).sum(dim=(1, 2)) + 2.0 * lam2 + 1e-12   # >= curvature
     b = torch.zeros((C, s), dtype=torch.float64, device=dp.X.device)
     todo = torch.ones(C, dtype=torch.bool, device=dp.X.device)
-    if instance.loss is LossKind.SQUARED_ERROR:
+    if start is not None:
+        for c, b0 in enumerate(start):
+            b[c, :len(b0)] = torch.from_numpy(np.asarray(b0[:s], dtype=np.float64))
+    elif instance.loss is LossKind.SQUARED_ERROR:
         # exact ridge solution per support; projected gradient only where the box binds
         G = torch.einsum("csn,ctn->cst", Xs, Xs) + lam2 * torch.eye(s, dtype=torch.float64,
                                                                      device=dp.X.device)

@@ -87,6 +87,7 @@ _PROTOS = {
                                             c_u64, c_vp]),
     "l0_standardize_stats": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "l0_standardize_apply": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "l0_refit_ridge": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_f64, c_vp, c_vp, c_vp]),
     "l0_ops_workspace_bytes": (c_i32, [c_i64, ctypes.POINTER(c_u64)]),
     "l0_prox": (c_i32, [c_vp, c_i64, c_f64, c_i64, c_f64, c_vp, c_i32, c_vp, c_vp,
                         ctypes.POINTER(c_i64), c_vp, c_u64, c_vp]),

@@ -95,3 +95,32 @@ def test_certify_logistic_matches_enumeration(seed):
     if cert.status is CertificateStatus.OPTIMAL:
         assert cert.incumbent_objective == pytest.approx(obj, rel=1e-5)
     assert cert.status in (CertificateStatus.OPTIMAL, CertificateStatus.GAP_LIMIT)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_refit_ridge_kernel_matches_numpy(dtype):
+    """l0_refit_ridge (csrc/refit.cu): batched exact ridge refits on supports
+    of mixed sizes (1..48, padded), vs numpy's solve on the same (fp64-upcast)
+    columns; objectives |y - X_S b|^2 + l2 |b|^2 at 1e-10."""
+    import numpy as np
+    from paper_2502_09502_b200 import LossKind, ProblemInstance
+    from paper_2502_09502_b200.bnb import _refit
+    rng = np.random.default_rng(7)
+    n, p, lam2 = 700, 120, 0.37
+    X = rng.standard_normal((n, p))
+    if dtype == "fp32":
+        X = X.astype(np.float32)
+    y = rng.standard_normal(n) * 3.0
+    inst = ProblemInstance(X, y, LossKind.SQUARED_ERROR, 48, 1e6, lam2, dtype=dtype)
+    sizes = [1, 2, 5, 8, 13, 31, 48, 0, 7]
+    supports = [tuple(sorted(rng.choice(p, size=k, replace=False).tolist())) for k in sizes]
+    betas, objs = _refit(inst, supports, 10)
+    X64 = X.astype(np.float64)
+    for S, beta, obj in zip(supports, betas, objs):
+        XS = X64[:, list(S)]
+        b = np.linalg.solve(XS.T @ XS + lam2 * np.eye(len(S)), XS.T @ y) if S else np.zeros(0)
+        ref = np.zeros(p)
+        ref[list(S)] = b
+        np.testing.assert_allclose(beta, ref, rtol=1e-9, atol=1e-11)
+        r = y - XS @ b
+        assert obj == pytest.approx(float(r @ r + lam2 * b @ b), rel=1e-10)
