@@ -261,7 +261,8 @@ int32_t l0_batch_set_workspace(l0_batch* batch, void* d_ws, uint64_t bytes);
 int32_t l0_batch_solve(l0_batch* batch, int64_t k, double M, double lambda2,
                        const l0_fista_opts* opts, const l0_node* nodes /* n_nodes, nullable */,
                        const double* d_warm /* nullable, n_nodes x p warm starts */,
-                       const double* h_g0 /* with d_warm: g(beta_0) per node (l0_g_value) */,
+                       const double* h_g0 /* nullable: g(beta_0) per node; with d_warm and
+                                             h_g0 NULL the engine evaluates it (kb_g0) */,
                        double* d_beta_out, l0_report* reps, void* stream);
 int32_t l0_batch_destroy(l0_batch* batch);
 

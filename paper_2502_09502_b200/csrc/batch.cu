@@ -113,6 +113,86 @@ __global__ void kb_fill_nodes(BatchArgs g, const int64_t* off, const int* idx, c
   }
 }
 
+// g(beta_0) of each node's warm start (perspective.py:76-132, the per-node
+// envelope of the initial composite objective, fista.py:143) -- one CTA per
+// node: fixed-zero / fixed-one / box / budget feasibility, then the top
+// k_g free magnitudes (radix selection + rank sort) into the majorization
+// greedy (envelope_from_top), as the single engine's envelope_of.
+__global__ void __launch_bounds__(512) kb_g0(BatchArgs g, const double* __restrict__ warm, double* __restrict__ g0) {
+  __shared__ SelectSmem sel;
+  __shared__ double red[32];
+  __shared__ double cand[kCandCap], cand2[kCandCap];
+  __shared__ int ncand;
+  __shared__ double s_gfree;
+  const int64_t b = blockIdx.x, p = g.p;
+  const Params* P = g.prm + b;
+  const double* w = warm + b * p;
+  const uint8_t* mk = g.mask + b * g.pv;
+  double* mag = g.scratch + b * g.pv;   // |beta| on free coordinates, -1 elsewhere
+  const double M = P->M, Mtol = dmul(M, dadd(1.0, kFeasRtol));
+  double total = 0.0, amax = 0.0, s2 = 0.0;
+  int bad = 0;
+  for (int64_t j = threadIdx.x; j < p; j += blockDim.x) {
+    const double x = w[j];
+    const int c = mk[j];
+    if (c == FREE) {
+      const double a = fabs(x);
+      mag[j] = a;
+      total += a;
+      amax = fmax(amax, a);
+    } else {
+      mag[j] = -1.0;
+      if (c == FIXED_ZERO && fabs(x) > kZeroAtol) bad = 1;
+      if (c == FIXED_ONE) {
+        if (fabs(x) > Mtol) bad = 1;
+        s2 = fma(x, x, s2);
+      }
+    }
+  }
+  total = block_sum(total, red);
+  amax = block_max(amax, red);
+  s2 = block_sum(s2, red);
+  bad = __syncthreads_or(bad);
+  const int64_t nf = P->n_free, kg = P->k_g;
+  int path = 0;
+  if (bad) path = 3;
+  else if (nf == 0 || kg == 0) path = 2;
+  else if (amax > Mtol || total > dmul(dmul((double)kg, M), dadd(1.0, kFeasRtol))) path = 3;
+  double gfree = 0.0;
+  if (path == 0) {
+    const int64_t kk = kg < nf ? kg : nf;
+    if (kk > kCandCap) {   // beyond the on-chip top-k: flag (the host checks n_free / k)
+      path = 3;
+    } else {
+      double tau;
+      int64_t cgt;
+      block_kth_largest(mag, p, kk, sel, &tau, &cgt);
+      if (threadIdx.x == 0) ncand = 0;
+      __syncthreads();
+      for (int64_t j = threadIdx.x; j < p; j += blockDim.x)
+        if (mag[j] > tau) cand[atomicAdd(&ncand, 1)] = mag[j];
+      __syncthreads();
+      for (int64_t i = cgt + threadIdx.x; i < kk; i += blockDim.x) cand[i] = tau;
+      __syncthreads();
+      block_rank_sort_desc(cand, cand2, (int)kk);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double gv = envelope_from_top(cand2, kk, total);
+        if (threadIdx.x == 0) s_gfree = gv;
+      }
+      __syncthreads();
+      gfree = s_gfree;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double v;
+    if (path == 3) v = CUDART_INF;
+    else if (P->node_mode) v = dadd(dadd(0.0, dmul(0.5, s2)), gfree);
+    else v = gfree;
+    g0[b] = v;
+  }
+}
+
 __global__ void kb_state_init(BatchArgs g, const double* g0) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.B) return;

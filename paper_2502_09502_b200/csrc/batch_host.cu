@@ -587,12 +587,19 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
     L0_B_TRY(cudaGetLastError());
     ++launches;
   }
-  if (d_warm && !h_g0) return set_error(L0_INVALID, "warm starts need g(beta_0) per node (h_g0)");
   double* d_g0 = nullptr;
   if (h_g0) {
     // g(beta_0) per node rides in the per-node gv scratch until the state init reads it
     d_g0 = g.gv;   // [B][3 pv + 8] doubles: the first B doubles are free at this point
     L0_B_TRY(cudaMemcpyAsync(d_g0, h_g0, 8ull * B, cudaMemcpyHostToDevice, s));
+  } else if (d_warm) {
+    if (k > kCandCap)
+      return set_error(L0_UNSUPPORTED, "warm starts with k > 2048 need g(beta_0) per node (h_g0)");
+    // g(beta_0) of every warm start on the device (kb_g0: one CTA per node)
+    d_g0 = g.gv;
+    kb_g0<<<(unsigned)B, 512, 0, s>>>(g, d_warm, d_g0);
+    L0_B_TRY(cudaGetLastError());
+    ++launches;
   }
   kb_state_init<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(g, d_g0);
   ++launches;

@@ -163,11 +163,10 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
     p = instance.p
     # warm starts (NodeState.warm_start; fista.py:130-137): beta_0 per node and
     # g(beta_0) for the initial objective; cold nodes start at 0 with g = 0
+    # g(beta_0) of the warm starts is evaluated by the engine (kb_g0)
     warm = g0 = None
     if any(nd is not None and getattr(nd, "warm_start", None) is not None for nd in nodes):
-        from .perspective import g_value
         warm = torch.zeros((len(nodes), p), dtype=torch.float64, device=dp.X.device)
-        g0 = np.zeros(len(nodes))
         for i, nd in enumerate(nodes):
             ws = getattr(nd, "warm_start", None) if nd is not None else None
             if ws is None:
@@ -176,7 +175,6 @@ def solve_relaxation_batched(instance: ProblemInstance, nodes, opts: Optional[Fi
             if tuple(w.shape) != (p,):
                 raise InvalidInputError("warm start has the wrong dimension")
             warm[i].copy_(w)
-            g0[i] = g_value(w, params[i])
     beta_out = torch.empty((len(nodes), p), dtype=torch.float64, device=dp.X.device)
     reps = (native.Report * len(nodes))()
     rc = lib.l0_batch_solve(handle, int(instance.k), float(instance.M), float(instance.lambda2),
