@@ -71,6 +71,31 @@ struct BatchArgs {
   double* slab_below;
   double* slab_hfone;
   double* slab_htop;  // [B][S][kHTop]
+  int sf_init;        // split-K partials of the dense MODE_INIT forward contraction
+  // Support-compacted forward contraction (sparse_fwd).  The forward operand
+  // (the step beta_t - beta_{t-1}, or beta_t on re-syncs) is zero outside the
+  // nodes' prox supports: every coordinate past the PAVA pool end is a tail
+  // singleton whose output is gamma - mu / rho = 0 (prox.py:104-116 with
+  // nu = x).  On C4 a node's step has ~300 nonzeros of 5000 and the union over
+  // the batch ~500, so GEMM_F contracts only the X columns of that union:
+  // a slot cache of X columns (hi/lo, gathered from X^T once per new column)
+  // and the operand rows compacted to the same slots.  Exact zeros contribute
+  // nothing to the fp32 accumulation, so this is the dense product's value.
+  int sparse_fwd;
+  int* umask;         // [pp] nonzero forward operand in some node (kb_window sets, kb_union clears)
+  int* slot_of;       // [pp] slot of column j (-1: not cached)
+  int* col_of;        // [pp] column cached in slot s (-1: free)
+  int* uctl;          // [0] slots in use, [1..2] slots to gather [s0, s1), [3] GEMM_F K (slots
+                      // rounded up to 32), [4] rebuilds, [5] columns gathered (statistics)
+  const float* xth;   // X^T hi/lo (p x nn): the gather source (coalesced rows)
+  const float* xtl;
+  float* xuh;         // [n][pp] cached X columns by slot (GEMM_F A operand)
+  float* xul;
+  float* bsh;         // [B][pp] forward operand by slot (GEMM_F B operand)
+  float* bsl;
+  int* fx_n;          // [B] fixed-one columns of node b outside the cache with a nonzero step
+  int* fx_j;          // [B][kFoneDirect] their ids
+  double* fx_v;       // [B][kFoneDirect] and steps (kb_gather -> kb_obj)
 };
 
 constexpr int kRowThreads = 256;
@@ -80,6 +105,9 @@ constexpr int kRowsPerBlock = 2048;
 // so the restart test F(u_t) + ... >= previous (fista.py:168) sees accurate
 // differences; every kResync iterations u is recomputed from beta_t.
 constexpr int64_t kResync = 40;
+// sparse_fwd: nodes with at most this many fixed-one coordinates get their
+// step on those columns added by kb_obj (fp64) unless the column is cached
+constexpr int kFoneDirect = 32;
 __device__ __forceinline__ bool resync_at(int64_t t) { return t % kResync == 0; }
 
 __device__ __forceinline__ int64_t gvs(const BatchArgs& g) { return 3 * g.pv + 8; }
@@ -448,11 +476,178 @@ __global__ void __launch_bounds__(kWinThreads, 1) kb_window(BatchArgs g) {
   const double* out = a.beta + ring(t) * g.pv;
   const double* bprev = a.beta + ring(t - 1) * g.pv;
   const int64_t pos = g.slot[b];                      // compacted contraction row
+  const bool direct_fone = a.prm->node_mode && a.prm->n_fone <= kFoneDirect;
   for (int64_t j = threadIdx.x; j < g.pp; j += kWinThreads) {
     float h = 0.f, l = 0.f;
     if (j < g.p) tf32_split(full ? out[j] : dsub(out[j], bprev[j]), h, l);
     g.bh[pos * g.pp + j] = h;
     g.bl[pos * g.pp + j] = l;
+    // a node's few fixed-one columns stay out of the shared column cache (they
+    // would widen every node's contraction for one node's sake); kb_obj adds
+    // their step in fp64 instead
+    if (g.sparse_fwd && (h != 0.f || l != 0.f) && !(direct_fone && a.mask[j] == FIXED_ONE)) g.umask[j] = 1;
+  }
+}
+
+// rank of this thread's flag among the block's set flags (thread order) and
+// the block total; all threads call it
+__device__ __forceinline__ int block_flag_rank(int f, int* wtot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) wtot[warp] = __popc(m);
+  __syncthreads();
+  int off = 0, tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    const int c = wtot[w];
+    if (w < warp) off += c;
+    tot += c;
+  }
+  __syncthreads();
+  *total = tot;
+  return off + __popc(m & ((1u << lane) - 1u));
+}
+
+// Union of the forward operand's supports over the nodes -> slots of the X
+// column cache.  New columns are appended (ascending index) after the slots
+// in use; when the stale slots (columns no longer in the union, operand 0
+// there) would exceed a quarter of the union, the cache is rebuilt compactly.
+// kb_gather then fetches the X columns of the slots [s0, s1) only: in steady
+// state the union is unchanged and nothing is gathered.
+__global__ void __launch_bounds__(1024) kb_union(BatchArgs g) {
+  __shared__ int wtot[32];
+  __shared__ int red[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t p = g.p;
+  int cu = 0, cn = 0;
+  for (int64_t j = tid; j < p; j += blockDim.x) {
+    const int m = g.umask[j];
+    cu += m;
+    cn += (m && g.slot_of[j] < 0) ? 1 : 0;
+  }
+  cu = __reduce_add_sync(0xffffffffu, cu);
+  cn = __reduce_add_sync(0xffffffffu, cn);
+  if (lane == 0) { red[0][warp] = cu; red[1][warp] = cn; }
+  __syncthreads();
+  cu = 0;
+  cn = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { cu += red[0][w]; cn += red[1][w]; }
+  const int ext0 = g.uctl[0];
+  const bool rebuild = ext0 + cn > cu + cu / 4 + 64 || ext0 + cn > (int)g.pp;
+  if (rebuild) {
+    for (int s = tid; s < ext0; s += blockDim.x) {
+      const int j = g.col_of[s];
+      if (j >= 0) g.slot_of[j] = -1;
+      g.col_of[s] = -1;
+    }
+    __syncthreads();
+  }
+  int base = rebuild ? 0 : ext0;
+  for (int64_t j0 = 0; j0 < p; j0 += blockDim.x) {
+    const int64_t j = j0 + tid;
+    const int m = j < p ? g.umask[j] : 0;
+    const int f = m && (rebuild || g.slot_of[j] < 0);
+    int tot;
+    const int r = block_flag_rank(f, wtot, &tot);
+    if (f) {
+      g.slot_of[j] = base + r;
+      g.col_of[base + r] = (int)j;
+    }
+    if (m) g.umask[j] = 0;
+    base += tot;
+  }
+  if (tid == 0) {
+    const int s0 = rebuild ? 0 : ext0;
+    g.uctl[0] = base;
+    g.uctl[1] = s0;
+    g.uctl[2] = base;
+    g.uctl[3] = min((base + 31) / 32 * 32, (int)g.pp);
+    if (rebuild) g.uctl[4] += 1;
+    g.uctl[5] += base - s0;
+  }
+}
+
+// (1) X columns of the new slots [s0, s1) from X^T (32 slots x 64 rows per
+// item through shared memory: coalesced reads along rows of X^T, 128-byte
+// row segments written); (2) the forward operand rows by slot (zero in free
+// slots and in the padding up to the K of GEMM_F).  Persistent grid.
+constexpr int kGatherRows = 64;
+__global__ void __launch_bounds__(256) kb_gather(BatchArgs g) {
+  __shared__ float th[32][kGatherRows + 1], tl[32][kGatherRows + 1];
+  const int s0 = g.uctl[1], s1 = g.uctl[2], kpad = g.uctl[3];
+  const int64_t n = g.n, pp = g.pp, nn = g.nn;
+  const int rtiles = (int)((n + kGatherRows - 1) / kGatherRows);
+  const int items = rtiles * ((s1 - s0 + 31) / 32);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int sb = s0 + (it / rtiles) * 32;
+    const int64_t r0 = (int64_t)(it % rtiles) * kGatherRows;
+    for (int i = ty; i < 32; i += 8) {
+      const int sl = sb + i;
+      const int j = sl < s1 ? g.col_of[sl] : -1;
+      for (int c = tx; c < kGatherRows; c += 32) {
+        const int64_t r = r0 + c;
+        float h = 0.f, l = 0.f;
+        if (j >= 0 && r < n) {
+          h = __ldg(g.xth + (int64_t)j * nn + r);
+          l = __ldg(g.xtl + (int64_t)j * nn + r);
+        }
+        th[i][c] = h;
+        tl[i][c] = l;
+      }
+    }
+    __syncthreads();
+    for (int c = ty; c < kGatherRows; c += 8) {
+      const int64_t r = r0 + c;
+      const int sl = sb + tx;
+      if (r < n && sl < s1) {
+        g.xuh[r * pp + sl] = th[tx][c];
+        g.xul[r * pp + sl] = tl[tx][c];
+      }
+    }
+    __syncthreads();
+  }
+  // per node: its fixed-one columns that stay outside the cache, with their
+  // step (fp64), for kb_obj -- one warp per node
+  {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = gw; b < g.B; b += nw) {
+      const Params* P = g.prm + b;
+      const State* st = g.st + b;
+      if (!P->node_mode || P->n_fone > kFoneDirect || st->done || st->dual_only) continue;
+      const int64_t t = st->t + 1;
+      const bool full = resync_at(t);
+      int j = -1;
+      double v = 0.0;
+      if (lane < P->n_fone) {
+        j = g.fone[b * g.fone_stride + lane];
+        const double bt = g.beta[(b * 3 + ring(t)) * g.pv + j];
+        v = full ? bt : dsub(bt, g.beta[(b * 3 + ring(t - 1)) * g.pv + j]);
+        if (g.slot_of[j] >= 0 || v == 0.0) j = -1;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
+      if (j >= 0) {
+        const int r = __popc(m & ((1u << lane) - 1u));
+        g.fx_j[b * kFoneDirect + r] = j;
+        g.fx_v[b * kFoneDirect + r] = v;
+      }
+      if (lane == 0) g.fx_n[b] = __popc(m);
+    }
+  }
+  const int64_t rows = g.flags[3];
+  const int64_t tot = rows * kpad;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / kpad;
+    const int sl = (int)(e - r * kpad);
+    const int j = g.col_of[sl];
+    float h = 0.f, l = 0.f;
+    if (j >= 0) {
+      h = g.bh[r * pp + j];
+      l = g.bl[r * pp + j];
+    }
+    g.bsh[r * pp + sl] = h;
+    g.bsl[r * pp + sl] = l;
   }
 }
 
@@ -477,7 +672,24 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
   // compacted contraction row (MODE_INIT: every node, slot = node)
   const float* cfb = g.cf + (mode == MODE_ITER ? (int64_t)g.slot[b] : b) * nn;
   const int64_t cstride = B * nn;
-  const int sf = g.sf;
+  // fixed-one columns outside the column cache (sparse_fwd, see kb_window):
+  // u += X[:, j] * step_j in fp64, X[:, j] = hi + lo of X^T's row j (exact);
+  // the (j, step) list was made by kb_gather
+  __shared__ int fx_j[kFoneDirect];
+  __shared__ double fx_v[kFoneDirect];
+  const Params* Pb = g.prm + b;
+  const bool fx = mode == MODE_ITER && g.sparse_fwd && Pb->node_mode && Pb->n_fone <= kFoneDirect;
+  int fx_n = 0;
+  if (fx) {
+    fx_n = g.fx_n[b];
+    if (threadIdx.x < fx_n) {
+      fx_j[threadIdx.x] = g.fx_j[b * kFoneDirect + threadIdx.x];
+      fx_v[threadIdx.x] = g.fx_v[b * kFoneDirect + threadIdx.x];
+    }
+    __syncthreads();
+  }
+  const int nfx = fx_n;
+  const int sf = mode == MODE_ITER ? g.sf : g.sf_init;
   const int i0 = (int)r0, i1 = (int)r1;
   // two rows per thread per step (16-byte loads; nn and r0 are even); two
   // steps unrolled so their loads are in flight together
@@ -502,6 +714,14 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
       yv[0] = g.y[i];
       yv[1] = 0.0;
       if (delta) upv[0] = uprev[i];
+    }
+    for (int e = 0; e < nfx; ++e) {
+      const int64_t o = (int64_t)fx_j[e] * nn + i;   // even: 8-byte aligned pairs
+      const double v = fx_v[e];
+      const float2 xh = __ldg(reinterpret_cast<const float2*>(g.xth + o));
+      const float2 xl = __ldg(reinterpret_cast<const float2*>(g.xtl + o));
+      u[0] = fma((double)xh.x + (double)xl.x, v, u[0]);
+      if (two) u[1] = fma((double)xh.y + (double)xl.y, v, u[1]);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -578,6 +798,12 @@ __global__ void kb_request_stop(BatchArgs g, int term) {
 }
 
 inline int64_t kb_prox_capacity() { return (int64_t)kWinThreads * kK2Slab; }
+
+cudaError_t kb_sparse_fwd_prep(const BatchArgs& g, int grid, cudaStream_t s) {
+  kb_union<<<1, 1024, 0, s>>>(g);
+  kb_gather<<<grid, 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
 
 cudaError_t kb_prox_launch(const BatchArgs& g, cudaStream_t s) {
   kb_step<<<dim3((unsigned)g.S, (unsigned)g.B), kK2Slab, 0, s>>>(g);

@@ -24,8 +24,10 @@ struct Batch {
   uint64_t ws_bytes = 0;
   void* ws = nullptr;
   float *xh = nullptr, *xl = nullptr, *xth = nullptr, *xtl = nullptr;
-  TcGemmArgs gf{}, gt{};
+  TcGemmArgs gf{}, gt{}, gfs{};   // forward (dense: MODE_INIT), transpose, forward (support-compacted)
   CUtensorMap m_xh{}, m_xl{}, m_xth{}, m_xtl{}, m_bh{}, m_bl{}, m_rh{}, m_rl{};
+  CUtensorMap m_xuh{}, m_xul{}, m_bsh{}, m_bsl{};
+  int sparse = 1;                // support-compacted forward contraction (L0_SPARSE_FWD=0: dense)
   int* h_flags = nullptr;   // pinned mirror of flags[0..8)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_chunk = nullptr;
@@ -89,6 +91,22 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
   g.slot = (int*)take(4ull * B);
   Bt.sk_part = Bt.streamk ? (float*)take(4ull * Bt.sms * kTcBN * kTcBM) : nullptr;
   Bt.sk_flag = Bt.streamk ? (int*)take(4ull * Bt.sms) : nullptr;
+  g.sparse_fwd = Bt.sparse;
+  if (Bt.sparse) {
+    g.umask = (int*)take(4ull * pp);
+    g.slot_of = (int*)take(4ull * pp);
+    g.col_of = (int*)take(4ull * pp);
+    g.uctl = (int*)take(4ull * 8);
+    g.xuh = (float*)take(4ull * n * pp);
+    g.xul = (float*)take(4ull * n * pp);
+    g.bsh = (float*)take(4ull * B * pp);
+    g.bsl = (float*)take(4ull * B * pp);
+    g.fx_n = (int*)take(4ull * B);
+    g.fx_j = (int*)take(4ull * B * kFoneDirect);
+    g.fx_v = (double*)take(8ull * B * kFoneDirect);
+    g.xth = Bt.xth;
+    g.xtl = Bt.xtl;
+  }
   return off + 1024;
 }
 
@@ -125,7 +143,13 @@ static int batch_iteration(Batch& Bt, cudaStream_t s, cudaEvent_t* ev) {
   L0_B_TRY(kb_prox_launch(g, s));
   L0_B_TRY(rec(3));
   L0_B_TRY(rec(4));
-  L0_B_TRY(tc_gemm_launch(Bt.m_xh, Bt.m_xl, Bt.m_bh, Bt.m_bl, Bt.gf, std::min(Bt.gf.units, Bt.sms), s));
+  if (Bt.sparse) {
+    // union of the operand supports -> X column cache, then the compacted contraction
+    L0_B_TRY(kb_sparse_fwd_prep(g, Bt.sms * 4, s));
+    L0_B_TRY(tc_gemm_launch(Bt.m_xuh, Bt.m_xul, Bt.m_bsh, Bt.m_bsl, Bt.gfs, std::min(Bt.gfs.units, Bt.sms), s));
+  } else {
+    L0_B_TRY(tc_gemm_launch(Bt.m_xh, Bt.m_xl, Bt.m_bh, Bt.m_bl, Bt.gf, std::min(Bt.gf.units, Bt.sms), s));
+  }
   L0_B_TRY(rec(5));
   kb_obj<<<rgrid, kRowThreads, 0, s>>>(g, MODE_ITER);
   L0_B_TRY(cudaGetLastError());
@@ -240,7 +264,8 @@ static cudaError_t tune_splits(Batch& Bt, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   e = tune_one(Bt, Bt.gt, Bt.m_xth, Bt.m_xtl, Bt.m_rh, Bt.m_rl, Bt.sct_cap, s);
   if (e != cudaSuccess) return e;
-  g.sf = Bt.gf.S;
+  g.sf_init = Bt.gf.S;
+  g.sf = Bt.sparse ? Bt.gfs.S : Bt.gf.S;
   g.sct = Bt.gt.S;
   return cudaMemsetAsync(g.flags, 0, 4ull * 8, s);
 }
@@ -373,7 +398,16 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
       t->streamk = 1;
     }
   }
-  g.sf = gf.S;
+  // support-compacted forward (K = the cached columns, read on the device):
+  // a few dozen K blocks per unit at steady state, so two splits fill the SMs
+  Bt->sparse = getenv("L0_SPARSE_FWD") ? atoi(getenv("L0_SPARSE_FWD")) : 1;
+  TcGemmArgs& gfs = Bt->gfs;
+  gfs = gf;
+  gfs.S = getenv("L0_TC_SFS") ? std::max(1, atoi(getenv("L0_TC_SFS"))) : 2;
+  gfs.units = gfs.S * gfs.m_tiles * gfs.n_tiles;
+  gfs.streamk = 0;
+  g.sf_init = gf.S;
+  g.sf = Bt->sparse ? gfs.S : gf.S;
   g.sct = gt.S;
   // partial capacity for the measured split choice (l0_batch_set_workspace)
   Bt->sf_cap = std::max(gf.S, std::min(8, std::max(1, gf.kb_total / 8)));
@@ -383,7 +417,8 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   Bt->sct_cap = gt.S;
   if (getenv("L0_TC_SF")) Bt->sf_cap = gf.S;
   if (getenv("L0_TC_ST")) Bt->sct_cap = gt.S;
-  if (Bt->streamk) Bt->sf_cap = Bt->sct_cap = 1;
+  if (Bt->sparse) Bt->sf_cap = std::max(Bt->sf_cap, gfs.S);
+  if (Bt->streamk) Bt->sf_cap = Bt->sct_cap = std::max(1, Bt->sparse ? gfs.S : 1);
   Bt->ws_bytes = batch_carve(*Bt, nullptr);
   cudaError_t e = cudaStreamCreateWithFlags(&Bt->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&Bt->ev_in, cudaEventDisableTiming);
@@ -438,6 +473,26 @@ int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
   rc |= tc_make_map(&Bt->m_bl, g.bl, g.B, p, g.pp, kTcBN);
   rc |= tc_make_map(&Bt->m_rh, g.rh, 2 * g.B, n, g.nn, kTcBN);
   rc |= tc_make_map(&Bt->m_rl, g.rl, 2 * g.B, n, g.nn, kTcBN);
+  if (Bt->sparse) {
+    rc |= tc_make_map(&Bt->m_xuh, g.xuh, n, p, g.pp, kTcBM);
+    rc |= tc_make_map(&Bt->m_xul, g.xul, n, p, g.pp, kTcBM);
+    rc |= tc_make_map(&Bt->m_bsh, g.bsh, g.B, p, g.pp, kTcBN);
+    rc |= tc_make_map(&Bt->m_bsl, g.bsl, g.B, p, g.pp, kTcBN);
+    L0_B_TRY(cudaMemsetAsync(g.umask, 0, 4ull * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.slot_of, 0xff, 4ull * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.col_of, 0xff, 4ull * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.uctl, 0, 4ull * 8, s));
+    L0_B_TRY(cudaMemsetAsync(g.xuh, 0, 4ull * n * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.xul, 0, 4ull * n * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bsh, 0, 4ull * g.B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bsl, 0, 4ull * g.B * g.pp, s));
+    TcGemmArgs& gfs = Bt->gfs;
+    gfs.ldc = g.nn;
+    gfs.c_split = g.B * g.nn;
+    gfs.C = g.cf;
+    gfs.n_active = g.flags + 3;
+    gfs.k_active = g.uctl + 3;
+  }
   if (rc) return set_error(L0_CUDA, "cuTensorMapEncodeTiled failed");
   TcGemmArgs& gf = Bt->gf;
   gf.ldc = g.nn;

@@ -97,12 +97,12 @@ __device__ __forceinline__ int64_t sk_start(int64_t total, int c, int G) { retur
 
 struct SegIter {
   const TcGemmArgs& g;
-  int nt_live, units;
+  int nt_live, units, kbt;
   int64_t step, end, total;   // stream-K
   int u;                      // split-K
-  __device__ SegIter(const TcGemmArgs& g_, int ntl) : g(g_), nt_live(ntl) {
+  __device__ SegIter(const TcGemmArgs& g_, int ntl, int kbt_) : g(g_), nt_live(ntl), kbt(kbt_) {
     units = g.S * g.m_tiles * nt_live;
-    total = (int64_t)g.m_tiles * nt_live * g.kb_total;
+    total = (int64_t)g.m_tiles * nt_live * kbt;
     step = sk_start(total, blockIdx.x, gridDim.x);
     end = sk_start(total, blockIdx.x + 1, gridDim.x);
     u = blockIdx.x;
@@ -110,13 +110,13 @@ struct SegIter {
   __device__ bool next(Seg& r) {
     if (g.streamk) {
       if (step >= end) return false;
-      const int64_t tile = step / g.kb_total;
+      const int64_t tile = step / kbt;
       r.s = 0;
       r.nt = (int)(tile % nt_live);
       r.mt = (int)(tile / nt_live);
-      r.kb0 = (int)(step - tile * g.kb_total);
-      r.kb1 = (int)min((int64_t)g.kb_total, (int64_t)r.kb0 + (end - step));
-      r.kind = r.kb0 > 0 ? 1 : (r.kb1 < g.kb_total ? 2 : 0);
+      r.kb0 = (int)(step - tile * kbt);
+      r.kb1 = (int)min((int64_t)kbt, (int64_t)r.kb0 + (end - step));
+      r.kind = r.kb0 > 0 ? 1 : (r.kb1 < kbt ? 2 : 0);
       step += r.kb1 - r.kb0;
       return true;
     }
@@ -125,8 +125,8 @@ struct SegIter {
     const int rest = u / nt_live;
     r.mt = rest % g.m_tiles;
     r.s = rest / g.m_tiles;
-    r.kb0 = (int)(((int64_t)g.kb_total * r.s) / g.S);
-    r.kb1 = (int)(((int64_t)g.kb_total * (r.s + 1)) / g.S);
+    r.kb0 = (int)(((int64_t)kbt * r.s) / g.S);
+    r.kb1 = (int)(((int64_t)kbt * (r.s + 1)) / g.S);
     r.kind = 0;
     u += gridDim.x;
     return true;
@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_act = g.n_active ? (int64_t)*g.n_active : g.N;
   const int nt_live = (int)min((int64_t)g.n_tiles, (n_act + kTcBN - 1) / kTcBN);
+  const int kbt = g.k_active ? (int)min((int64_t)g.kb_total, ((int64_t)*g.k_active + kTcBK - 1) / kTcBK)
+                             : g.kb_total;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_ah) : "memory");
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(g, nt_live);
+      SegIter it(g, nt_live, kbt);
       Seg w;
       while (it.next(w)) {
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int li = 0;
-      SegIter it(g, nt_live);
+      SegIter it(g, nt_live, kbt);
       Seg w;
       while (it.next(w)) {
         const int acc = li & 1;
@@ -216,6 +218,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * kTcBN);
         const int kb0 = w.kb0, kb1 = w.kb1;
+        if (kb0 == kb1) {   // empty split-K unit (dynamic K): the epilogue writes zeros
+          bar_arrive(&tfull[acc]);
+          ++li;
+          continue;
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           bar_wait(&full[stage], phase);
           tc_fence_after();
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp & 3;
     const int et = threadIdx.x - 128;          // 0..127 over the four epilogue warps
     int li = 0;
-    SegIter it(g, nt_live);
+    SegIter it(g, nt_live, kbt);
     Seg w;
     while (it.next(w)) {
       const int acc = li & 1;
@@ -266,8 +273,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // CTAs holding the later K blocks of this tile (stream-K kind 2)
         int c_first = 0, c_last = -1;
         if (w.kind == 2) {
-          const int64_t total = (int64_t)g.m_tiles * nt_live * g.kb_total;
-          const int64_t tile_end = ((int64_t)w.mt * nt_live + w.nt + 1) * g.kb_total;
+          const int64_t total = (int64_t)g.m_tiles * nt_live * kbt;
+          const int64_t tile_end = ((int64_t)w.mt * nt_live + w.nt + 1) * kbt;
           c_first = blockIdx.x + 1;
           c_last = blockIdx.x;
           while (c_last + 1 < (int)gridDim.x && sk_start(total, c_last + 1, gridDim.x) < tile_end) ++c_last;
@@ -278,10 +285,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           asm volatile("bar.sync 1, 128;" ::: "memory");
         }
         float* cbase = g.C + (int64_t)w.s * g.c_split;
+        const bool empty_unit = w.kb0 == w.kb1;
 #pragma unroll 1
         for (int c = 0; c < kTcBN / 32; ++c) {
           uint32_t v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kTcBN + c * 32), v);
+          if (!empty_unit) {
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kTcBN + c * 32), v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0u;
+          }
           float f[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);

@@ -37,6 +37,8 @@ struct TcGemmArgs {
   int m_tiles, n_tiles;
   int kb_total;         // K blocks of kTcBK
   const int* n_active;  // nullable: rows of B actually needed (<= N), read on device
+  const int* k_active;  // nullable: K extent actually used (<= K), read on device; the
+                        // split-K units divide the live K blocks, empty units write zeros
   // stream-K mode (streamk = 1): one output C (S = 1), the (tile, K-block)
   // steps split evenly over the persistent CTAs; a tile that straddles CTAs
   // is finished by the CTA holding its first K block, which adds the other
