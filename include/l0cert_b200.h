@@ -274,6 +274,14 @@ int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K
                           const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
                           int64_t ldc, int32_t splits, int32_t* h_splits, void* d_ws,
                           uint64_t ws_bytes, void* stream);
+/* The same contraction in 3xFP16 (kind::f16, twice the TF32 tensor rate): A
+ * and B scaled by powers of two below 2^14, split into fp16 hi + lo, three
+ * products accumulated in fp32, C unscaled exactly (the batched engine's
+ * contraction; tc_gemm.cuh).  Same arguments and workspace as above. */
+int32_t l0_tc_gemm_3xf16(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                         const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
+                         int64_t ldc, int32_t splits, int32_t* h_splits, void* d_ws,
+                         uint64_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -44,10 +44,14 @@ struct BatchArgs {
   uint8_t* mask;    // [B][pv]
   int* fone;        // [B][fone_stride]
   int64_t fone_stride;
-  float* bh;        // [B][pp]  beta+ split (GEMM_F B operand)
-  float* bl;
-  float* rh;        // [2B][nn] R | Z split (GEMM_T B operand)
-  float* rl;
+  __half* bh;       // [B][pp]  beta+ (or step) 3xFP16 split (GEMM_F B operand), scaled per row
+  __half* bl;
+  __half* rh;       // [2B][nn] R | Z 3xFP16 split (GEMM_T B operand), scaled per row
+  __half* rl;
+  float* rinv;      // [2B] 1 / scale of each GEMM_T B row (kb_rhs)
+  float* binv;      // [B]  1 / scale of each GEMM_F B row (kb_window / kb_warm_scale)
+  double* gbound;   // [B][rblocks] bound on |grad F| over the block's rows for any momentum (kb_obj)
+  double xsc;       // power-of-two scale of X in its fp16 splits (|X xsc| < 2^14)
   float* cf;        // [sf][B][nn]
   int sf;
   float* ct;        // [st][2B][pp]
@@ -87,12 +91,12 @@ struct BatchArgs {
   int* col_of;        // [pp] column cached in slot s (-1: free)
   int* uctl;          // [0] slots in use, [1..2] slots to gather [s0, s1), [3] GEMM_F K (slots
                       // rounded up to 32), [4] rebuilds, [5] columns gathered (statistics)
-  const float* xth;   // X^T hi/lo (p x nn): the gather source (coalesced rows)
-  const float* xtl;
-  float* xuh;         // [n][pp] cached X columns by slot (GEMM_F A operand)
-  float* xul;
-  float* bsh;         // [B][pp] forward operand by slot (GEMM_F B operand)
-  float* bsl;
+  const __half* xth;  // X^T hi/lo (p x nn): the gather source (coalesced rows)
+  const __half* xtl;
+  __half* xuh;        // [n][pp] cached X columns by slot (GEMM_F A operand)
+  __half* xul;
+  __half* bsh;        // [B][pp] forward operand by slot (GEMM_F B operand)
+  __half* bsl;
   int* fx_n;          // [B] fixed-one columns of node b outside the cache with a nonzero step
   int* fx_j;          // [B][kFoneDirect] their ids
   double* fx_v;       // [B][kFoneDirect] and steps (kb_gather -> kb_obj)
@@ -116,17 +120,28 @@ __device__ __forceinline__ int64_t gvs(const BatchArgs& g) { return 3 * g.pv + 8
 // and its TF32 split into the forward contraction's rows
 __global__ void kb_warm(BatchArgs g, const double* warm) {
   const int64_t b = blockIdx.y;
+  const double sc = 1.0 / (double)g.binv[b];   // power of two (kb_warm_scale)
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.pp; j += (int64_t)gridDim.x * blockDim.x) {
     const double w = j < g.p ? warm[b * g.p + j] : 0.0;
     if (j < g.pv) {
       g.beta[(b * 3 + 0) * g.pv + j] = w;
       g.beta[(b * 3 + 2) * g.pv + j] = w;
     }
-    float h, l;
-    tf32_split(w, h, l);
+    __half h, l;
+    f16_split(w * sc, h, l);
     g.bh[b * g.pp + j] = h;
     g.bl[b * g.pp + j] = l;
   }
+}
+
+// per-node fp16 scale of the warm starts (rows b of the MODE_INIT forward operand)
+__global__ void kb_warm_scale(BatchArgs g, const double* warm) {
+  __shared__ double red[32];
+  const int64_t b = blockIdx.x;
+  double m = 0.0;
+  for (int64_t j = threadIdx.x; j < g.p; j += blockDim.x) m = fmax(m, fabs(warm[b * g.p + j]));
+  m = block_max(m, red);
+  if (threadIdx.x == 0) g.binv[b] = ldexpf(1.f, -f16_exp(m));
 }
 
 // per-node classes from a compact list (node b: entries [off[b], off[b+1]),
@@ -298,10 +313,20 @@ __global__ void __launch_bounds__(kRowThreads, 4) kb_rhs(BatchArgs g) {
   const double* uprev = g.u + (ring(t - 2) * B + b) * nn;
   // compacted contraction rows: R at slot, Z at (active count) + slot
   const int64_t pos = g.slot[b], nact = g.flags[5];
-  float* rh = g.rh + pos * nn;
-  float* rl = g.rl + pos * nn;
-  float* zh = g.rh + (nact + pos) * nn;
-  float* zl = g.rl + (nact + pos) * nn;
+  __half* rh = g.rh + pos * nn;
+  __half* rl = g.rl + pos * nn;
+  __half* zh = g.rh + (nact + pos) * nn;
+  __half* zl = g.rl + (nact + pos) * nn;
+  // fp16 scale of the node's rows: kb_obj bounded |grad F(u_t + c (u_t - u_{t-1}))|
+  // for every c in [0, 1] (and c = 0 is zeta), so |R sc|, |Z sc| < 2^14
+  double gb = 0.0;
+  for (int r = 0; r < g.rblocks; ++r) gb = fmax(gb, g.gbound[b * g.rblocks + r]);
+  const int sx = f16_exp(gb);
+  const double sc = ldexp(1.0, sx);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g.rinv[pos] = ldexpf(1.f, -sx);
+    g.rinv[nact + pos] = ldexpf(1.f, -sx);
+  }
   double facc[3] = {0.0, 0.0, 0.0};
   int bad = 0;
   const int r0 = blockIdx.x * kRowsPerBlock;
@@ -327,26 +352,26 @@ __global__ void __launch_bounds__(kRowThreads, 4) kb_rhs(BatchArgs g) {
       uc[0] = ucur[i]; up[0] = uprev[i]; yi[0] = g.y[i];
       uc[1] = 0.0; up[1] = 0.0; yi[1] = 0.0;
     }
-    float gh[2], gl[2], zh2[2], zl2[2];
+    __half gh[2], gl[2], zh2[2], zl2[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !two) break;
       double gr = 0.0, zv = 0.0;
       row(uc[h], up[h], yi[h], gr, zv);
-      tf32_split(gr, gh[h], gl[h]);
+      f16_split(gr * sc, gh[h], gl[h]);
       if (wz) {
-        tf32_split(zv, zh2[h], zl2[h]);
+        f16_split(zv * sc, zh2[h], zl2[h]);
         conj_accumulate(g.loss, zv, yi[h], facc);
       }
     }
     if (two) {
       if (wg) {
-        *reinterpret_cast<float2*>(rh + i) = make_float2(gh[0], gh[1]);
-        *reinterpret_cast<float2*>(rl + i) = make_float2(gl[0], gl[1]);
+        *reinterpret_cast<__half2*>(rh + i) = __halves2half2(gh[0], gh[1]);
+        *reinterpret_cast<__half2*>(rl + i) = __halves2half2(gl[0], gl[1]);
       }
       if (wz) {
-        *reinterpret_cast<float2*>(zh + i) = make_float2(zh2[0], zh2[1]);
-        *reinterpret_cast<float2*>(zl + i) = make_float2(zl2[0], zl2[1]);
+        *reinterpret_cast<__half2*>(zh + i) = __halves2half2(zh2[0], zh2[1]);
+        *reinterpret_cast<__half2*>(zl + i) = __halves2half2(zl2[0], zl2[1]);
       }
     } else {
       if (wg) { rh[i] = gh[0]; rl[i] = gl[0]; }
@@ -477,15 +502,24 @@ __global__ void __launch_bounds__(kWinThreads, 1) kb_window(BatchArgs g) {
   const double* bprev = a.beta + ring(t - 1) * g.pv;
   const int64_t pos = g.slot[b];                      // compacted contraction row
   const bool direct_fone = a.prm->node_mode && a.prm->n_fone <= kFoneDirect;
+  // exact per-row fp16 scale from the largest |operand| of this node
+  double am = 0.0;
+  for (int64_t j = threadIdx.x; j < g.p; j += kWinThreads)
+    am = fmax(am, fabs(full ? out[j] : dsub(out[j], bprev[j])));
+  am = block_max(am, ps.red);
+  const int sx = f16_exp(am);
+  const double sc = ldexp(1.0, sx);
+  if (threadIdx.x == 0) g.binv[pos] = ldexpf(1.f, -sx);
   for (int64_t j = threadIdx.x; j < g.pp; j += kWinThreads) {
-    float h = 0.f, l = 0.f;
-    if (j < g.p) tf32_split(full ? out[j] : dsub(out[j], bprev[j]), h, l);
+    __half h = __ushort_as_half(0), l = __ushort_as_half(0);
+    if (j < g.p) f16_split((full ? out[j] : dsub(out[j], bprev[j])) * sc, h, l);
     g.bh[pos * g.pp + j] = h;
     g.bl[pos * g.pp + j] = l;
     // a node's few fixed-one columns stay out of the shared column cache (they
     // would widen every node's contraction for one node's sake); kb_obj adds
     // their step in fp64 instead
-    if (g.sparse_fwd && (h != 0.f || l != 0.f) && !(direct_fone && a.mask[j] == FIXED_ONE)) g.umask[j] = 1;
+    if (g.sparse_fwd && (f16_nonzero(h) || f16_nonzero(l)) && !(direct_fone && a.mask[j] == FIXED_ONE))
+      g.umask[j] = 1;
   }
 }
 
@@ -560,7 +594,7 @@ __global__ void __launch_bounds__(1024) kb_union(BatchArgs g) {
     g.uctl[0] = base;
     g.uctl[1] = s0;
     g.uctl[2] = base;
-    g.uctl[3] = min((base + 31) / 32 * 32, (int)g.pp);
+    g.uctl[3] = min((base + 63) / 64 * 64, (int)g.pp);   // whole fp16 K blocks
     if (rebuild) g.uctl[4] += 1;
     g.uctl[5] += base - s0;
   }
@@ -572,7 +606,7 @@ __global__ void __launch_bounds__(1024) kb_union(BatchArgs g) {
 // slots and in the padding up to the K of GEMM_F).  Persistent grid.
 constexpr int kGatherRows = 64;
 __global__ void __launch_bounds__(256) kb_gather(BatchArgs g) {
-  __shared__ float th[32][kGatherRows + 1], tl[32][kGatherRows + 1];
+  __shared__ __half th[32][kGatherRows + 2], tl[32][kGatherRows + 2];
   const int s0 = g.uctl[1], s1 = g.uctl[2], kpad = g.uctl[3];
   const int64_t n = g.n, pp = g.pp, nn = g.nn;
   const int rtiles = (int)((n + kGatherRows - 1) / kGatherRows);
@@ -586,10 +620,10 @@ __global__ void __launch_bounds__(256) kb_gather(BatchArgs g) {
       const int j = sl < s1 ? g.col_of[sl] : -1;
       for (int c = tx; c < kGatherRows; c += 32) {
         const int64_t r = r0 + c;
-        float h = 0.f, l = 0.f;
+        __half h = __ushort_as_half(0), l = __ushort_as_half(0);
         if (j >= 0 && r < n) {
-          h = __ldg(g.xth + (int64_t)j * nn + r);
-          l = __ldg(g.xtl + (int64_t)j * nn + r);
+          h = g.xth[(int64_t)j * nn + r];
+          l = g.xtl[(int64_t)j * nn + r];
         }
         th[i][c] = h;
         tl[i][c] = l;
@@ -641,7 +675,7 @@ __global__ void __launch_bounds__(256) kb_gather(BatchArgs g) {
     const int64_t r = e / kpad;
     const int sl = (int)(e - r * kpad);
     const int j = g.col_of[sl];
-    float h = 0.f, l = 0.f;
+    __half h = __ushort_as_half(0), l = __ushort_as_half(0);
     if (j >= 0) {
       h = g.bh[r * pp + j];
       l = g.bl[r * pp + j];
@@ -663,7 +697,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
   const int64_t n = g.n, nn = g.nn, B = g.B;
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
   const int64_t r1 = min(n, r0 + kRowsPerBlock);
-  double lsum = 0.0;
+  double lsum = 0.0, gmax = 0.0;
   int bad = 0;
   const bool delta = mode == MODE_ITER && !resync_at(t);
   const double* uprev = g.u + (ring(t - 1) * B + b) * nn;
@@ -705,7 +739,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
       }
       const double2 y2 = *reinterpret_cast<const double2*>(g.y + i);
       yv[0] = y2.x; yv[1] = y2.y;
-      if (delta) {
+      if (mode == MODE_ITER) {   // the step base, and u_{t-1} of the gradient bound
         const double2 p2 = *reinterpret_cast<const double2*>(uprev + i);
         upv[0] = p2.x; upv[1] = p2.y;
       }
@@ -713,13 +747,13 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
       for (int s = 0; s < sf; ++s) u[0] += (double)cfb[s * cstride + i];
       yv[0] = g.y[i];
       yv[1] = 0.0;
-      if (delta) upv[0] = uprev[i];
+      if (mode == MODE_ITER) upv[0] = uprev[i];
     }
     for (int e = 0; e < nfx; ++e) {
-      const int64_t o = (int64_t)fx_j[e] * nn + i;   // even: 8-byte aligned pairs
-      const double v = fx_v[e];
-      const float2 xh = __ldg(reinterpret_cast<const float2*>(g.xth + o));
-      const float2 xl = __ldg(reinterpret_cast<const float2*>(g.xtl + o));
+      const int64_t o = (int64_t)fx_j[e] * nn + i;   // even: 4-byte aligned pairs
+      const double v = fx_v[e] / g.xsc;
+      const float2 xh = __half22float2(*reinterpret_cast<const __half2*>(g.xth + o));
+      const float2 xl = __half22float2(*reinterpret_cast<const __half2*>(g.xtl + o));
       u[0] = fma((double)xh.x + (double)xl.x, v, u[0]);
       if (two) u[1] = fma((double)xh.y + (double)xl.y, v, u[1]);
     }
@@ -729,6 +763,14 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
       if (delta) u[h] = dadd(upv[h], u[h]);
       if (!isfinite(u[h])) bad = 1;
       lsum += loss_term(g.loss, u[h], yv[h]);
+      // |grad F(u + c (u - u_prev))| for every c in [0, 1] (the next kb_rhs's fp16 scale)
+      const double du = mode == MODE_ITER ? fabs(u[h] - upv[h]) : 0.0;
+      const double ay = fabs(yv[h]);
+      double gbd;
+      if (g.loss == SQUARED_ERROR) gbd = 2.0 * (fabs(u[h] - yv[h]) + du);
+      else if (g.loss == LOGISTIC) gbd = ay;
+      else gbd = 2.0 * ay * (1.0 + ay * (fabs(u[h]) + du));
+      gmax = fmax(gmax, gbd * (1.0 + 1e-12));
     }
     if (two) {
       *reinterpret_cast<double2*>(uo + i) = make_double2(u[0], u[1]);
@@ -739,8 +781,10 @@ __global__ void __launch_bounds__(kRowThreads, 3) kb_obj(BatchArgs g, int mode) 
     }
   }
   const double csum = block_sum(lsum, red);
+  gmax = block_max(gmax, red);
   const int anybad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
+    g.gbound[b * g.rblocks + blockIdx.x] = gmax;
     double* lp = g.lpart + (b * g.rblocks + blockIdx.x) * 2;
     lp[0] = csum;
     lp[1] = anybad ? 1.0 : 0.0;

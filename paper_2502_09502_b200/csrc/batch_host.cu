@@ -23,7 +23,8 @@ struct Batch {
   int sms = 148;
   uint64_t ws_bytes = 0;
   void* ws = nullptr;
-  float *xh = nullptr, *xl = nullptr, *xth = nullptr, *xtl = nullptr;
+  __half *xh = nullptr, *xl = nullptr, *xth = nullptr, *xtl = nullptr;   // 3xFP16 splits of X (scaled)
+  unsigned* xmax = nullptr;      // max |X| (float bits) for the X scale
   TcGemmArgs gf{}, gt{}, gfs{};   // forward (dense: MODE_INIT), transpose, forward (support-compacted)
   CUtensorMap m_xh{}, m_xl{}, m_xth{}, m_xtl{}, m_bh{}, m_bl{}, m_rh{}, m_rl{};
   CUtensorMap m_xuh{}, m_xul{}, m_bsh{}, m_bsl{};
@@ -52,14 +53,18 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
     return r;
   };
   const int64_t n = g.n, p = g.p, B = g.B, pv = g.pv, pp = g.pp, nn = g.nn;
-  Bt.xh = (float*)take(4ull * n * pp);
-  Bt.xl = (float*)take(4ull * n * pp);
-  Bt.xth = (float*)take(4ull * p * nn);
-  Bt.xtl = (float*)take(4ull * p * nn);
-  g.bh = (float*)take(4ull * B * pp);
-  g.bl = (float*)take(4ull * B * pp);
-  g.rh = (float*)take(4ull * 2 * B * nn);
-  g.rl = (float*)take(4ull * 2 * B * nn);
+  Bt.xh = (__half*)take(2ull * n * pp);
+  Bt.xl = (__half*)take(2ull * n * pp);
+  Bt.xth = (__half*)take(2ull * p * nn);
+  Bt.xtl = (__half*)take(2ull * p * nn);
+  Bt.xmax = (unsigned*)take(4ull);
+  g.bh = (__half*)take(2ull * B * pp);
+  g.bl = (__half*)take(2ull * B * pp);
+  g.rh = (__half*)take(2ull * 2 * B * nn);
+  g.rl = (__half*)take(2ull * 2 * B * nn);
+  g.rinv = (float*)take(4ull * 2 * B);
+  g.binv = (float*)take(4ull * B);
+  g.gbound = (double*)take(8ull * B * g.rblocks);
   g.cf = (float*)take(4ull * Bt.sf_cap * B * nn);
   g.ct = (float*)take(4ull * Bt.sct_cap * 2 * B * pp);
   g.u = (double*)take(8ull * 3 * B * nn);
@@ -97,10 +102,10 @@ static uint64_t batch_carve(Batch& Bt, char* base) {
     g.slot_of = (int*)take(4ull * pp);
     g.col_of = (int*)take(4ull * pp);
     g.uctl = (int*)take(4ull * 8);
-    g.xuh = (float*)take(4ull * n * pp);
-    g.xul = (float*)take(4ull * n * pp);
-    g.bsh = (float*)take(4ull * B * pp);
-    g.bsl = (float*)take(4ull * B * pp);
+    g.xuh = (__half*)take(2ull * n * pp);
+    g.xul = (__half*)take(2ull * n * pp);
+    g.bsh = (__half*)take(2ull * B * pp);
+    g.bsl = (__half*)take(2ull * B * pp);
     g.fx_n = (int*)take(4ull * B);
     g.fx_j = (int*)take(4ull * B * kFoneDirect);
     g.fx_v = (double*)take(8ull * B * kFoneDirect);
@@ -276,37 +281,67 @@ extern "C" {
 static constexpr int kSkMaxCtas = 256;
 uint64_t l0_tc_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const int64_t ldk = (K + 31) / 32 * 32;
-  return (uint64_t)(2 * (M + N) * ldk) * 4 + 1024 + 4ull * kSkMaxCtas * (kTcBN * kTcBM + 1) + 256;
+  return (uint64_t)(2 * (M + N) * ldk) * 4 + 1024 + 4ull * kSkMaxCtas * (kTcBN * kTcBM + 1) + 256 + 64;
 }
 
-int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
-                          const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
-                          int64_t ldc, int32_t splits, int32_t* h_splits_out, void* d_ws,
-                          uint64_t ws_bytes, void* stream) {
+static int32_t tc_gemm_abi(int f16, const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                           const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C, int64_t ldc,
+                           int32_t splits, int32_t* h_splits_out, void* d_ws, uint64_t ws_bytes, void* stream) {
   if (!d_A || !d_B || !d_C || !d_ws) return set_error(L0_INVALID, "null argument");
   if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < M)
     return set_error(L0_INVALID, "bad GEMM shape");
   if (ws_bytes < l0_tc_gemm_workspace_bytes(M, N, K)) return set_error(L0_INVALID, "workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
+  // operand regions sized for fp32 rows of ldk (the fp16 rows of ldk16 fit in them)
   const int64_t ldk = (K + 31) / 32 * 32;
+  const int64_t ldk16 = (K + 63) / 64 * 64;
   char* base = (char*)(((uintptr_t)d_ws + 255) & ~uintptr_t(255));
   float* ah = (float*)base;
   float* al = ah + M * ldk;
   float* bh = al + M * ldk;
   float* bl = bh + N * ldk;
-  auto split = [&](const void* src, int dt, int64_t rows, int64_t ld, float* h, float* l) {
+  double sa = 1.0, sb = 1.0;
+  if (f16) {
+    // power-of-two scales from max |A|, max |B| (3xFP16, tc_gemm.cuh)
+    unsigned* mx = (unsigned*)(bl + N * ldk + (int64_t)kSkMaxCtas * (kTcBN * kTcBM + 1));   // after the stream-K flags
+    if (cudaMemsetAsync(mx, 0, 8, s) != cudaSuccess) return set_error(L0_CUDA, "memset failed");
+    auto amax = [&](const void* src, int dt, int64_t rows, int64_t ld, unsigned* o) {
+      if (dt == L0_F64) k_absmax<double><<<148, 256, 0, s>>>((const double*)src, rows, K, ld, o);
+      else k_absmax<float><<<148, 256, 0, s>>>((const float*)src, rows, K, ld, o);
+    };
+    amax(d_A, a_dtype, M, lda, mx);
+    amax(d_B, b_dtype, N, ldb, mx + 1);
+    unsigned hb[2] = {0, 0};
+    if (cudaMemcpyAsync(hb, mx, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+      return set_error(L0_CUDA, "operand maxima failed");
+    float fa, fb;
+    std::memcpy(&fa, &hb[0], 4);
+    std::memcpy(&fb, &hb[1], 4);
+    sa = std::ldexp(1.0, f16_exp(fa));
+    sb = std::ldexp(1.0, f16_exp(fb));
+  }
+  auto split = [&](const void* src, int dt, int64_t rows, int64_t ld, float* h, float* l, double sc) {
+    if (f16) {
+      const int blocks = (int)std::min<int64_t>((rows * ldk16 + 255) / 256, 148 * 16);
+      if (dt == L0_F64)
+        k_split_rows_h<double><<<blocks, 256, 0, s>>>((const double*)src, rows, K, ld, sc, (__half*)h, (__half*)l, ldk16);
+      else
+        k_split_rows_h<float><<<blocks, 256, 0, s>>>((const float*)src, rows, K, ld, sc, (__half*)h, (__half*)l, ldk16);
+      return;
+    }
     const int blocks = (int)std::min<int64_t>((rows * ldk + 255) / 256, 148 * 16);
     if (dt == L0_F64)
       k_split_rows<double><<<blocks, 256, 0, s>>>((const double*)src, rows, K, ld, h, l, ldk);
     else
       k_split_rows<float><<<blocks, 256, 0, s>>>((const float*)src, rows, K, ld, h, l, ldk);
   };
-  split(d_A, a_dtype, M, lda, ah, al);
-  split(d_B, b_dtype, N, ldb, bh, bl);
+  split(d_A, a_dtype, M, lda, ah, al, sa);
+  split(d_B, b_dtype, N, ldb, bh, bl, sb);
   if (cudaGetLastError() != cudaSuccess) return set_error(L0_CUDA, "split kernel launch failed");
+  const int64_t ld_op = f16 ? ldk16 : ldk;
   CUtensorMap m_ah, m_al, m_bh, m_bl;
-  if (tc_make_map(&m_ah, ah, M, K, ldk, kTcBM) || tc_make_map(&m_al, al, M, K, ldk, kTcBM) ||
-      tc_make_map(&m_bh, bh, N, K, ldk, kTcBN) || tc_make_map(&m_bl, bl, N, K, ldk, kTcBN))
+  if (tc_make_map(&m_ah, ah, M, K, ld_op, kTcBM, f16) || tc_make_map(&m_al, al, M, K, ld_op, kTcBM, f16) ||
+      tc_make_map(&m_bh, bh, N, K, ld_op, kTcBN, f16) || tc_make_map(&m_bl, bl, N, K, ld_op, kTcBN, f16))
     return set_error(L0_CUDA, "cuTensorMapEncodeTiled failed");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -319,6 +354,8 @@ int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K
   g.c_split = N * ldc;
   g.C = d_C;
   g.n_active = nullptr;
+  g.f16 = f16;
+  g.a_inv_scale = (float)(1.0 / (sa * sb));
   tc_gemm_plan(g, sms, splits > 0 ? splits : 32);
   if (splits > 0) {
     g.S = splits;
@@ -338,6 +375,22 @@ int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K
   cudaError_t e = tc_gemm_launch(m_ah, m_al, m_bh, m_bl, g, grid, s);
   if (e != cudaSuccess) return set_error(L0_CUDA, std::string("tc_gemm: ") + cudaGetErrorString(e));
   return L0_OK;
+}
+
+int32_t l0_tc_gemm_3xtf32(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                          const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
+                          int64_t ldc, int32_t splits, int32_t* h_splits_out, void* d_ws,
+                          uint64_t ws_bytes, void* stream) {
+  return tc_gemm_abi(0, d_A, a_dtype, M, K, lda, d_B, b_dtype, N, ldb, d_C, ldc, splits, h_splits_out, d_ws,
+                     ws_bytes, stream);
+}
+
+int32_t l0_tc_gemm_3xf16(const void* d_A, int32_t a_dtype, int64_t M, int64_t K, int64_t lda,
+                         const void* d_B, int32_t b_dtype, int64_t N, int64_t ldb, float* d_C,
+                         int64_t ldc, int32_t splits, int32_t* h_splits_out, void* d_ws,
+                         uint64_t ws_bytes, void* stream) {
+  return tc_gemm_abi(1, d_A, a_dtype, M, K, lda, d_B, b_dtype, N, ldb, d_C, ldc, splits, h_splits_out, d_ws,
+                     ws_bytes, stream);
 }
 
 int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out) {
@@ -373,6 +426,7 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   // (the zeta rows only on bound checks), K = n, split count planned for N = B
   TcGemmArgs& gf = Bt->gf;
   gf.M = a.n; gf.N = n_nodes; gf.K = a.p;
+  gf.f16 = 1;
   tc_gemm_plan(gf, Bt->sms, 32);
   if (const char* e = getenv("L0_TC_SF")) {   // tuning override
     gf.S = std::max(1, atoi(e));
@@ -380,6 +434,7 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
   }
   TcGemmArgs& gt = Bt->gt;
   gt.M = a.p; gt.N = n_nodes; gt.K = a.n;
+  gt.f16 = 1;
   tc_gemm_plan(gt, Bt->sms, 32);
   if (const char* e = getenv("L0_TC_ST")) gt.S = std::max(1, atoi(e));
   gt.N = 2 * n_nodes;
@@ -449,49 +504,66 @@ int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
   const EngineArgs& a = Bt->prob->a;
   cudaStream_t s = Bt->stream;
   const int64_t n = g.n, p = g.p;
-  // X -> hi/lo TF32 operands, row-major (forward) and transposed (transpose pass)
+  // X -> hi/lo 3xFP16 operands scaled by 2^sx (|X 2^sx| < 2^14), row-major
+  // (forward) and transposed (transpose pass)
   const int blocks = (int)std::min<int64_t>((n * g.pp + 255) / 256, (int64_t)Bt->sms * 16);
   const dim3 tgrid((unsigned)((p + 31) / 32), (unsigned)((g.nn + 31) / 32));
+  L0_B_TRY(cudaMemsetAsync(Bt->xmax, 0, 4, s));
+  if (a.dtype == F64) k_absmax<double><<<Bt->sms * 4, 256, 0, s>>>((const double*)a.X, n, p, a.ld, Bt->xmax);
+  else k_absmax<float><<<Bt->sms * 4, 256, 0, s>>>((const float*)a.X, n, p, a.ld, Bt->xmax);
+  L0_B_TRY(cudaGetLastError());
+  unsigned xm_bits = 0;
+  L0_B_TRY(cudaMemcpyAsync(&xm_bits, Bt->xmax, 4, cudaMemcpyDeviceToHost, s));
+  L0_B_TRY(cudaStreamSynchronize(s));
+  float xm = 0.f;
+  std::memcpy(&xm, &xm_bits, 4);
+  if (!std::isfinite(xm)) return set_error(L0_INVALID, "X contains non-finite entries");
+  const int sx = f16_exp((double)xm);
+  g.xsc = std::ldexp(1.0, sx);
   if (a.dtype == F64) {
-    k_split_rows<double><<<blocks, 256, 0, s>>>((const double*)a.X, n, p, a.ld, Bt->xh, Bt->xl, g.pp);
-    k_split_transpose<double><<<tgrid, dim3(32, 8), 0, s>>>((const double*)a.X, n, p, a.ld, Bt->xth, Bt->xtl, g.nn);
+    k_split_rows_h<double><<<blocks, 256, 0, s>>>((const double*)a.X, n, p, a.ld, g.xsc, Bt->xh, Bt->xl, g.pp);
+    k_split_transpose_h<double><<<tgrid, dim3(32, 8), 0, s>>>((const double*)a.X, n, p, a.ld, g.xsc, Bt->xth, Bt->xtl, g.nn);
   } else {
-    k_split_rows<float><<<blocks, 256, 0, s>>>((const float*)a.X, n, p, a.ld, Bt->xh, Bt->xl, g.pp);
-    k_split_transpose<float><<<tgrid, dim3(32, 8), 0, s>>>((const float*)a.X, n, p, a.ld, Bt->xth, Bt->xtl, g.nn);
+    k_split_rows_h<float><<<blocks, 256, 0, s>>>((const float*)a.X, n, p, a.ld, g.xsc, Bt->xh, Bt->xl, g.pp);
+    k_split_transpose_h<float><<<tgrid, dim3(32, 8), 0, s>>>((const float*)a.X, n, p, a.ld, g.xsc, Bt->xth, Bt->xtl, g.nn);
   }
   L0_B_TRY(cudaGetLastError());
-  L0_B_TRY(cudaMemsetAsync(g.rh, 0, 4ull * 2 * g.B * g.nn, s));
-  L0_B_TRY(cudaMemsetAsync(g.rl, 0, 4ull * 2 * g.B * g.nn, s));
+  L0_B_TRY(cudaMemsetAsync(g.rh, 0, 2ull * 2 * g.B * g.nn, s));
+  L0_B_TRY(cudaMemsetAsync(g.rl, 0, 2ull * 2 * g.B * g.nn, s));
+  L0_B_TRY(cudaMemsetAsync(g.rinv, 0, 4ull * 2 * g.B, s));
+  L0_B_TRY(cudaMemsetAsync(g.binv, 0, 4ull * g.B, s));
   L0_B_TRY(cudaMemsetAsync(g.cnt, 0, 4ull * g.B, s));
   L0_B_TRY(cudaMemsetAsync(g.flags, 0, 4ull * 8, s));
   int rc = 0;
-  rc |= tc_make_map(&Bt->m_xh, Bt->xh, n, p, g.pp, kTcBM);
-  rc |= tc_make_map(&Bt->m_xl, Bt->xl, n, p, g.pp, kTcBM);
-  rc |= tc_make_map(&Bt->m_xth, Bt->xth, p, n, g.nn, kTcBM);
-  rc |= tc_make_map(&Bt->m_xtl, Bt->xtl, p, n, g.nn, kTcBM);
-  rc |= tc_make_map(&Bt->m_bh, g.bh, g.B, p, g.pp, kTcBN);
-  rc |= tc_make_map(&Bt->m_bl, g.bl, g.B, p, g.pp, kTcBN);
-  rc |= tc_make_map(&Bt->m_rh, g.rh, 2 * g.B, n, g.nn, kTcBN);
-  rc |= tc_make_map(&Bt->m_rl, g.rl, 2 * g.B, n, g.nn, kTcBN);
+  rc |= tc_make_map(&Bt->m_xh, Bt->xh, n, p, g.pp, kTcBM, 1);
+  rc |= tc_make_map(&Bt->m_xl, Bt->xl, n, p, g.pp, kTcBM, 1);
+  rc |= tc_make_map(&Bt->m_xth, Bt->xth, p, n, g.nn, kTcBM, 1);
+  rc |= tc_make_map(&Bt->m_xtl, Bt->xtl, p, n, g.nn, kTcBM, 1);
+  rc |= tc_make_map(&Bt->m_bh, g.bh, g.B, p, g.pp, kTcBN, 1);
+  rc |= tc_make_map(&Bt->m_bl, g.bl, g.B, p, g.pp, kTcBN, 1);
+  rc |= tc_make_map(&Bt->m_rh, g.rh, 2 * g.B, n, g.nn, kTcBN, 1);
+  rc |= tc_make_map(&Bt->m_rl, g.rl, 2 * g.B, n, g.nn, kTcBN, 1);
   if (Bt->sparse) {
-    rc |= tc_make_map(&Bt->m_xuh, g.xuh, n, p, g.pp, kTcBM);
-    rc |= tc_make_map(&Bt->m_xul, g.xul, n, p, g.pp, kTcBM);
-    rc |= tc_make_map(&Bt->m_bsh, g.bsh, g.B, p, g.pp, kTcBN);
-    rc |= tc_make_map(&Bt->m_bsl, g.bsl, g.B, p, g.pp, kTcBN);
+    rc |= tc_make_map(&Bt->m_xuh, g.xuh, n, p, g.pp, kTcBM, 1);
+    rc |= tc_make_map(&Bt->m_xul, g.xul, n, p, g.pp, kTcBM, 1);
+    rc |= tc_make_map(&Bt->m_bsh, g.bsh, g.B, p, g.pp, kTcBN, 1);
+    rc |= tc_make_map(&Bt->m_bsl, g.bsl, g.B, p, g.pp, kTcBN, 1);
     L0_B_TRY(cudaMemsetAsync(g.umask, 0, 4ull * g.pp, s));
     L0_B_TRY(cudaMemsetAsync(g.slot_of, 0xff, 4ull * g.pp, s));
     L0_B_TRY(cudaMemsetAsync(g.col_of, 0xff, 4ull * g.pp, s));
     L0_B_TRY(cudaMemsetAsync(g.uctl, 0, 4ull * 8, s));
-    L0_B_TRY(cudaMemsetAsync(g.xuh, 0, 4ull * n * g.pp, s));
-    L0_B_TRY(cudaMemsetAsync(g.xul, 0, 4ull * n * g.pp, s));
-    L0_B_TRY(cudaMemsetAsync(g.bsh, 0, 4ull * g.B * g.pp, s));
-    L0_B_TRY(cudaMemsetAsync(g.bsl, 0, 4ull * g.B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.xuh, 0, 2ull * n * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.xul, 0, 2ull * n * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bsh, 0, 2ull * g.B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bsl, 0, 2ull * g.B * g.pp, s));
     TcGemmArgs& gfs = Bt->gfs;
     gfs.ldc = g.nn;
     gfs.c_split = g.B * g.nn;
     gfs.C = g.cf;
     gfs.n_active = g.flags + 3;
     gfs.k_active = g.uctl + 3;
+    gfs.a_inv_scale = (float)(1.0 / g.xsc);
+    gfs.b_inv_scale = g.binv;
   }
   if (rc) return set_error(L0_CUDA, "cuTensorMapEncodeTiled failed");
   TcGemmArgs& gf = Bt->gf;
@@ -499,11 +571,15 @@ int32_t l0_batch_set_workspace(l0_batch* Bt, void* d_ws, uint64_t bytes) {
   gf.c_split = g.B * g.nn;
   gf.C = g.cf;
   gf.n_active = g.flags + 3;
+  gf.a_inv_scale = (float)(1.0 / g.xsc);
+  gf.b_inv_scale = g.binv;
   TcGemmArgs& gt = Bt->gt;
   gt.ldc = g.pp;
   gt.c_split = 2 * g.B * g.pp;
   gt.C = g.ct;
   gt.n_active = g.flags + 2;
+  gt.a_inv_scale = (float)(1.0 / g.xsc);
+  gt.b_inv_scale = g.rinv;
   if (Bt->streamk) {
     for (TcGemmArgs* t : {&gf, &gt}) {
       t->sk_part = Bt->sk_part;
@@ -660,14 +736,16 @@ int32_t l0_batch_solve(l0_batch* Bt, int64_t k, double M, double lambda2, const 
   ++launches;
   if (d_warm) {
     // warm starts (fista.py:130-137): beta_0 -> ring slots, split for u_0 = X beta_0
+    kb_warm_scale<<<(unsigned)B, 256, 0, s>>>(g, d_warm);
     kb_warm<<<dim3((unsigned)std::min<int64_t>((g.pp + 255) / 256, 64), (unsigned)B), 256, 0, s>>>(g, d_warm);
     L0_B_TRY(cudaGetLastError());
-    ++launches;
+    launches += 2;
   } else {
     // cold start: beta_0 = 0 (fista.py:130-137); u_0 = X beta_0 through the forward contraction
     L0_B_TRY(cudaMemsetAsync(g.beta, 0, 8ull * 3 * B * pv, s));
-    L0_B_TRY(cudaMemsetAsync(g.bh, 0, 4ull * B * g.pp, s));
-    L0_B_TRY(cudaMemsetAsync(g.bl, 0, 4ull * B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bh, 0, 2ull * B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.bl, 0, 2ull * B * g.pp, s));
+    L0_B_TRY(cudaMemsetAsync(g.binv, 0, 4ull * B, s));
   }
   Bt->gf.n_active = nullptr;
   L0_B_TRY(tc_gemm_launch(Bt->m_xh, Bt->m_xl, Bt->m_bh, Bt->m_bl, Bt->gf, std::min(Bt->gf.units, Bt->sms), s));

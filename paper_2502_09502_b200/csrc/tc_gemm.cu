@@ -133,9 +133,20 @@ struct SegIter {
   }
 };
 
-// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = kTcBN
+// instruction descriptors: D f32, both K-major, M = 128, N = kTcBN; A/B tf32
+// (format 2, kind::tf32, K = 8 per MMA) or f16 (format 0, kind::f16, K = 16);
+// either way one MMA consumes 32 bytes of each operand's 128-byte row
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcBN >> 3) << 17) |
                             ((uint32_t)(kTcBM >> 4) << 24);
+constexpr uint32_t kIdescF16 = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(kTcBN >> 3) << 17) |
+                               ((uint32_t)(kTcBM >> 4) << 24);
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
@@ -154,7 +165,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_act = g.n_active ? (int64_t)*g.n_active : g.N;
   const int nt_live = (int)min((int64_t)g.n_tiles, (n_act + kTcBN - 1) / kTcBN);
-  const int kbt = g.k_active ? (int)min((int64_t)g.kb_total, ((int64_t)*g.k_active + kTcBK - 1) / kTcBK)
+  const int bke = g.f16 ? 64 : kTcBK;   // K elements per 128-byte block
+  const int kbt = g.k_active ? (int)min((int64_t)g.kb_total, ((int64_t)*g.k_active + bke - 1) / bke)
                              : g.kb_total;
 
   if (warp == 0 && lane == 0) {
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           bar_wait(&empty[stage], phase ^ 1u);
           unsigned char* st = smem + stage * kStageBytes;
           bar_expect(&full[stage], kStageBytes);
-          const int x = kb * kTcBK;
+          const int x = kb * bke;
           tma_load_2d(st, &map_ah, x, w.mt * kTcBM, &full[stage]);
           tma_load_2d(st + kTileA, &map_al, x, w.mt * kTcBM, &full[stage]);
           tma_load_2d(st + 2 * kTileA, &map_bh, x, w.nt * kTcBN, &full[stage]);
@@ -230,12 +242,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint64_t ah = kmajor_sw128_desc(st), al = kmajor_sw128_desc(st + kTileA);
           const uint64_t bh = kmajor_sw128_desc(st + 2 * kTileA);
           const uint64_t bl = kmajor_sw128_desc(st + 2 * kTileA + kTileB);
+          if (g.f16) {
 #pragma unroll
-          for (int k = 0; k < kTcBK / 8; ++k) {
-            const uint64_t o = (uint64_t)(2 * k);   // +32 bytes per K=8 step (>> 4)
-            mma_tf32(d, ah + o, bh + o, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            mma_tf32(d, ah + o, bl + o, kIdesc, 1u);
-            mma_tf32(d, al + o, bh + o, kIdesc, 1u);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t o = (uint64_t)(2 * k);   // +32 bytes per K=16 step (>> 4)
+              mma_f16(d, ah + o, bh + o, kIdescF16, (kb > kb0 || k > 0) ? 1u : 0u);
+              mma_f16(d, ah + o, bl + o, kIdescF16, 1u);
+              mma_f16(d, al + o, bh + o, kIdescF16, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t o = (uint64_t)(2 * k);   // +32 bytes per K=8 step (>> 4)
+              mma_tf32(d, ah + o, bh + o, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              mma_tf32(d, ah + o, bl + o, kIdesc, 1u);
+              mma_tf32(d, al + o, bh + o, kIdesc, 1u);
+            }
           }
           tc_commit(&empty[stage]);
           if (++stage == kTcStages) { stage = 0; phase ^= 1u; }
@@ -305,9 +327,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           const int64_t r0 = (int64_t)w.nt * kTcBN + c * 32;
           if (m < g.M) {
+            const float as = g.a_inv_scale;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if (r0 + j < n_act) cbase[(r0 + j) * g.ldc + m] = f[j];
+              if (r0 + j < n_act) {
+                const float sc = g.b_inv_scale ? as * __ldg(g.b_inv_scale + r0 + j) : as;
+                cbase[(r0 + j) * g.ldc + m] = f[j] * sc;
+              }
             }
           }
         }
@@ -345,15 +371,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-int tc_make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+int tc_make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows,
+                int f16) {
   auto fn = encode_fn();
   if (!fn) return 1;
-  if ((ld * 4) % 16 != 0 || ((uintptr_t)base) % 16 != 0) return 2;
+  const int es = f16 ? 2 : 4;
+  if ((ld * es) % 16 != 0 || ((uintptr_t)base) % 16 != 0) return 2;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)tc_bk(f16), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 3;
@@ -362,8 +391,8 @@ int tc_make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K, in
 void tc_gemm_plan(TcGemmArgs& g, int sms, int max_splits) {
   g.m_tiles = (int)((g.M + kTcBM - 1) / kTcBM);
   g.n_tiles = (int)((g.N + kTcBN - 1) / kTcBN);
-  g.kb_total = (int)((g.K + kTcBK - 1) / kTcBK);
-  const double t_kb = 0.85e-6;                          // one 32-deep K block, 3 MMA groups
+  g.kb_total = (int)((g.K + tc_bk(g.f16) - 1) / tc_bk(g.f16));
+  const double t_kb = 0.85e-6;   // one K block (32 tf32 / 64 f16), 3 MMA groups
   const double part_bytes = 8.0 * (double)g.N * (double)g.M;   // write + read of one split
   int best = 1;
   double best_t = 1e30;

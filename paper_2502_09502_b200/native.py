@@ -111,6 +111,8 @@ _PROTOS = {
     "l0_tc_gemm_workspace_bytes": (c_u64, [c_i64, c_i64, c_i64]),
     "l0_tc_gemm_3xtf32": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i32, c_i64, c_i64,
                                   c_vp, c_i64, c_i32, ctypes.POINTER(c_i32), c_vp, c_u64, c_vp]),
+    "l0_tc_gemm_3xf16": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i32, c_i64, c_i64,
+                                 c_vp, c_i64, c_i32, ctypes.POINTER(c_i32), c_vp, c_u64, c_vp]),
 }
 
 EXPORTED = tuple(_PROTOS)

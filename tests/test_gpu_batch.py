@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _gemm(A, B, splits=0):
+def _gemm(A, B, splits=0, kind="3xtf32"):
     from paper_2502_09502_b200 import native
     lib = native.lib()
     M, K = A.shape
@@ -22,7 +22,8 @@ def _gemm(A, B, splits=0):
     S_max = 64
     C = torch.zeros((S_max, N, M), dtype=torch.float32, device="cuda")
     dt = lambda t: native.F64 if t.dtype == torch.float64 else native.F32
-    native.check(lib.l0_tc_gemm_3xtf32(A.data_ptr(), dt(A), M, K, A.stride(0), B.data_ptr(), dt(B), N,
+    fn = lib.l0_tc_gemm_3xtf32 if kind == "3xtf32" else lib.l0_tc_gemm_3xf16
+    native.check(fn(A.data_ptr(), dt(A), M, K, A.stride(0), B.data_ptr(), dt(B), N,
                                        B.stride(0), C.data_ptr(), M, splits, ctypes.byref(s_out),
                                        ws.data_ptr(), ws.numel(), None))
     torch.cuda.synchronize()
@@ -57,6 +58,30 @@ def test_tc_gemm_3xtf32(M, N, K, splits, dtype):
         assert S == splits
     if splits < 0:
         assert S == 1
+
+
+@pytest.mark.parametrize("M,N,K,splits,dtype,amp", [
+    (128, 256, 64, 1, torch.float32, 1.0),
+    (300, 40, 100, 1, torch.float32, 1e-3),
+    (300, 40, 100, 3, torch.float64, 1e4),
+    (1000, 512, 777, 0, torch.float32, 1.0),
+    (4999, 300, 2048, 0, torch.float64, 37.0),
+    (2000, 1024, 5000, 0, torch.float32, 1.0),
+    (4999, 300, 2048, -1, torch.float32, 1.0),
+    (3000, 512, 1024, -1, torch.float32, 1e-6),
+])
+def test_tc_gemm_3xf16(M, N, K, splits, dtype, amp):
+    """The batched engine's contraction: 3xFP16 with power-of-two operand
+    scaling (tc_gemm.cuh) -- fp32-class accuracy at any operand magnitude."""
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N)
+    A = (torch.randn(M, K, generator=g, device="cuda", dtype=torch.float64) * amp).to(dtype)
+    B = torch.randn(N, K, generator=g, device="cuda", dtype=torch.float64).to(dtype)
+    B[:, ::7] *= 1e-3    # small entries: their lo parts are fp16 subnormals
+    C, S = _gemm(A, B, splits, kind="3xf16")
+    ref = B.double() @ A.double().T
+    scale = B.double().abs() @ A.double().abs().T
+    err = ((C - ref).abs() / scale).max().item()
+    assert err < 4e-6 * max(1.0, K / 5000), (err, S)
 
 
 # ---------------------------------------------------------------------------
