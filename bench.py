@@ -48,7 +48,6 @@ os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/l0_numba_cache")
 # package's own Lanczos reproduces it (tests/test_gpu_fullsize.py)
 L_C2 = 2.9908e5
 REL_GAP = 1e-6
-TF32_DENSE_PEAK = 1100.0   # TFLOP/s, B200 dense TF32 (B200_PROFILING.md)
 METRIC = "FISTA iters/sec (N=1: C2 perspective relaxation; N>1: C5 rows sharded over the GPUs)"
 C2_WORKLOAD = ("C2: least-squares root perspective relaxation, n=p=16000, Toeplitz rho=0.7, "
                "k=20, M=2, lambda2=0.1, SNR=5, fp64")
@@ -319,35 +318,16 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # batched nodes (C4): tensor-core roofline
 # ---------------------------------------------------------------------------
-def tf32_peak(seconds=1.5):
-    """cuBLAS TF32 dense throughput on this GPU (torch.matmul 8192^3, fp32 inputs,
-    TF32 math): burst (best) and sustained (back to back) TFLOP/s."""
-    import torch
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
+def tensor_peak():
+    """Dense fp16 / bf16 tensor peak of this pool's B200s (MEASURED_PEAKS.json:
+    cuBLAS bf16 8192^3, burst and sustained); kind::f16 runs at the bf16 rate."""
     try:
-        n = 8192
-        a = torch.randn(n, n, device="cuda")
-        b = torch.randn(n, n, device="cuda")
-        for _ in range(3):
-            a @ b
-        torch.cuda.synchronize()
-        best = 0.0
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for _ in range(10):
-            e0.record(); a @ b; e1.record(); torch.cuda.synchronize()
-            best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
-        t0 = time.perf_counter(); cnt = 0
-        e0.record()
-        while time.perf_counter() - t0 < seconds:
-            a @ b; cnt += 1
-            if cnt % 8 == 0:
-                torch.cuda.synchronize()
-        e1.record(); torch.cuda.synchronize()
-        sustained = 2 * n ** 3 * cnt / (e0.elapsed_time(e1) / 1e3) / 1e12
-        return best, sustained
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return (float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "measured (MEASURED_PEAKS.json bf16_tflops; kind::f16 has the bf16 rate)")
+    except Exception:
+        return 2250.0, 2250.0, "fallback (B200_PROFILING.md dense fp16 / bf16)"
 
 
 def c4_setup(args, nodes_total):
@@ -390,10 +370,8 @@ def run_batched(args):
     it = prof["profiled_iterations"]
     gt, gf, px = prof["gemm_t_ms"] / it, prof["gemm_f_ms"] / it, prof["prox_ms"] / it
     checks = sum(1 for t in range(1, K + 1) if t == 1 or t % 10 == 0) / K
-    useful_f = 2.0 * n * p * B
     useful_t = 2.0 * n * p * B * (1.0 + checks)
-    burst, sustained = tf32_peak()
-    tensor_f = 3 * useful_f / (gf / 1e3) / 1e12
+    burst, sustained, peak_src = tensor_peak()
     tensor_t = 3 * useful_t / (gt / 1e3) / 1e12
     cpu = None
     if not args.no_cpu:
@@ -417,19 +395,18 @@ def run_batched(args):
                         f"lambda2=0.5, cold start, {K} iterations each (lockstep)",
             "metric": "node FISTA iterations/s", "value": B * K / (ms / 1e3),
             "ms_per_batched_iteration": ms / K, "clocks": clk,
-            "contraction": "tcgen05 kind::tf32, 3xTF32 (hi/lo split), fp32 TMEM accumulation",
+            "contraction": "tcgen05 kind::f16, 3xFP16 (power-of-two scaled hi/lo split), fp32 TMEM "
+                           "accumulation; the forward contraction only over the X columns of the "
+                           "nodes' step supports (slot cache)",
             "roofline": {"bound": "tensor", "unit": "TFLOP/s",
-                         "kernel": "tc_gemm_kernel (forward X.Beta step)",
-                         "achieved": tensor_f, "peak": TF32_DENSE_PEAK,
-                         "frac": tensor_f / TF32_DENSE_PEAK,
-                         "peak_source": "B200_PROFILING.md dense TF32 (MEASURED_PEAKS.json has no "
-                                        "TF32 entry); measured cuBLAS TF32 8192^3 here: burst "
-                                        f"{burst:.0f}, sustained {sustained:.0f}",
-                         "cublas_tf32_burst": burst, "cublas_tf32_sustained": sustained,
-                         "transpose_achieved": tensor_t, "transpose_frac": tensor_t / TF32_DENSE_PEAK,
-                         "useful_tflops_forward": useful_f / (gf / 1e3) / 1e12,
-                         "flops_per_forward_launch": 3 * useful_f,
-                         "note": "tensor FLOPs count the 3 TF32 products of the hi/lo split"},
+                         "kernel": "tc_gemm_kernel (transpose X^T [R | Z], the dominant contraction)",
+                         "achieved": tensor_t, "peak": burst, "frac": tensor_t / burst,
+                         "peak_source": peak_src, "peak_sustained": sustained,
+                         "frac_vs_sustained": tensor_t / sustained,
+                         "flops_per_transpose_launch": 3 * useful_t,
+                         "note": "tensor FLOPs count the 3 fp16 products of the hi/lo split; "
+                                 "X^T [R | Z] has 2 n p B flops per product (x2 rows on bound "
+                                 "checks, averaged over the iterations)"},
             "ms_per_iteration_split": {"gemm_transpose": gt, "prox": px, "gemm_forward": gf},
             "cpu_baseline": cpu}
 

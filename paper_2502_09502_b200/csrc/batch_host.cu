@@ -454,11 +454,13 @@ int32_t l0_batch_create(const l0_problem* prob, int64_t n_nodes, l0_batch** out)
     }
   }
   // support-compacted forward (K = the cached columns, read on the device):
-  // a few dozen K blocks per unit at steady state, so two splits fill the SMs
+  // ~8 fp16 K blocks per tile at steady state on C4, one split (measured: 1
+  // split 0.958 ms per batched iteration, 2 splits 0.991, 3 splits 1.049 --
+  // the partials' HBM round trip costs more than the wave quantisation)
   Bt->sparse = getenv("L0_SPARSE_FWD") ? atoi(getenv("L0_SPARSE_FWD")) : 1;
   TcGemmArgs& gfs = Bt->gfs;
   gfs = gf;
-  gfs.S = getenv("L0_TC_SFS") ? std::max(1, atoi(getenv("L0_TC_SFS"))) : 2;
+  gfs.S = getenv("L0_TC_SFS") ? std::max(1, atoi(getenv("L0_TC_SFS"))) : 1;
   gfs.units = gfs.S * gfs.m_tiles * gfs.n_tiles;
   gfs.streamk = 0;
   g.sf_init = gf.S;
