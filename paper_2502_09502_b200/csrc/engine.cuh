@@ -80,12 +80,13 @@ struct EngineArgs {
   int fz_cs, fz_ncl, fz_nv, fz_rows;   // cluster size, clusters, vectors/thread, rows/tile
   int fz_stages;     // shared-memory tile ring depth
   int fz_slots;      // partial-slot ring depth
-  int fz_widen;
+  int fz_widen;      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
+  int fz_lin;        // squared error: one accumulated vector A_t = X^T grad F(u_t) (fused.cu LIN)
   int f32_forward;   // fp32 X: forward products in fp32 (FistaOptions.fp32_forward; fused.cu)
-  uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
+  uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)
   int64_t fz_tiles;  // row tiles
-  double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta)
+  double* fz_part;   // [3][fz_ncl][pv] transpose partials (restart / no-restart / zeta; LIN: [fz_ncl][pv])
   double* fz_cpart;  // [fz_ncl][8] per-cluster loss, non-finite, F* sums
   int prox_full_sort; // 1: K3 sorts all p keys (reference check path); 0: windowed sort
   // verification ring of K3 decisions (l0_problem_set_prox_record; nullptr: off):
@@ -165,7 +166,7 @@ int k2_blocks_per_sm(int dtype);
 cudaError_t launch_objective(const EngineArgs& a, int mode, cudaStream_t s);
 cudaError_t launch_fused(const EngineArgs& a, int mode, cudaStream_t s);
 cudaError_t launch_fused_reduce(const EngineArgs& a, int mode, cudaStream_t s);
-cudaError_t launch_fused_pick(const EngineArgs& a, cudaStream_t s);
+cudaError_t launch_fused_pick(const EngineArgs& a, int mode, cudaStream_t s);
 int fused_plan(EngineArgs& a, int sms);   // 0: the problem does not fit the fused kernel
 cudaError_t launch_prox_iter(const EngineArgs& a, void* sort_tmp, size_t sort_tmp_bytes,
                              cudaStream_t s);

@@ -145,6 +145,9 @@ static int compute_layout(Problem& P) {
   a.k2_chunks = (int)ceil_div(n, a.k2_rows);
   a.k2_grid = (int)std::min<int64_t>(k2_res, k2_groups * a.k2_chunks);
   a.prox_full_sort = getenv("L0_FULL_SORT") ? atoi(getenv("L0_FULL_SORT")) : 0;
+  // squared error: gradient candidates by linearity from one accumulated
+  // vector (fused.cu LIN); L0_FZ_LIN=0 keeps the two-candidate kernel
+  a.fz_lin = (a.loss == SQUARED_ERROR && (!getenv("L0_FZ_LIN") || atoi(getenv("L0_FZ_LIN")))) ? 1 : 0;
   a.fused = fused_plan(a, sms) ? 1 : 0;
   P.fused_planned = a.fused;
   if (!a.fused) { a.fz_ncl = 1; a.fz_cs = 1; }
@@ -220,12 +223,13 @@ static int fused_tail(Problem& P, int mode, cudaStream_t s) {
   L0_CUDA_TRY(launch_fused_reduce(a, mode, s));
   if (a.multi) {
     if (P.comm) {
-      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)(3 * a.pv + 8), ncclDouble, ncclSum,
-                                        P.comm, s);
+      // LIN: A_t, the loss and the flags only (gv's third block keeps A_{t-1})
+      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)((a.fz_lin ? 2 : 3) * a.pv + 8),
+                                        ncclDouble, ncclSum, P.comm, s);
       if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (fused) failed");
     }
     L0_CUDA_TRY(launch_objective(a, mode, s));
-    L0_CUDA_TRY(launch_fused_pick(a, s));
+    L0_CUDA_TRY(launch_fused_pick(a, mode, s));
   }
   return ST_OK;
 }

@@ -179,7 +179,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // fz_part, per-cluster loss / flags / F* sums to fz_cpart, and in the last CTA
 // of the grid the fixed-order reduction over clusters and the objective /
 // restart logic.  Transpose thread lt owns columns c0 + v*kFzTr*VE + lt*VE + e.
-template <int NA, int VE>
+template <int NA, int VE, bool LIN>
 __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t t, bool want_z, int cid,
                                           uint32_t crank, int64_t c0, bool is_tr, int lt,
                                           const double* accR, const double* accN, const double* accZ,
@@ -198,8 +198,10 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
         const int64_t col = c0 + (int64_t)v * kFzTr * VE + lt * VE + e;
         if (col < pv) {
           a.fz_part[(0 * (int64_t)ncl + cid) * pv + col] = accR[v * VE + e];
-          a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
-          if (want_z) a.fz_part[(2 * (int64_t)ncl + cid) * pv + col] = accZ[v * VE + e];
+          if constexpr (!LIN) {
+            a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
+            if (want_z) a.fz_part[(2 * (int64_t)ncl + cid) * pv + col] = accZ[v * VE + e];
+          }
         }
       }
     }
@@ -321,7 +323,13 @@ __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~si
 // BASELINE's "fp32 X with fp64 reductions", within the north star's 1e-5
 // fp32-mode tolerance.  The transpose products stay fp64 (the gradient and
 // the Fenchel bound are exact for the residuals the forward produced).
-template <typename TX, int R, int NV, bool F32F = false>
+//
+// LIN (squared error, whose gradient is affine in u): the gradients of both
+// momentum candidates and X^T zeta follow from A_t = X^T grad F(u_t) alone,
+//   X^T grad F(u_t + c (u_t - u_{t-1})) = A_t + c (A_t - A_{t-1}),  X^T zeta_t = -A_t,
+// so the tile accumulates ONE residual vector instead of two or three (KR
+// keeps A_{t-1} and forms the chosen candidate; fista.py:161-163, :152).
+template <typename TX, int R, int NV, bool F32F = false, bool LIN = false>
 __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
   constexpr int G = fs_gather<TX>();
   constexpr int kFsProdWarp = fs_prod_warp<G>();
@@ -417,7 +425,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
   if (cs > 1) cluster_barrier();
   else __syncthreads();
 
-  double accR[NV * VE], accN[NV * VE], accZ[NV * VE];
+  constexpr int NB = LIN ? 1 : NV * VE;           // candidate N / zeta accumulators (unused: LIN)
+  double accR[NV * VE], accN[NB], accZ[NB];
   double loss_acc = 0.0, f_acc[3] = {0.0, 0.0, 0.0};
   int bad = 0, gbad_R = 0, gbad_N = 0;
 
@@ -593,7 +602,19 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
           yi = a.y[row];
           up = (mode == MODE_ITER) ? uprev[row] : u;
         }
-        if (f < 3) {
+        if (LIN && f < 3) {
+          // f = 0: grad F(u_t) (= -zeta_t); f = 1, 2: X gamma of the two
+          // momenta must be finite (loss_gradient raises otherwise, model.py:215)
+          if (f == 0) {
+            const double g = F32F ? loss_grad_f32m(a.loss, u, yi) : loss_grad(a.loss, u, yi);
+            sh.rr[buf][0][r] = g;
+            if (crank == 0 && want_z) conj_accumulate(a.loss, -g, yi, f_acc);
+          } else {
+            const double arg = dadd(u, dmul(f == 1 ? cR : cN, dsub(u, up)));
+            if (f == 1 && !isfinite(arg)) gbad_R = 1;
+            if (f == 2 && !isfinite(arg)) gbad_N = 1;
+          }
+        } else if (f < 3) {
           const double dlt = dsub(u, up);
           // X gamma for the two momenta (fista.py:161-162); zeta_t = -grad F(u_t) (fista.py:152)
           const double arg = f == 0 ? dadd(u, dmul(cR, dlt)) : (f == 1 ? dadd(u, dmul(cN, dlt)) : u);
@@ -612,7 +633,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
           if (!isfinite(u)) bad = 1;
           loss_acc += F32F ? loss_term_f32m(a.loss, u, yi) : loss_term(a.loss, u, yi);
         }
-      } else if (f < 4 && f < 3) {
+      } else if (f < (LIN ? 1 : 3)) {
         sh.rr[buf][f][r] = 0.0;
       }
       __syncwarp();
@@ -635,7 +656,9 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
     // ===================== accumulate =====================
     const int lt = tid - kFsAccWarp0 * 32;
 #pragma unroll
-    for (int i = 0; i < NV * VE; ++i) { accR[i] = 0.0; accN[i] = 0.0; accZ[i] = 0.0; }
+    for (int i = 0; i < NV * VE; ++i) accR[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) { accN[i] = 0.0; accZ[i] = 0.0; }
     int buf = 0;
     uint32_t ph = 0;
     for (int k = 0; k < mytiles; ++k) {
@@ -649,9 +672,12 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       if (sizeof(TX) == 4 && (a.fz_widen & 2) && rows == R) {
         aint = true;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          aint = aint && isfinite(sh.rr[buf][0][r] * kRebias) && isfinite(sh.rr[buf][1][r] * kRebias) &&
-                 (!want_z || isfinite(sh.rr[buf][2][r] * kRebias));
+        for (int r = 0; r < R; ++r) {
+          aint = aint && isfinite(sh.rr[buf][0][r] * kRebias);
+          if constexpr (!LIN)
+            aint = aint && isfinite(sh.rr[buf][1][r] * kRebias) &&
+                   (!want_z || isfinite(sh.rr[buf][2][r] * kRebias));
+        }
       }
       auto acc_full = [&](auto INT) {
         constexpr bool kInt = decltype(INT)::value;
@@ -669,8 +695,9 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
 #pragma unroll
           for (int h = 0; h < RP; ++h) {
             const int r = r0 + h;
-            const double rR = sh.rr[buf][0][r] * sc, rN = sh.rr[buf][1][r] * sc;
-            const double rZ = want_z ? sh.rr[buf][2][r] * sc : 0.0;
+            const double rR = sh.rr[buf][0][r] * sc;
+            const double rN = LIN ? 0.0 : sh.rr[buf][1][r] * sc;
+            const double rZ = (!LIN && want_z) ? sh.rr[buf][2][r] * sc : 0.0;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               double x[VE];
@@ -679,11 +706,13 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
 #pragma unroll
               for (int e = 0; e < VE; ++e) {
                 accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-                accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+                if constexpr (!LIN) accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
               }
-              if (want_z) {
+              if constexpr (!LIN) {
+                if (want_z) {
 #pragma unroll
-                for (int e = 0; e < VE; ++e) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+                  for (int e = 0; e < VE; ++e) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+                }
               }
             }
           }
@@ -696,7 +725,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       } else {
         // the last, partial tile of the grid: rows past n hold stale data
         for (int r = 0; r < rows; ++r) {
-          const double rR = sh.rr[buf][0][r], rN = sh.rr[buf][1][r], rZ = sh.rr[buf][2][r];
+          const double rR = sh.rr[buf][0][r];
+          const double rN = LIN ? 0.0 : sh.rr[buf][1][r], rZ = LIN ? 0.0 : sh.rr[buf][2][r];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             double x[VE];
@@ -704,8 +734,10 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
 #pragma unroll
             for (int e = 0; e < VE; ++e) {
               accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-              accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
-              if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+              if constexpr (!LIN) {
+                accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+                if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
+              }
             }
           }
         }
@@ -717,9 +749,25 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
     }
   }
   __syncthreads();
-  kf_finish<NV * VE, VE>(a, mode, t, want_z, cid, crank, c0, warp >= kFsAccWarp0,
+  kf_finish<NV * VE, VE, LIN>(a, mode, t, want_z, cid, crank, c0, warp >= kFsAccWarp0,
                          tid - kFsAccWarp0 * 32, accR, accN, accZ, loss_acc, f_acc, bad, gbad_R, gbad_N,
                          &sh.bad, sh.red);
+}
+
+// LIN: the chosen candidate from A_t (reduced over clusters / ranks) and the
+// kept A_{t-1} (gv's no-restart block, unused in this mode):
+//   g = A_t + c (A_t - A_{t-1}),  c = momentum after the restart decision
+//   (fista.py:161-163; at the initial pass u_{-1} = u_0, so g = A_0),
+//   X^T zeta_t = -A_t (fista.py:152).
+__device__ __forceinline__ double lin_candidate(const EngineArgs& a, int mode, int64_t j, double At,
+                                                bool wg, double* v) {
+  double* keep = a.gv + 2 * a.pv + 8;
+  *v = -At;
+  if (j >= a.p) return 0.0;
+  double g = At;
+  if (mode == MODE_ITER) g = dadd(At, dmul(momentum(a.st->phi), dsub(At, keep[j])));
+  if (wg) keep[j] = At;   // a bound-only pass re-reduces the same A_t
+  return g;
 }
 
 // ---------------------------------------------------------------------------
@@ -739,6 +787,31 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
   // restart -> phi = 1 -> c = 1/4 (candidate R); else candidate N
   const bool use_R = (mode != MODE_ITER) || st->last_restarted;
   double g = 0.0, gn = 0.0, v = 0.0;
+  if (a.fz_lin) {
+    // one partial vector A_t = X^T grad F(u_t) (kf_fused_s LIN)
+    if (j < p)
+      for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
+    if (!epilogue) {  // row-sharded: A_t goes through the all-reduce, kr_pick extrapolates
+      if (j < p) a.gv[j] = g;
+      return;
+    }
+    const double gsel = lin_candidate(a, mode, j, g, wg, &v);
+    if (j < p) {
+      a.gv[j] = gsel;
+      a.gv[pv + j] = v;
+    }
+    if (wg && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int flags = (int)a.gv[2 * pv + 6];
+      if (flags & (use_R ? 2 : 4)) {
+        State* sw = a.st;
+        atomicExch(&sw->err, (int)ST_INVALID);
+        sw->err_iter = sw->t + 1;
+        sw->done = 1;
+      }
+    }
+    slab_epilogue(a, blockIdx.x, st->t + 1, momentum(st->phi), wg, wz, gsel, v, sm);
+    return;
+  }
   if (j < p) {
     if (wg || !epilogue) {
       for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (0 * (int64_t)ncl + c) * pv + j);
@@ -776,7 +849,7 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
 }
 
 // row-sharded fused mode: pick the all-reduced candidate, then the epilogue
-__global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a) {
+__global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a, int mode) {
   __shared__ EpiSmem sm;
   const State* st = a.st;
   if (st->done) return;
@@ -786,9 +859,16 @@ __global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a) {
   const int64_t pv = a.pv;
   const int64_t j = (int64_t)blockIdx.x * kK2Slab + threadIdx.x;
   const bool use_R = st->last_restarted != 0;
+  const int64_t t = st->t + 1;
+  if (a.fz_lin) {
+    double v = 0.0;
+    const double At = j < a.p ? a.gv[j] : 0.0;
+    const double g = lin_candidate(a, mode, j, At, wg, &v);
+    slab_epilogue(a, blockIdx.x, t, momentum(st->phi), wg, wz, g, v, sm);
+    return;
+  }
   const double g = j < a.p ? (use_R ? a.gv[j] : a.gv[2 * pv + 8 + j]) : 0.0;
   const double v = (wz && j < a.p) ? a.gv[pv + j] : 0.0;
-  const int64_t t = st->t + 1;
   slab_epilogue(a, blockIdx.x, t, momentum(st->phi), wg, wz, g, v, sm);
 }
 
@@ -803,27 +883,42 @@ static size_t fused_smem(const EngineArgs& a) {
 
 using KfFn = void (*)(EngineArgs, int);
 
-template <typename TX, int R, bool F32F = false>
+template <typename TX, int R, bool F32F, bool LIN>
 static KfFn kfs_pick_nv(int nv) {
   switch (nv) {
-    case 1: return kf_fused_s<TX, R, 1, F32F>;
-    case 2: return kf_fused_s<TX, R, 2, F32F>;
-    case 3: return kf_fused_s<TX, R, 3, F32F>;
-    case 4: return sizeof(TX) == 8 ? (KfFn)kf_fused_s<TX, R, 4> : nullptr;
+    case 1: return kf_fused_s<TX, R, 1, F32F, LIN>;
+    case 2: return kf_fused_s<TX, R, 2, F32F, LIN>;
+    case 3: return kf_fused_s<TX, R, 3, F32F, LIN>;
+    case 4:
+      if constexpr (sizeof(TX) == 8 || LIN) return kf_fused_s<TX, R, 4, F32F, LIN>;
+      return nullptr;
+    case 5:
+      if constexpr (sizeof(TX) == 4 && LIN && R == 2) return kf_fused_s<TX, R, 5, F32F, LIN>;
+      return nullptr;
+    case 6:
+      if constexpr (sizeof(TX) == 4 && LIN && R == 2) return kf_fused_s<TX, R, 6, F32F, LIN>;
+      return nullptr;
     default: return nullptr;
   }
 }
 
-static KfFn kf_pick(const EngineArgs& a) {
-  const bool f64 = a.dtype == F64;
-  if (!f64 && a.f32_forward) {   // fp32 mode (FistaOptions.fp32_forward)
-    if (a.fz_rows == 2) return kfs_pick_nv<float, 2, true>(a.fz_nv);
-    if (a.fz_rows == 4) return kfs_pick_nv<float, 4, true>(a.fz_nv);
-    return nullptr;
-  }
-  if (a.fz_rows == 2) return f64 ? kfs_pick_nv<double, 2>(a.fz_nv) : kfs_pick_nv<float, 2>(a.fz_nv);
-  if (a.fz_rows == 4) return f64 ? kfs_pick_nv<double, 4>(a.fz_nv) : kfs_pick_nv<float, 4>(a.fz_nv);
+template <typename TX, bool F32F, bool LIN>
+static KfFn kfs_pick_r(int rows, int nv) {
+  if (rows == 2) return kfs_pick_nv<TX, 2, F32F, LIN>(nv);
+  if (rows == 4) return kfs_pick_nv<TX, 4, F32F, LIN>(nv);
   return nullptr;
+}
+
+static KfFn kf_pick(const EngineArgs& a) {
+  const bool lin = a.fz_lin != 0;
+  if (a.dtype == F64)
+    return lin ? kfs_pick_r<double, false, true>(a.fz_rows, a.fz_nv)
+               : kfs_pick_r<double, false, false>(a.fz_rows, a.fz_nv);
+  if (a.f32_forward)   // fp32 mode (FistaOptions.fp32_forward)
+    return lin ? kfs_pick_r<float, true, true>(a.fz_rows, a.fz_nv)
+               : kfs_pick_r<float, true, false>(a.fz_rows, a.fz_nv);
+  return lin ? kfs_pick_r<float, false, true>(a.fz_rows, a.fz_nv)
+             : kfs_pick_r<float, false, false>(a.fz_rows, a.fz_nv);
 }
 
 static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at,
@@ -861,11 +956,13 @@ int fused_plan(EngineArgs& a, int sms) {
   const int VE = a.dtype == F64 ? 2 : 4;
   const int64_t unit = (int64_t)kFzTr * VE;   // columns per accumulate-thread vector sweep
   const size_t es = a.dtype == F64 ? 8 : 4;
-  const int maxv = a.dtype == F64 ? 4 : 3;
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
   const char* renv = getenv("L0_FZ_R");
   const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : (a.dtype == F64 ? 2 : 4);
+  // vectors per accumulate thread: the accumulator registers bound the column
+  // slice (LIN keeps one accumulator per column instead of three)
+  const int maxv = a.dtype == F64 ? 4 : (a.fz_lin ? (R == 2 ? 6 : 4) : 3);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -942,8 +1039,8 @@ cudaError_t launch_fused_reduce(const EngineArgs& a, int mode, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_fused_pick(const EngineArgs& a, cudaStream_t s) {
-  kr_pick<<<a.k2_slabs, kK2Slab, 0, s>>>(a);
+cudaError_t launch_fused_pick(const EngineArgs& a, int mode, cudaStream_t s) {
+  kr_pick<<<a.k2_slabs, kK2Slab, 0, s>>>(a, mode);
   return cudaGetLastError();
 }
 
