@@ -607,7 +607,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   // it/s, C5 73.6 vs 64.3, C3 even), the two-pass engine otherwise (small X:
   // L2 serves the second pass)
   const double x_bytes = (double)a.n * (double)a.ld * (a.dtype == F64 ? 8.0 : 4.0);
-  const int auto_fused = P->fused_planned && a.fz_cs >= 4 && a.fz_cs <= 8 &&
+  const int auto_fused = P->fused_planned && a.fz_cs >= (a.fz_lin ? 2 : 4) && a.fz_cs <= 8 &&
                          x_bytes > 512e6;   // L2-resident X (C1): the second pass hits L2
   const int want_fused = (o->engine_path == 2) ? P->fused_planned
                          : (o->engine_path == 1) ? 0 : auto_fused;

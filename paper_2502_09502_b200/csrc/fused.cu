@@ -948,7 +948,11 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
 // Cluster size, rows per tile and ring depth: the smallest cluster (override:
 // L0_FZ_CS) whose column slice fits the accumulate registers, R = 2 rows per
 // tile for fp64 X (C2: 0.352 ms; R = 4 spills at 17 warps: 0.39 ms) and 4 for
-// fp32 X (C5: 9.96 vs 12.0 ms, C3: 1.18 vs 1.59 ms; L0_FZ_R overrides), and as many stages as the shared memory holds next to the
+// fp32 X with two or three accumulated vectors (C5: 9.96 vs 12.0 ms, C3: 1.18
+// vs 1.59 ms; L0_FZ_R overrides); fp32 X in the LIN kernel takes 2-row tiles
+// and up to 6 vectors per thread, i.e. half the cluster size (C5 at n = 200k:
+// clusters of 2 x 5120 columns, 148 SMs, KF 1.17 ms = 6.85 TB/s against 1.67
+// ms with 4-row tiles in clusters of 4 on 132 SMs), and as many stages as the shared memory holds next to the
 // partial slots (<= kFsMaxStages; slots = 2 x stages, see the slot-reuse
 // argument above; L0_FZ_S caps the stages).
 int fused_plan(EngineArgs& a, int sms) {
@@ -959,7 +963,7 @@ int fused_plan(EngineArgs& a, int sms) {
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
   const char* renv = getenv("L0_FZ_R");
-  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : (a.dtype == F64 ? 2 : 4);
+  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : ((a.dtype == F64 || a.fz_lin) ? 2 : 4);
   // vectors per accumulate thread: the accumulator registers bound the column
   // slice (LIN keeps one accumulator per column instead of three)
   const int maxv = a.dtype == F64 ? 4 : (a.fz_lin ? (R == 2 ? 6 : 4) : 3);
@@ -984,7 +988,8 @@ int fused_plan(EngineArgs& a, int sms) {
     a.fz_slots = 2 * S;
     // fp32 X: widen by integer rebias (bit 0 forward warps, bit 1 accumulate
     // warps) instead of F2F on the XU pipe; L0_FZ_WIDEN overrides
-    a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : 3;
+    // (LIN: forward warps only -- C5 at n = 200k: 1.168 vs 1.194 ms with both)
+    a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : (a.fz_lin ? 1 : 3);
     a.fz_cs = cs;
     // suspend-time hint of the role waits (ns); L0_FZ_SLEEP overrides
     a.fz_sleep = getenv("L0_FZ_SLEEP") ? (uint32_t)atoi(getenv("L0_FZ_SLEEP")) : 1000u;
