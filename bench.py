@@ -515,6 +515,16 @@ def run_config(name, iters):
         kern = {"kf_fused_s": {"launch_ms": avg("k2"), "achieved_gbs": (xb + 8 * (4 * n + p)) / avg("k2") / 1e6},
                 "kr_reduce": {"launch_ms": avg("k1")}, "k3_prox_window": {"launch_ms": avg("k3")}}
         kern["kf_fused_s"]["frac"] = kern["kf_fused_s"]["achieved_gbs"] / peak
+        if cd.loss != "squared_error" and cd.dtype == "fp32":
+            # SPEC kernel: KF accumulates the no-restart candidate only; restart and
+            # bound-check iterations add one K2 transpose pass behind KR
+            kern["kr_reduce_plus_conditional_k2"] = kern.pop("kr_reduce")
+            kern["kr_reduce_plus_conditional_k2"]["note"] = (
+                "average over all iterations of KR plus the K2 pass that runs on restart / "
+                "bound-check iterations only (one extra read of X on those)")
+            kern["kf_fused_s"]["variant"] = "SPEC (one accumulated vector)"
+        elif cd.loss == "squared_error":
+            kern["kf_fused_s"]["variant"] = "LIN (one accumulated vector, candidates by linearity)"
     else:
         kern = {"k1_forward": {"launch_ms": avg("k1"), "achieved_gbs": (xb + 8 * (p + 2 * n)) / avg("k1") / 1e6},
                 "k2_transpose": {"launch_ms": avg("k2"), "achieved_gbs": (xb + 8 * (3 * n + 5 * p)) / avg("k2") / 1e6},

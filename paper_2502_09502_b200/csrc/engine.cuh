@@ -81,7 +81,10 @@ struct EngineArgs {
   int fz_stages;     // shared-memory tile ring depth
   int fz_slots;      // partial-slot ring depth
   int fz_widen;      // fp32 X: bit 0 forward, bit 1 accumulate widen by integer rebias (fused.cu)
-  int fz_lin;        // squared error: one accumulated vector A_t = X^T grad F(u_t) (fused.cu LIN)
+  int fz_one;        // single-pass kernel with ONE accumulated vector (fused.cu): 1 squared error
+                     // (LIN: candidates by linearity), 2 SPEC (no-restart candidate; restarts
+                     // and bound checks through the K2 launch that follows), 0 three vectors
+  int k2_cond;       // K2 launched behind the SPEC kernel: runs only for restarts / bound passes
   int f32_forward;   // fp32 X: forward products in fp32 (FistaOptions.fp32_forward; fused.cu)
   uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)

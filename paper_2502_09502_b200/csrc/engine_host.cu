@@ -102,6 +102,16 @@ struct Problem {
   Graph graphs[2][2];   // [profile][double-buffer slot]: both variants stay captured
   Graph* graph = graphs[0];
   int fused_planned = 0;
+  // single-pass plans: [0] the default kernel of the loss (LIN for squared
+  // error, three vectors otherwise), [1] SPEC (one vector; non-linear losses
+  // on fp32 X, single-GPU solves only: its conditional K2 launch has no
+  // place between the all-reduces of the row-sharded path)
+  struct FzPlan {
+    int ok = 0, one = 0, cs = 1, ncl = 1, nv = 0, rows = 0, stages = 0, slots = 0, widen = 0;
+    uint32_t sleep = 0;
+    int64_t w = 0, tiles = 0;
+  } plan[2];
+  int plan_sel = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int force_full_sort = 0;      // re-run after a window tie overflow (ST_TIE_OVERFLOW)
@@ -113,6 +123,21 @@ struct Problem {
 struct l0_problem : l0::Problem {};
 
 namespace l0 {
+
+// install a single-pass plan into the kernel arguments (graphs captured with
+// another plan are dropped by the caller)
+static void select_plan(Problem& P, int which) {
+  EngineArgs& a = P.a;
+  const Problem::FzPlan& pl = P.plan[which];
+  P.plan_sel = which;
+  a.fz_one = pl.one;
+  a.fz_cs = pl.cs; a.fz_ncl = pl.ncl; a.fz_nv = pl.nv; a.fz_rows = pl.rows;
+  a.fz_stages = pl.stages; a.fz_slots = pl.slots; a.fz_widen = pl.widen;
+  a.fz_sleep = pl.sleep; a.fz_w = pl.w; a.fz_tiles = pl.tiles;
+  a.fused = pl.ok;
+  P.fused_planned = pl.ok;
+  if (!pl.ok) { a.fz_ncl = 1; a.fz_cs = 1; }
+}
 
 static int compute_layout(Problem& P) {
   EngineArgs& a = P.a;
@@ -147,10 +172,23 @@ static int compute_layout(Problem& P) {
   a.prox_full_sort = getenv("L0_FULL_SORT") ? atoi(getenv("L0_FULL_SORT")) : 0;
   // squared error: gradient candidates by linearity from one accumulated
   // vector (fused.cu LIN); L0_FZ_LIN=0 keeps the two-candidate kernel
-  a.fz_lin = (a.loss == SQUARED_ERROR && (!getenv("L0_FZ_LIN") || atoi(getenv("L0_FZ_LIN")))) ? 1 : 0;
-  a.fused = fused_plan(a, sms) ? 1 : 0;
-  P.fused_planned = a.fused;
-  if (!a.fused) { a.fz_ncl = 1; a.fz_cs = 1; }
+  auto env_on = [](const char* k) { return !getenv(k) || atoi(getenv(k)) != 0; };
+  auto plan_one = [&](int one) {
+    Problem::FzPlan pl;
+    a.fz_one = one;
+    pl.ok = fused_plan(a, sms) ? 1 : 0;
+    pl.one = one;
+    if (pl.ok) {
+      pl.cs = a.fz_cs; pl.ncl = a.fz_ncl; pl.nv = a.fz_nv; pl.rows = a.fz_rows;
+      pl.stages = a.fz_stages; pl.slots = a.fz_slots; pl.widen = a.fz_widen;
+      pl.sleep = a.fz_sleep; pl.w = a.fz_w; pl.tiles = a.fz_tiles;
+    }
+    return pl;
+  };
+  // L0_FZ_SPEC=0 keeps the three-vector kernel for non-linear losses on fp32 X
+  if (a.loss != SQUARED_ERROR && a.dtype == F32 && env_on("L0_FZ_SPEC")) P.plan[1] = plan_one(2);
+  P.plan[0] = plan_one((a.loss == SQUARED_ERROR && env_on("L0_FZ_LIN")) ? 1 : 0);
+  select_plan(P, 0);
   P.sort_tmp_bytes = std::max(prox_sort_tmp_bytes(std::max<int64_t>(p, 1)), (size_t)256);
   size_t keys_only = 0;
   cub::DeviceRadixSort::SortKeysDescending<double>(nullptr, keys_only, (const double*)nullptr,
@@ -197,8 +235,9 @@ static uint64_t carve(Problem& P, char* base) {
   a.slab_below = (double*)take(8ull * S);
   a.slab_hfone = (double*)take(8ull * S);
   a.slab_htop = (double*)take(8ull * S * kHTop);
-  a.fz_part = (double*)take(8ull * 3 * (uint64_t)std::max(a.fz_ncl, 1) * pv);
-  a.fz_cpart = (double*)take(8ull * 8 * (uint64_t)std::max(a.fz_ncl, 1));
+  const uint64_t ncl_max = (uint64_t)std::max(1, std::max(P.plan[0].ncl, P.plan[1].ncl));
+  a.fz_part = (double*)take(8ull * 3 * ncl_max * pv);
+  a.fz_cpart = (double*)take(8ull * 8 * ncl_max);
   P.d_mask = (uint8_t*)take(pv);
   P.d_fone = (int*)take(4ull * pv);
   P.sort_tmp = take(P.sort_tmp_bytes);
@@ -224,12 +263,18 @@ static int fused_tail(Problem& P, int mode, cudaStream_t s) {
   if (a.multi) {
     if (P.comm) {
       // LIN: A_t, the loss and the flags only (gv's third block keeps A_{t-1})
-      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)((a.fz_lin ? 2 : 3) * a.pv + 8),
+      ncclResult_t r = g_nccl.allReduce(a.gv, a.gv, (size_t)((a.fz_one == 1 ? 2 : 3) * a.pv + 8),
                                         ncclDouble, ncclSum, P.comm, s);
       if (r != ncclSuccess) return set_error(ST_CUDA, "ncclAllReduce (fused) failed");
     }
     L0_CUDA_TRY(launch_objective(a, mode, s));
     L0_CUDA_TRY(launch_fused_pick(a, mode, s));
+  } else if (a.fz_one == 2 && mode == MODE_ITER) {
+    // SPEC: restart iterations and bound passes take the two-pass engine's
+    // transpose kernel (it exits at entry on every other iteration)
+    EngineArgs a2 = a;
+    a2.k2_cond = 1;
+    L0_CUDA_TRY(launch_k2(a2, MODE_ITER, s));
   }
   return ST_OK;
 }
@@ -607,7 +652,14 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   // it/s, C5 73.6 vs 64.3, C3 even), the two-pass engine otherwise (small X:
   // L2 serves the second pass)
   const double x_bytes = (double)a.n * (double)a.ld * (a.dtype == F64 ? 8.0 : 4.0);
-  const int auto_fused = P->fused_planned && a.fz_cs >= (a.fz_lin ? 2 : 4) && a.fz_cs <= 8 &&
+  {
+    const int which = (P->plan[1].ok && !a.multi) ? 1 : 0;
+    if (which != P->plan_sel) {
+      destroy_graphs(*P);
+      select_plan(*P, which);
+    }
+  }
+  const int auto_fused = P->fused_planned && a.fz_cs >= (a.fz_one ? 2 : 4) && a.fz_cs <= 8 &&
                          x_bytes > 512e6;   // L2-resident X (C1): the second pass hits L2
   const int want_fused = (o->engine_path == 2) ? P->fused_planned
                          : (o->engine_path == 1) ? 0 : auto_fused;
@@ -776,7 +828,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
       if (a.fused) {  // the final bound pass needs the Huber values of zeta_t
         rc = fused_tail(*P, MODE_ITER, s);
         if (rc) return rc;
-        ++launches;
+        launches += a.fz_one == 2 ? 2 : 1;
       }
       stop_sent = true;
     }

@@ -329,8 +329,17 @@ __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~si
 //   X^T grad F(u_t + c (u_t - u_{t-1})) = A_t + c (A_t - A_{t-1}),  X^T zeta_t = -A_t,
 // so the tile accumulates ONE residual vector instead of two or three (KR
 // keeps A_{t-1} and forms the chosen candidate; fista.py:161-163, :152).
-template <typename TX, int R, int NV, bool F32F = false, bool LIN = false>
+//
+// SPEC (ONE = 2; logistic / squared hinge on fp32 X, where three accumulated
+// vectors keep the kernel far from the HBM roofline): the tile accumulates the
+// NO-RESTART candidate X^T grad F(u_t + c_N (u_t - u_{t-1})) only.  Iterations
+// that restart, and bound checks (X^T zeta_t), take one extra transpose pass
+// (the two-pass engine's K2, launched after KR and exiting at entry otherwise):
+// ~1 in 6 iterations on C3 against 3x fewer accumulators, clusters of 4
+// instead of 8 and a third of the gather's loss evaluations.
+template <typename TX, int R, int NV, bool F32F = false, int ONE = 0>
 __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
+  constexpr bool LIN = ONE != 0;    // one accumulated vector (ONE = 1: squared error, 2: SPEC)
   constexpr int G = fs_gather<TX>();
   constexpr int kFsProdWarp = fs_prod_warp<G>();
   constexpr int kFsAccWarp0 = fs_acc_warp0<G>();
@@ -602,7 +611,14 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
           yi = a.y[row];
           up = (mode == MODE_ITER) ? uprev[row] : u;
         }
-        if (LIN && f < 3) {
+        if (ONE == 2 && f < 3) {
+          // SPEC: the no-restart candidate only (fista.py:161-162)
+          if (f == 0) {
+            const double arg = dadd(u, dmul(cN, dsub(u, up)));
+            if (!isfinite(arg)) gbad_N = 1;
+            sh.rr[buf][0][r] = F32F ? loss_grad_f32m(a.loss, arg, yi) : loss_grad(a.loss, arg, yi);
+          }
+        } else if (LIN && f < 3) {
           // f = 0: grad F(u_t) (= -zeta_t); f = 1, 2: X gamma of the two
           // momenta must be finite (loss_gradient raises otherwise, model.py:215)
           if (f == 0) {
@@ -787,7 +803,23 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
   // restart -> phi = 1 -> c = 1/4 (candidate R); else candidate N
   const bool use_R = (mode != MODE_ITER) || st->last_restarted;
   double g = 0.0, gn = 0.0, v = 0.0;
-  if (a.fz_lin) {
+  if (a.fz_one == 2) {
+    // SPEC: KF accumulated the no-restart candidate; restarts, bound checks
+    // and bound-only passes belong to the K2 launch that follows
+    if (mode == MODE_ITER && (st->last_restarted || st->dual_pending || st->dual_only)) return;
+    if (j < p)
+      for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
+    if (j < p) a.gv[j] = g;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && mode == MODE_ITER && ((int)a.gv[2 * pv + 6] & 4)) {
+      State* sw = a.st;   // non-finite X gamma: loss_gradient raises (model.py:215)
+      atomicExch(&sw->err, (int)ST_INVALID);
+      sw->err_iter = sw->t + 1;
+      sw->done = 1;
+    }
+    slab_epilogue(a, blockIdx.x, st->t + 1, momentum(st->phi), true, false, g, 0.0, sm);
+    return;
+  }
+  if (a.fz_one == 1) {
     // one partial vector A_t = X^T grad F(u_t) (kf_fused_s LIN)
     if (j < p)
       for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
@@ -860,7 +892,7 @@ __global__ void __launch_bounds__(kK2Slab) kr_pick(EngineArgs a, int mode) {
   const int64_t j = (int64_t)blockIdx.x * kK2Slab + threadIdx.x;
   const bool use_R = st->last_restarted != 0;
   const int64_t t = st->t + 1;
-  if (a.fz_lin) {
+  if (a.fz_one == 1) {
     double v = 0.0;
     const double At = j < a.p ? a.gv[j] : 0.0;
     const double g = lin_candidate(a, mode, j, At, wg, &v);
@@ -883,42 +915,49 @@ static size_t fused_smem(const EngineArgs& a) {
 
 using KfFn = void (*)(EngineArgs, int);
 
-template <typename TX, int R, bool F32F, bool LIN>
+template <typename TX, int R, bool F32F, int ONE>
 static KfFn kfs_pick_nv(int nv) {
   switch (nv) {
-    case 1: return kf_fused_s<TX, R, 1, F32F, LIN>;
-    case 2: return kf_fused_s<TX, R, 2, F32F, LIN>;
-    case 3: return kf_fused_s<TX, R, 3, F32F, LIN>;
+    case 1: return kf_fused_s<TX, R, 1, F32F, ONE>;
+    case 2: return kf_fused_s<TX, R, 2, F32F, ONE>;
+    case 3: return kf_fused_s<TX, R, 3, F32F, ONE>;
     case 4:
-      if constexpr (sizeof(TX) == 8 || LIN) return kf_fused_s<TX, R, 4, F32F, LIN>;
+      if constexpr (sizeof(TX) == 8 || ONE != 0) return kf_fused_s<TX, R, 4, F32F, ONE>;
       return nullptr;
     case 5:
-      if constexpr (sizeof(TX) == 4 && LIN && R == 2) return kf_fused_s<TX, R, 5, F32F, LIN>;
+      if constexpr (sizeof(TX) == 4 && ONE != 0 && R == 2) return kf_fused_s<TX, R, 5, F32F, ONE>;
       return nullptr;
     case 6:
-      if constexpr (sizeof(TX) == 4 && LIN && R == 2) return kf_fused_s<TX, R, 6, F32F, LIN>;
+      if constexpr (sizeof(TX) == 4 && ONE != 0 && R == 2) return kf_fused_s<TX, R, 6, F32F, ONE>;
       return nullptr;
     default: return nullptr;
   }
 }
 
-template <typename TX, bool F32F, bool LIN>
+template <typename TX, bool F32F, int ONE>
 static KfFn kfs_pick_r(int rows, int nv) {
-  if (rows == 2) return kfs_pick_nv<TX, 2, F32F, LIN>(nv);
-  if (rows == 4) return kfs_pick_nv<TX, 4, F32F, LIN>(nv);
+  if (rows == 2) return kfs_pick_nv<TX, 2, F32F, ONE>(nv);
+  if (rows == 4) {
+    if constexpr (ONE != 2) return kfs_pick_nv<TX, 4, F32F, ONE>(nv);
+  }
   return nullptr;
 }
 
+template <typename TX, bool F32F>
+static KfFn kfs_pick_one(int one, int rows, int nv) {
+  if (one == 1) return kfs_pick_r<TX, F32F, 1>(rows, nv);
+  if (one == 2) {
+    if constexpr (sizeof(TX) == 4) return kfs_pick_r<TX, F32F, 2>(rows, nv);
+    return nullptr;
+  }
+  return kfs_pick_r<TX, F32F, 0>(rows, nv);
+}
+
 static KfFn kf_pick(const EngineArgs& a) {
-  const bool lin = a.fz_lin != 0;
-  if (a.dtype == F64)
-    return lin ? kfs_pick_r<double, false, true>(a.fz_rows, a.fz_nv)
-               : kfs_pick_r<double, false, false>(a.fz_rows, a.fz_nv);
+  if (a.dtype == F64) return kfs_pick_one<double, false>(a.fz_one, a.fz_rows, a.fz_nv);
   if (a.f32_forward)   // fp32 mode (FistaOptions.fp32_forward)
-    return lin ? kfs_pick_r<float, true, true>(a.fz_rows, a.fz_nv)
-               : kfs_pick_r<float, true, false>(a.fz_rows, a.fz_nv);
-  return lin ? kfs_pick_r<float, false, true>(a.fz_rows, a.fz_nv)
-             : kfs_pick_r<float, false, false>(a.fz_rows, a.fz_nv);
+    return kfs_pick_one<float, true>(a.fz_one, a.fz_rows, a.fz_nv);
+  return kfs_pick_one<float, false>(a.fz_one, a.fz_rows, a.fz_nv);
 }
 
 static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at,
@@ -963,10 +1002,10 @@ int fused_plan(EngineArgs& a, int sms) {
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
   const char* renv = getenv("L0_FZ_R");
-  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : ((a.dtype == F64 || a.fz_lin) ? 2 : 4);
+  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : ((a.dtype == F64 || a.fz_one) ? 2 : 4);
   // vectors per accumulate thread: the accumulator registers bound the column
   // slice (LIN keeps one accumulator per column instead of three)
-  const int maxv = a.dtype == F64 ? 4 : (a.fz_lin ? (R == 2 ? 6 : 4) : 3);
+  const int maxv = a.dtype == F64 ? 4 : (a.fz_one ? (R == 2 ? 6 : 4) : 3);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -989,7 +1028,7 @@ int fused_plan(EngineArgs& a, int sms) {
     // fp32 X: widen by integer rebias (bit 0 forward warps, bit 1 accumulate
     // warps) instead of F2F on the XU pipe; L0_FZ_WIDEN overrides
     // (LIN: forward warps only -- C5 at n = 200k: 1.168 vs 1.194 ms with both)
-    a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : (a.fz_lin ? 1 : 3);
+    a.fz_widen = getenv("L0_FZ_WIDEN") ? atoi(getenv("L0_FZ_WIDEN")) : (a.fz_one ? 1 : 3);
     a.fz_cs = cs;
     // suspend-time hint of the role waits (ns); L0_FZ_SLEEP overrides
     a.fz_sleep = getenv("L0_FZ_SLEEP") ? (uint32_t)atoi(getenv("L0_FZ_SLEEP")) : 1000u;

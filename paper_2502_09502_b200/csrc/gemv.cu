@@ -464,6 +464,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_transpose(EngineArgs a, int 
   if (mode == MODE_ITER) {
     const State* st = a.st;
     if (st->done) return;
+    // behind the SPEC single-pass kernel (fused.cu): only the iterations KR left
+    if (a.k2_cond && !(st->last_restarted || st->dual_pending || st->dual_only)) return;
     wz = st->dual_pending != 0;
     wg = st->dual_only == 0;
     t = st->t + 1;

@@ -141,7 +141,11 @@ def test_batched_default_options_converge_like_single():
     from paper_2502_09502_b200 import solve_relaxation_batched
     inst, nodes = _c4_instance(0.1, 8)
     L = lipschitz_constant(inst)
-    opts = FistaOptions(max_iterations=3000, lipschitz=L, gap_tolerance=1e-4)
+    # the objective is ~5e4 here and the batched contractions are fp32-class
+    # (1e-7 relative ~ 5e-3 absolute): a gap tolerance below that floor makes
+    # the stopping iteration a matter of round-off (tools/flaky_batch.py: 1760
+    # vs 120 iterations at 1e-4, equal counts from 1e-3 up)
+    opts = FistaOptions(max_iterations=3000, lipschitz=L, gap_tolerance=5e-3)
     reps = solve_relaxation_batched(inst, nodes, opts=opts)
     for i, nd in enumerate(nodes):
         ref = solve_relaxation(inst, nd, opts=opts)
@@ -150,7 +154,7 @@ def test_batched_default_options_converge_like_single():
         # move one, so the stopping check may land a few cadence points apart
         assert abs(reps[i].iterations - ref.iterations) <= max(40, ref.iterations // 2)
         assert _rel(reps[i].primal_value, ref.primal_value) < 1e-5
-        assert reps[i].gap <= 1e-4 or reps[i].termination.value != "converged"
+        assert reps[i].gap <= 5e-3 or reps[i].termination.value != "converged"
 
 
 def test_batched_infeasible_node_raises():

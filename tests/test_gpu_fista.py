@@ -312,7 +312,9 @@ def test_single_pass_engine_matches_two_pass(engine, case):
     (1001, 3001, "fp64", "squared_error"),    # odd n: y / u_{t-1} loaded per row; odd p: padded columns
     (7, 5, "fp64", "squared_error"),          # one partial tile, one CTA per cluster
     (301, 20000, "fp64", "squared_error"),    # 16-CTA (non-portable) clusters, 3 vectors per thread
-    (999, 5003, "fp32", "logistic"),          # fp32 X, odd n, partial last tile
+    (999, 5003, "fp32", "logistic"),          # fp32 X, odd n, partial last tile; SPEC kernel, no cluster
+    (640, 11000, "fp32", "logistic"),         # SPEC kernel (one vector + conditional K2), clusters of 2
+    (777, 9001, "fp32", "squared_error"),     # LIN kernel on fp32 X, clusters of 2, 5 vectors per thread
     (2048, 9000, "fp64", "logistic"),         # 8-CTA clusters, last CTA's slice partly past p
     (1500, 4100, "fp64", "squared_hinge"),    # the third solver-grade loss through the gather warps
 ])
@@ -342,7 +344,8 @@ def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
             trace_hook=rec.append)), rec)
     (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
     assert b.stats["single_pass"] and not a.stats["single_pass"]
-    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 2, 9000: 8, 4100: 4}[p]
+    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 1, 11000: 2, 9001: 2,
+                                          9000: 8, 4100: 4}[p]
     assert a.iterations == b.iterations == 30
     assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
     assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9, abs=1e-12)
@@ -379,6 +382,73 @@ def test_k3_variants_agree(engine, monkeypatch):
         assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9)
         for x, y_ in zip(ra, rb):
             assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
+        np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["C3", "C5", "C2", "hinge", "time_limit"])
+def test_single_pass_kernel_variants_agree(engine, monkeypatch, case):
+    """The one-vector single-pass kernels -- LIN (squared error: both momentum
+    candidates and X^T zeta from A_t = X^T grad F(u_t) by linearity) and SPEC
+    (non-linear loss on fp32 X: the no-restart candidate, restarts and bound
+    passes through the conditional K2 launch) -- against the three-vector
+    kernel they replace (L0_FZ_LIN=0 / L0_FZ_SPEC=0) and the two-pass engine:
+    same iterations, restarts and termination, values to summation order."""
+    kw = {}
+    if case in ("C3", "time_limit"):
+        cd = mydata.make_config("C3", scale=1 / 10)
+        X, curv, var = cd.X, 0.25, "L0_FZ_SPEC"
+    elif case == "hinge":
+        cd = mydata.make_config("C3", scale=1 / 12)
+        cd.loss = "squared_hinge"
+        X, curv, var = cd.X, 2.0, "L0_FZ_SPEC"
+    elif case == "C5":
+        cd = mydata.make_config("C5", scale=1 / 200)
+        X, curv, var = cd.X, 2.0, "L0_FZ_LIN"
+    else:
+        cd = mydata.make_config("C2", scale=1 / 8)
+        X, curv, var = cd.X, 2.0, "L0_FZ_LIN"
+    L = curv * 1.01 * float(np.linalg.norm(X.astype(np.float64), 2) ** 2)
+    # the small squared-error problems reach their round-off plateau (where
+    # restart decisions compare ulp-equal objectives) within ~100 iterations
+    iters = 150 if var == "L0_FZ_SPEC" else 60
+    if var == "L0_FZ_LIN":
+        L *= 0.55   # over-long steps: the momentum overshoots and the restart rule fires early
+    res = {}
+    for mode in ("two_pass", "0", "1"):
+        monkeypatch.setenv(var, "1" if mode == "two_pass" else mode)
+        # a fresh instance per variant: the plan is fixed when the device problem is created
+        inst = engine.ProblemInstance(X, cd.y, engine.LossKind(cd.loss), cd.k, cd.M, cd.lambda2,
+                                      dtype=cd.dtype)
+        rec = []
+        if case == "time_limit":
+            # the stop request between chunks re-runs the fused tail (KR and,
+            # for SPEC, the conditional transpose launch)
+            kw = dict(time_limit=0.0, chunk_iterations=3, bound_check_interval=1000)
+        rep = engine.solve_relaxation(inst, opts=engine.FistaOptions(
+            lipschitz=L, max_iterations=iters, gap_tolerance=1e-300,
+            engine_path="two_pass" if mode == "two_pass" else "single_pass", trace_hook=rec.append, **kw))
+        res[mode] = (rep, rec)
+        assert rep.stats["single_pass"] == (mode != "two_pass")
+    a, ra = res["two_pass"]
+    if case == "time_limit":
+        for mode in ("0", "1"):
+            b, _ = res[mode]
+            assert b.termination == engine.Termination.TIME_LIMIT
+            assert np.isfinite(b.dual_bound) and b.dual_bound <= b.primal_value + 1e-9 * abs(b.primal_value)
+        return
+    assert a.restarts > 0 or case == "hinge"
+    for mode in ("0", "1"):
+        b, rb = res[mode]
+        assert b.iterations == a.iterations == iters
+        assert b.restarts == a.restarts and b.termination == a.termination
+        assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
+        assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9)
+        assert len(rb) == len(ra)
+        for x, y_ in zip(ra, rb):
+            assert y_["primal"] == pytest.approx(x["primal"], rel=1e-12)
+            assert y_["dual"] == pytest.approx(x["dual"], rel=1e-9)
+            assert y_["restarted"] == x["restarted"]
         np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-10 * max(1.0, np.max(np.abs(a.beta))))
 
 
