@@ -804,9 +804,10 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
   const bool use_R = (mode != MODE_ITER) || st->last_restarted;
   double g = 0.0, gn = 0.0, v = 0.0;
   if (a.fz_one == 2) {
-    // SPEC: KF accumulated the no-restart candidate; restarts, bound checks
-    // and bound-only passes belong to the K2 launch that follows
-    if (mode == MODE_ITER && (st->last_restarted || st->dual_pending || st->dual_only)) return;
+    // SPEC: KF accumulated the no-restart candidate; the restart candidate,
+    // X^T zeta of bound checks and bound-only passes belong to the K2 launch
+    // that follows (the two halves of the slab epilogue are independent)
+    if (mode == MODE_ITER && (st->last_restarted || st->dual_only)) return;
     if (j < p)
       for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
     if (j < p) a.gv[j] = g;
