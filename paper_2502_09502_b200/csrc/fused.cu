@@ -300,7 +300,9 @@ constexpr int kFsGatherWarp = kFzFwdWarps;
 template <int G> constexpr int fs_prod_warp() { return kFzFwdWarps + G; }
 template <int G> constexpr int fs_acc_warp0() { return kFzFwdWarps + G + 1; }
 template <int G> constexpr int fs_block() { return (kFzFwdWarps + G + 1 + kFzTrWarps) * 32; }
-template <typename TX> constexpr int fs_gather() { return sizeof(TX) == 8 ? 4 : 2; }
+// (fp64 X in 1-row tiles: 3 gather warps -- half the rows per tile -- make a
+// 16-warp CTA, whose threads get 128 registers instead of 96)
+template <typename TX, int R = 2> constexpr int fs_gather() { return sizeof(TX) == 8 ? (R == 1 ? 3 : 4) : 2; }
 
 struct FsShared {
   uint64_t full[kFsMaxStages];        // stage landed (bulk-copy complete_tx)
@@ -338,9 +340,9 @@ __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~si
 // ~1 in 6 iterations on C3 against 3x fewer accumulators, clusters of 4
 // instead of 8 and a third of the gather's loss evaluations.
 template <typename TX, int R, int NV, bool F32F = false, int ONE = 0>
-__global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
+__global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
   constexpr bool LIN = ONE != 0;    // one accumulated vector (ONE = 1: squared error, 2: SPEC)
-  constexpr int G = fs_gather<TX>();
+  constexpr int G = fs_gather<TX, R>();
   constexpr int kFsProdWarp = fs_prod_warp<G>();
   constexpr int kFsAccWarp0 = fs_acc_warp0<G>();
   constexpr int kFsBlock = fs_block<G>();
@@ -563,6 +565,14 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       const int buf = k % S, q = k % NS;
       const uint32_t ph = (uint32_t)((k / S) & 1), qph = (uint32_t)((k / NS) & 1);
       const int rows = tile_rows(k);
+      // y / u_{t-1} that do not ride with the tile (odd n, 1-row tiles): the
+      // global loads go out before the waits
+      double y_pre = 0.0, up_pre = 0.0;
+      if (!side(k) && (lane / (32 / R)) < rows && (lane % (32 / R)) < 4) {
+        const int64_t row = tile_of(k) * R + lane / (32 / R);
+        y_pre = a.y[row];
+        if (mode == MODE_ITER) up_pre = uprev[row];
+      }
       mbar_wait_cluster(&sh.xb[q], qph, a.fz_sleep);
       mbar_wait(&sh.full[buf], ph, a.fz_sleep);            // y / u_{t-1} of the stage
       if (lane == 0) FZ_STAMP(a, k, 3);
@@ -603,13 +613,14 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX>()>(), 1) kf_fused_s(Eng
       if (f < 4 && r < rows) {
         const double u = us[0];
         const int64_t row = tile_of(k) * R + r;
+        (void)row;
         double yi, up;
         if (side(k)) {
           yi = sh.sy[buf][r];
           up = (mode == MODE_ITER) ? sh.su[buf][r] : u;
         } else {
-          yi = a.y[row];
-          up = (mode == MODE_ITER) ? uprev[row] : u;
+          yi = y_pre;
+          up = (mode == MODE_ITER) ? up_pre : u;
         }
         if (ONE == 2 && f < 3) {
           // SPEC: the no-restart candidate only (fista.py:161-162)
@@ -926,10 +937,18 @@ static KfFn kfs_pick_nv(int nv) {
       if constexpr (sizeof(TX) == 8 || ONE != 0) return kf_fused_s<TX, R, 4, F32F, ONE>;
       return nullptr;
     case 5:
-      if constexpr (sizeof(TX) == 4 && ONE != 0 && R == 2) return kf_fused_s<TX, R, 5, F32F, ONE>;
+      if constexpr ((sizeof(TX) == 4 && ONE != 0 && R == 2) || (sizeof(TX) == 8 && ONE == 1 && R == 1))
+        return kf_fused_s<TX, R, 5, F32F, ONE>;
       return nullptr;
     case 6:
-      if constexpr (sizeof(TX) == 4 && ONE != 0 && R == 2) return kf_fused_s<TX, R, 6, F32F, ONE>;
+      if constexpr ((sizeof(TX) == 4 && ONE != 0 && R == 2) || (sizeof(TX) == 8 && ONE == 1 && R == 1))
+        return kf_fused_s<TX, R, 6, F32F, ONE>;
+      return nullptr;
+    case 7:
+      if constexpr (sizeof(TX) == 8 && ONE == 1 && R == 1) return kf_fused_s<TX, R, 7, F32F, ONE>;
+      return nullptr;
+    case 8:
+      if constexpr (sizeof(TX) == 8 && ONE == 1 && R == 1) return kf_fused_s<TX, R, 8, F32F, ONE>;
       return nullptr;
     default: return nullptr;
   }
@@ -937,6 +956,10 @@ static KfFn kfs_pick_nv(int nv) {
 
 template <typename TX, bool F32F, int ONE>
 static KfFn kfs_pick_r(int rows, int nv) {
+  if (rows == 1) {
+    if constexpr (sizeof(TX) == 8 && ONE == 1) return nv > 4 ? kfs_pick_nv<TX, 1, F32F, ONE>(nv) : nullptr;
+    return nullptr;
+  }
   if (rows == 2) return kfs_pick_nv<TX, 2, F32F, ONE>(nv);
   if (rows == 4) {
     if constexpr (ONE != 2) return kfs_pick_nv<TX, 4, F32F, ONE>(nv);
@@ -974,7 +997,9 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3((unsigned)(a.fz_cs * a.fz_ncl));
-  cfg.blockDim = dim3(a.dtype == F64 ? fs_block<fs_gather<double>()>() : fs_block<fs_gather<float>()>());
+  cfg.blockDim = dim3(a.dtype == F64 ? (a.fz_rows == 1 ? fs_block<fs_gather<double, 1>()>()
+                                                       : fs_block<fs_gather<double>()>())
+                                     : fs_block<fs_gather<float>()>());
   cfg.dynamicSmemBytes = smem;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.fz_cs;
@@ -1003,10 +1028,16 @@ int fused_plan(EngineArgs& a, int sms) {
   const char* env = getenv("L0_FZ_CS");
   const int want_cs = env ? atoi(env) : 0;
   const char* renv = getenv("L0_FZ_R");
-  const int R = renv ? (atoi(renv) == 4 ? 4 : 2) : ((a.dtype == F64 || a.fz_one) ? 2 : 4);
+  const int R0 = renv ? (atoi(renv) == 4 ? 4 : 2) : ((a.dtype == F64 || a.fz_one) ? 2 : 4);
   // vectors per accumulate thread: the accumulator registers bound the column
-  // slice (LIN keeps one accumulator per column instead of three)
-  const int maxv = a.dtype == F64 ? 4 : (a.fz_one ? (R == 2 ? 6 : 4) : 3);
+  // slice (LIN keeps one accumulator per column instead of three); fp64 LIN
+  // goes on to 8 vectors (4096 columns) with 1-row tiles, which keeps the
+  // tile bytes and the ring depth of the 2-row x 2048-column plan in half
+  // the cluster size (L0_FZ_WIDE=0: off)
+  const bool wide64 = a.dtype == F64 && a.fz_one == 1 && !renv &&
+                      (!getenv("L0_FZ_WIDE") || atoi(getenv("L0_FZ_WIDE")));
+  const int maxv0 = a.dtype == F64 ? 4 : (a.fz_one ? (R0 == 2 ? 6 : 4) : 3);
+  const int maxv = wide64 ? 8 : maxv0;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1017,6 +1048,7 @@ int fused_plan(EngineArgs& a, int sms) {
     const int64_t W = ((need + unit - 1) / unit) * unit;
     const int nv = (int)(W / unit);
     if (nv > maxv) continue;
+    const int R = nv > maxv0 ? 1 : R0;
     // stages S and slots 2S: fixed + 2S*cs*4*R*8 (+ align) + S*R*W*es <= budget
     const size_t fixed = fs_align(sizeof(FsShared)) + 128;
     if (fixed >= budget) continue;

@@ -309,9 +309,12 @@ def test_single_pass_engine_matches_two_pass(engine, case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,p,dtype,loss", [
-    (1001, 3001, "fp64", "squared_error"),    # odd n: y / u_{t-1} loaded per row; odd p: padded columns
+    (1001, 3001, "fp64", "squared_error"),    # LIN, 1-row x 3072-column tiles (6 vectors per thread), no
+                                              # cluster; odd n: y / u_{t-1} loaded per row; odd p: padded columns
     (7, 5, "fp64", "squared_error"),          # one partial tile, one CTA per cluster
-    (301, 20000, "fp64", "squared_error"),    # 16-CTA (non-portable) clusters, 3 vectors per thread
+    (301, 20000, "fp64", "logistic"),         # 16-CTA (non-portable) clusters, 3 vectors per thread
+    (300, 20001, "fp64", "squared_error"),    # LIN, 1-row tiles in clusters of 8, 5 vectors per thread
+    (1000, 1500, "fp64", "squared_error"),    # LIN, 2-row tiles, no cluster
     (999, 5003, "fp32", "logistic"),          # fp32 X, odd n, partial last tile; SPEC kernel, no cluster
     (640, 11000, "fp32", "logistic"),         # SPEC kernel (one vector + conditional K2), clusters of 2
     (777, 9001, "fp32", "squared_error"),     # LIN kernel on fp32 X, clusters of 2, 5 vectors per thread
@@ -344,8 +347,8 @@ def test_single_pass_edge_shapes(engine, n, p, dtype, loss):
             trace_hook=rec.append)), rec)
     (a, ra), (b, rb) = res["two_pass"], res["single_pass"]
     assert b.stats["single_pass"] and not a.stats["single_pass"]
-    assert b.stats["cluster_size"] == {3001: 2, 5: 1, 20000: 16, 5003: 1, 11000: 2, 9001: 2,
-                                          9000: 8, 4100: 4}[p]
+    assert b.stats["cluster_size"] == {3001: 1, 5: 1, 20000: 16, 20001: 8, 1500: 1, 5003: 1,
+                                          11000: 2, 9001: 2, 9000: 8, 4100: 4}[p]
     assert a.iterations == b.iterations == 30
     assert b.primal_value == pytest.approx(a.primal_value, rel=1e-12)
     assert b.dual_bound == pytest.approx(a.dual_bound, rel=1e-9, abs=1e-12)
