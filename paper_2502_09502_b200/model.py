@@ -141,7 +141,7 @@ class DeviceProblem:
             es = Xt.element_size()
             Xd = (torch.empty if ld == p else torch.zeros)((n, ld), dtype=tdt, device=dev)
             native.check(lib.l0_upload_rows(Xd.data_ptr(), ld * es, Xt.data_ptr(), p * es, p * es,
-                                            n, min(16, os.cpu_count() or 8),
+                                            n, min(8, os.cpu_count() or 8),   # tools/upload_bw.py: 8 > 12 > 16
                                             _device.stream_handle()))
         elif (Xt.device.type == "cuda" and Xt.dtype == tdt and Xt.dim() == 2 and Xt.stride(1) == 1
               and Xt.stride(0) >= p and Xt.stride(0) % align == 0 and n > 0

@@ -40,6 +40,7 @@ for _ in range(4):
     best = min(best, time.perf_counter() - t0)
 print(f"pinned torch copy: {Xp.numel() * 8 / best / 1e9:.1f} GB/s", flush=True)
 del Xp, Xd
-for mb, th in [(32, 16), (64, 16), (16, 16), (32, 8), (64, 12), (128, 16), (32, 24)]:
-    env = dict(os.environ, L0_UPLOAD_MB=str(mb), L0_UPLOAD_THREADS=str(th))
-    subprocess.run([sys.executable, __file__, "child"], env=env)
+for mb in (1, 2, 4, 8, 16):
+    for th in (4, 8, 12, 16):
+        env = dict(os.environ, L0_UPLOAD_MB=str(mb), L0_UPLOAD_THREADS=str(th))
+        subprocess.run([sys.executable, __file__, "child"], env=env)
