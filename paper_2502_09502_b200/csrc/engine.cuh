@@ -84,6 +84,7 @@ struct EngineArgs {
   int fz_one;        // single-pass kernel with ONE accumulated vector (fused.cu): 1 squared error
                      // (LIN: candidates by linearity), 2 SPEC (no-restart candidate; restarts
                      // and bound checks through the K2 launch that follows), 0 three vectors
+  int pdl;           // single-pass chain launched as programmatic dependents (engine.cuh pdl_*)
   int k2_cond;       // K2 launched behind the SPEC kernel: runs only for restarts / bound passes
   int f32_forward;   // fp32 X: forward products in fp32 (FistaOptions.fp32_forward; fused.cu)
   uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits
@@ -158,6 +159,25 @@ __device__ __forceinline__ void record_prox(int* rec, int cap, int w, const int*
   const int64_t m = len < w ? len : w;
   for (int64_t i = threadIdx.x; i < w; i += blockDim.x)
     r[kProxRecHead + i] = i < m ? perm[i] : -1;
+}
+
+// Programmatic dependent launch (single-pass chain K3 -> KF -> KR -> K3 ...):
+// a kernel launched with the attribute may become resident, and run whatever
+// does not depend on its predecessor, once every CTA of the predecessor has
+// executed pdl_launch(); pdl_wait() returns when the predecessor grid has
+// completed and its writes are visible.  Every kernel of the chain waits at
+// its top on every path, so completion stays transitive.  Both are no-ops in
+// a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline void pdl_attr(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, bool on) {
+  cfg.attrs = at;
+  cfg.numAttrs = 0;
+  if (on) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
+  }
 }
 
 // Launch helpers (defined in gemv.cu / prox.cu)

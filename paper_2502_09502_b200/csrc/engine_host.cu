@@ -668,6 +668,17 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   if (want_fused != a.fused) destroy_graphs(*P);
   a.fused = want_fused;
   a.f32_forward = (o->fp32_forward && a.dtype == F32 && a.fused) ? 1 : 0;
+  // L0_PDL=1: the single-pass chain as programmatic dependent launches (KF's
+  // first X tiles load while the prox runs; KR / K3 resident before their
+  // predecessor ends); not with per-kernel events or NCCL kernels between the
+  // launches.  Off by default: measured 1.3% slower on C2 (2814 vs 2850 it/s
+  // at K = 200, profiles/r2_ab_pdl.txt), equal on C3 / C5
+  {
+    const int pdl = (a.fused && !a.multi && !o->profile && getenv("L0_PDL") &&
+                     atoi(getenv("L0_PDL"))) ? 1 : 0;
+    if (pdl != a.pdl) destroy_graphs(*P);
+    a.pdl = pdl;
+  }
   // K3 variant: the windowed top-of-order sort, switched to the full key sort
   // for the rest of the solve once most iterations of a chunk needed window
   // extensions (a PAVA pool spanning much of p, as on C3: K3 0.34 -> 0.19 ms);

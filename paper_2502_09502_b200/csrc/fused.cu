@@ -362,16 +362,11 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   const size_t part_bytes = fs_align((size_t)NS * cs * kFzFwdWarps * R * 8);
   TX* tiles = reinterpret_cast<TX*>(reinterpret_cast<unsigned char*>(part) + part_bytes);
 
+  // Everything down to pdl_wait() is independent of the kernels before this
+  // one (geometry, barrier init, the first S tiles of X): launched as a
+  // programmatic dependent of K3 it runs while the prox is still working.
+  pdl_launch();   // KR may become resident (it waits for this grid at its top)
   State* st = a.st;
-  int64_t t = 0;
-  double cN = 0.25;
-  bool want_z = false;
-  if (mode == MODE_ITER) {
-    if (st->done || st->dual_only) return;
-    t = st->t + 1;
-    cN = momentum(st->phi + 1);
-    want_z = is_check(t, a.prm->bci) || !isfinite(st->best_dual);
-  }
   const double cR = 0.25;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = cs > 1 ? cluster_rank() : 0;
@@ -381,8 +376,6 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   const int64_t c0 = (int64_t)crank * W;
   const int wvalid = (int)max((int64_t)0, min((int64_t)W, ld - c0));
   const uint32_t row_bytes = (uint32_t)wvalid * (uint32_t)sizeof(TX);
-  const double* bsrc = (mode == MODE_ITER) ? a.beta + ring(t) * a.pv : a.beta;
-  const double* uprev = a.u + ((mode == MODE_ITER) ? ring(t - 1) * n : 0);
 
   const int ntiles = (int)a.fz_tiles;
   const int mytiles = cid < ntiles ? (ntiles - cid + ncl - 1) / ncl : 0;
@@ -414,25 +407,59 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   __syncthreads();
   if (tid == 0)
     for (int k = 0; k < NS && k < mytiles; ++k) mbar_arrive_expect(&sh.xb[k], slot_bytes(k));
-  auto issue = [&](int k, int b) {
+  // a stage's transaction count covers the X rows and the side copies; the X
+  // rows can be issued before the state of the solve is known
+  auto side_bytes = [&](int k) -> uint32_t {
+    return side(k) ? (uint32_t)tile_rows(k) * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
+  };
+  auto issue_x = [&](int k, int b) {
     const int64_t tile = tile_of(k);
     const int rows = tile_rows(k);
     TX* dst = tiles + (int64_t)b * R * W;
-    const uint32_t sb = side(k) ? (uint32_t)rows * 8u * (mode == MODE_ITER ? 2u : 1u) : 0u;
-    mbar_arrive_expect(&sh.full[b], row_bytes * rows + sb);
+    mbar_arrive_expect(&sh.full[b], row_bytes * rows + side_bytes(k));
     if (row_bytes > 0)
       for (int r = 0; r < rows; ++r)
         bulk_g2s(dst + (int64_t)r * W, static_cast<const TX*>(a.X) + (tile * R + r) * ld + c0,
                  row_bytes, &sh.full[b]);
-    if (sb) {
-      bulk_g2s(&sh.sy[b][0], a.y + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
-      if (mode == MODE_ITER) bulk_g2s(&sh.su[b][0], uprev + tile * R, (uint32_t)rows * 8u, &sh.full[b]);
-    }
+  };
+  auto issue_side = [&](int k, int b, const double* up) {
+    if (side_bytes(k) == 0) return;
+    const int64_t tile = tile_of(k);
+    const uint32_t rb = (uint32_t)tile_rows(k) * 8u;
+    bulk_g2s(&sh.sy[b][0], a.y + tile * R, rb, &sh.full[b]);
+    if (mode == MODE_ITER) bulk_g2s(&sh.su[b][0], up + tile * R, rb, &sh.full[b]);
   };
   // the first S tiles only need this CTA's barriers: in flight across the
-  // cluster barrier (which orders the peers' barrier init before any st.async)
+  // wait for the previous kernel and the cluster barrier (which orders the
+  // peers' barrier init before any st.async)
   if (warp == kFsProdWarp && lane == 0)
-    for (int k = 0; k < S && k < mytiles; ++k) issue(k, k);
+    for (int k = 0; k < S && k < mytiles; ++k) issue_x(k, k);
+
+  pdl_wait();     // K3's beta_t, the control state and u_{t-1} are complete from here on
+  int64_t t = 0;
+  double cN = 0.25;
+  bool want_z = false;
+  if (mode == MODE_ITER) {
+    if (st->done || st->dual_only) {
+      // nothing to do: complete the stages in flight before the CTA exits
+      if (warp == kFsProdWarp && lane == 0) {
+        for (int k = 0; k < S && k < mytiles; ++k) issue_side(k, k, a.u);
+        for (int k = 0; k < S && k < mytiles; ++k) mbar_wait(&sh.full[k], 0u, a.fz_sleep);
+      }
+      return;
+    }
+    t = st->t + 1;
+    cN = momentum(st->phi + 1);
+    want_z = is_check(t, a.prm->bci) || !isfinite(st->best_dual);
+  }
+  const double* bsrc = (mode == MODE_ITER) ? a.beta + ring(t) * a.pv : a.beta;
+  const double* uprev = a.u + ((mode == MODE_ITER) ? ring(t - 1) * n : 0);
+  auto issue = [&](int k, int b) {
+    issue_x(k, b);
+    issue_side(k, b, uprev);
+  };
+  if (warp == kFsProdWarp && lane == 0)
+    for (int k = 0; k < S && k < mytiles; ++k) issue_side(k, k, uprev);
   if (cs > 1) cluster_barrier();
   else __syncthreads();
 
@@ -802,6 +829,8 @@ __device__ __forceinline__ double lin_candidate(const EngineArgs& a, int mode, i
 // the restart decision, slab epilogue.  One CTA per 256-column slab.
 __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int epilogue) {
   __shared__ EpiSmem sm;
+  pdl_wait();     // KF (programmatic dependent launch: this grid may be resident before KF ends)
+  pdl_launch();   // ... and K3 behind this one
   const State* st = a.st;
   if (st->done) return;
   const int64_t pv = a.pv, p = a.p;
@@ -985,7 +1014,7 @@ static KfFn kf_pick(const EngineArgs& a) {
 }
 
 static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at,
-                                KfFn* fn) {
+                                KfFn* fn, bool pdl = false) {
   *fn = kf_pick(a);
   if (!*fn) return cudaErrorInvalidValue;
   const size_t smem = fused_smem(a);
@@ -1007,6 +1036,11 @@ static cudaError_t fused_config(const EngineArgs& a, cudaLaunchConfig_t& cfg, cu
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (pdl) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   return cudaSuccess;
 }
 
@@ -1073,7 +1107,7 @@ int fused_plan(EngineArgs& a, int sms) {
     a.fz_ncl = 1;   // grid of one cluster for the occupancy query
     int ncl = 0;
     cudaLaunchConfig_t cfg;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     KfFn fn = nullptr;
     cudaError_t e = fused_config(a, cfg, at, &fn);
     if (e != cudaSuccess) {
@@ -1097,9 +1131,9 @@ int fused_plan(EngineArgs& a, int sms) {
 
 cudaError_t launch_fused(const EngineArgs& a, int mode, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   KfFn fn = nullptr;
-  cudaError_t e = fused_config(a, cfg, at, &fn);
+  cudaError_t e = fused_config(a, cfg, at, &fn, a.pdl && mode == MODE_ITER);
   if (e != cudaSuccess) return e;
   cfg.stream = s;
   e = cudaLaunchKernelEx(&cfg, fn, a, mode);
@@ -1108,11 +1142,14 @@ cudaError_t launch_fused(const EngineArgs& a, int mode, cudaStream_t s) {
 }
 
 cudaError_t launch_fused_reduce(const EngineArgs& a, int mode, cudaStream_t s) {
-  if (a.multi) {
-    kr_reduce<<<a.k2_slabs, kK2Slab, 0, s>>>(a, mode, 0);
-  } else {
-    kr_reduce<<<a.k2_slabs, kK2Slab, 0, s>>>(a, mode, 1);
-  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3((unsigned)a.k2_slabs);
+  cfg.blockDim = dim3(kK2Slab);
+  cfg.stream = s;
+  pdl_attr(cfg, at, a.pdl && mode == MODE_ITER);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kr_reduce, a, mode, a.multi ? 0 : 1);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -713,6 +713,8 @@ __global__ void __launch_bounds__(kWinThreads, 1) k3_prox_window(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ProxSmem& ps = *reinterpret_cast<ProxSmem*>(smem_raw);
   WinSmem& sm = *reinterpret_cast<WinSmem*>(smem_raw + ((sizeof(ProxSmem) + 255) & ~size_t(255)));
+  pdl_wait();     // KR (or the SPEC kernel's K2) of the previous iteration
+  pdl_launch();   // KF may become resident and load its first X tiles while the prox runs
   prox_window_body(a, ps, sm);
 }
 
@@ -725,7 +727,15 @@ cudaError_t launch_prox_window(const EngineArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k3_prox_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  k3_prox_window<<<1, kWinThreads, smem, s>>>(a);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kWinThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  pdl_attr(cfg, at, a.pdl != 0);
+  e = cudaLaunchKernelEx(&cfg, k3_prox_window, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -21,7 +21,8 @@ for m in modes:
     inst = eng.ProblemInstance(cd.X, cd.y, eng.LossKind(cd.loss), cd.k, cd.M, cd.lambda2, dtype=cd.dtype)
     f32 = os.environ.get("FP32_FORWARD") == "1"
     o = lambda k: eng.FistaOptions(lipschitz=L, max_iterations=k, stop_on_gap=False, gap_tolerance=1e-300,
-                                   engine_path="single_pass", profile=True, fp32_forward=f32)
+                                   engine_path="single_pass", profile=os.environ.get("PROFILE", "1") == "1",
+                                   fp32_forward=f32)
     eng.solve_relaxation(inst, opts=o(3))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,11 +31,11 @@ for m in modes:
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     st = r.stats
-    kf = st['k2_ms'] / max(1, st['k2_count'])
+    kf = st.get('k2_ms', 0.0) / max(1, st.get('k2_count', 0)) or 1e-9
     xb = cd.n * cd.p * cd.X.itemsize
     same = "" if ref is None else (f" bitwise={np.array_equal(ref.beta, r.beta) and ref.primal_value == r.primal_value and ref.dual_bound == r.dual_bound}")
     print(f"{name} widen={m}: {iters/(ms/1e3):.1f} it/s ({ms/iters:.3f} ms/it) kf {kf:.4f} ms "
-          f"({xb/kf/1e6:.0f} GB/s) k3 {st['k3_ms']/max(1,st['k3_count']):.4f} obj {r.primal_value:.15g}{same}",
+          f"({xb/kf/1e6:.0f} GB/s) k3 {st.get('k3_ms', 0.0)/max(1,st.get('k3_count', 0)):.4f} obj {r.primal_value:.15g}{same}",
           flush=True)
     ref = ref or r
     del inst
