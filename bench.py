@@ -524,9 +524,13 @@ def run_config(name, iters):
             # bound-check iterations add one K2 transpose pass behind KR
             kern["kr_reduce_plus_conditional_k2"] = kern.pop("kr_reduce")
             kern["kr_reduce_plus_conditional_k2"]["note"] = (
-                "average over all iterations of KR plus the K2 pass that runs on restart / "
-                "bound-check iterations only (one extra read of X on those)")
-            kern["kf_fused_s"]["variant"] = "SPEC (one accumulated vector)"
+                "average over all iterations of KR plus the K2 pass that runs on restart "
+                "iterations only (one extra read of X on those)")
+            kern["kf_fused_s"]["variant"] = (
+                "SPEC: the no-restart candidate (one accumulated vector), plus X^T zeta in a "
+                "two-vector kernel on bound-check iterations; both kernels are launched every "
+                "iteration inside the timed event pair and one returns at entry, so launch_ms "
+                "averages the two")
         elif cd.loss == "squared_error":
             kern["kf_fused_s"]["variant"] = "LIN (one accumulated vector, candidates by linearity)"
     else:

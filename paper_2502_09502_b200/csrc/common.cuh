@@ -308,6 +308,8 @@ struct State {
   int last_restarted;
   int topk_fallbacks;     // diagnostics: g top-k window verification misses
   int win_ext;            // diagnostics: K3 iterations whose pool reached past the candidate window
+  int kf_token;           // SPEC: 1 until one of the two single-pass kernels has run this iteration
+                          // (the second one would otherwise see the advanced t); KR re-arms it
   double obj;             // composite objective at beta_t
   double g_next;          // g(beta_next) from the prox kernel
   double best_dual;

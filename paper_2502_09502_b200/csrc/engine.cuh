@@ -85,7 +85,9 @@ struct EngineArgs {
                      // (LIN: candidates by linearity), 2 SPEC (no-restart candidate; restarts
                      // and bound checks through the K2 launch that follows), 0 three vectors
   int pdl;           // single-pass chain launched as programmatic dependents (engine.cuh pdl_*)
+  int fz_spec2;      // SPEC: bound-check iterations run the two-vector kernel (ONE = 3) instead of K2
   int k2_cond;       // K2 launched behind the SPEC kernel: runs only for restarts / bound passes
+                     // (2: X^T zeta of bound checks comes from the ONE = 3 kernel)
   int f32_forward;   // fp32 X: forward products in fp32 (FistaOptions.fp32_forward; fused.cu)
   uint32_t fz_sleep;  // suspend-time hint (ns) of the single-pass kernel's mbarrier waits
   int64_t fz_w;      // columns per CTA (multiple of 256 * vector width)

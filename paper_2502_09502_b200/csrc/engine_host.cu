@@ -131,6 +131,7 @@ static void select_plan(Problem& P, int which) {
   const Problem::FzPlan& pl = P.plan[which];
   P.plan_sel = which;
   a.fz_one = pl.one;
+  a.fz_spec2 = (pl.one == 2 && (!getenv("L0_FZ_SPEC2") || atoi(getenv("L0_FZ_SPEC2")))) ? 1 : 0;
   a.fz_cs = pl.cs; a.fz_ncl = pl.ncl; a.fz_nv = pl.nv; a.fz_rows = pl.rows;
   a.fz_stages = pl.stages; a.fz_slots = pl.slots; a.fz_widen = pl.widen;
   a.fz_sleep = pl.sleep; a.fz_w = pl.w; a.fz_tiles = pl.tiles;
@@ -273,7 +274,7 @@ static int fused_tail(Problem& P, int mode, cudaStream_t s) {
     // SPEC: restart iterations and bound passes take the two-pass engine's
     // transpose kernel (it exits at entry on every other iteration)
     EngineArgs a2 = a;
-    a2.k2_cond = 1;
+    a2.k2_cond = a.fz_spec2 ? 2 : 1;
     L0_CUDA_TRY(launch_k2(a2, MODE_ITER, s));
   }
   return ST_OK;
@@ -289,6 +290,11 @@ static int launch_iteration(Problem& P, cudaStream_t s, cudaEvent_t* ev) {
     if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
     if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
     L0_CUDA_TRY(launch_fused(a, MODE_ITER, s));
+    if (a.fz_one == 2 && a.fz_spec2) {   // SPEC: the bound-check iterations' two-vector kernel
+      EngineArgs a3 = a;
+      a3.fz_one = 3;
+      L0_CUDA_TRY(launch_fused(a3, MODE_ITER, s));
+    }
     if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if (ev) L0_CUDA_TRY(cudaEventRecordWithFlags(ev[4], s, cudaEventRecordExternal));
     int rc = fused_tail(P, MODE_ITER, s);

@@ -179,7 +179,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // fz_part, per-cluster loss / flags / F* sums to fz_cpart, and in the last CTA
 // of the grid the fixed-order reduction over clusters and the objective /
 // restart logic.  Transpose thread lt owns columns c0 + v*kFzTr*VE + lt*VE + e.
-template <int NA, int VE, bool LIN>
+template <int NA, int VE, bool HASN, bool HASZ>
 __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t t, bool want_z, int cid,
                                           uint32_t crank, int64_t c0, bool is_tr, int lt,
                                           const double* accR, const double* accN, const double* accZ,
@@ -198,8 +198,8 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
         const int64_t col = c0 + (int64_t)v * kFzTr * VE + lt * VE + e;
         if (col < pv) {
           a.fz_part[(0 * (int64_t)ncl + cid) * pv + col] = accR[v * VE + e];
-          if constexpr (!LIN) {
-            a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
+          if constexpr (HASN) a.fz_part[(1 * (int64_t)ncl + cid) * pv + col] = accN[v * VE + e];
+          if constexpr (HASZ) {
             if (want_z) a.fz_part[(2 * (int64_t)ncl + cid) * pv + col] = accZ[v * VE + e];
           }
         }
@@ -231,6 +231,7 @@ __device__ __forceinline__ void kf_finish(const EngineArgs& a, int mode, int64_t
   // ---- last CTA: loss over clusters (fixed order), objective / restart ---------
   if (tid == 0) {
     *cnt_fused(a) = 0u;
+    st->kf_token = 0;
     double tot = 0.0, fs0 = 0.0, fs1 = 0.0, fs2 = 0.0;
     int flags = 0;
     for (int c = 0; c < ncl; ++c) {
@@ -341,7 +342,13 @@ __host__ __device__ constexpr size_t fs_align(size_t b) { return (b + 127) & ~si
 // instead of 8 and a third of the gather's loss evaluations.
 template <typename TX, int R, int NV, bool F32F = false, int ONE = 0>
 __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(EngineArgs a, int mode) {
-  constexpr bool LIN = ONE != 0;    // one accumulated vector (ONE = 1: squared error, 2: SPEC)
+  // ONE = 3 is SPEC's bound-check variant: the no-restart candidate AND X^T
+  // zeta_t (two vectors).  Both SPEC kernels are launched every iteration;
+  // ONE = 2 returns at entry on bound-check iterations, ONE = 3 on all others
+  // (EngineArgs::fz_spec2), so the conditional K2 pass is left with restarts.
+  constexpr bool LIN = ONE == 1 || ONE == 2;   // one accumulated vector
+  constexpr bool HASN = ONE == 0;              // accN: the second momentum candidate
+  constexpr bool HASZ = ONE == 0 || ONE == 3;  // accZ: X^T zeta on bound checks
   constexpr int G = fs_gather<TX, R>();
   constexpr int kFsProdWarp = fs_prod_warp<G>();
   constexpr int kFsAccWarp0 = fs_acc_warp0<G>();
@@ -367,6 +374,15 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   // programmatic dependent of K3 it runs while the prox is still working.
   pdl_launch();   // KR may become resident (it waits for this grid at its top)
   State* st = a.st;
+  // which of the two SPEC kernels owns this iteration (bound check or not)
+  auto not_mine = [&]() -> bool {
+    if (ONE != 2 && ONE != 3) return false;
+    if (ONE == 2 && !a.fz_spec2) return false;
+    if (st->kf_token == 0) return true;   // the other kernel ran this iteration (t has advanced)
+    const bool z = is_check(st->t + 1, a.prm->bci) || !isfinite(st->best_dual);
+    return ONE == 2 ? z : !z;
+  };
+  if (!a.pdl && mode == MODE_ITER && (st->done || st->dual_only || not_mine())) return;
   const double cR = 0.25;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = cs > 1 ? cluster_rank() : 0;
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   double cN = 0.25;
   bool want_z = false;
   if (mode == MODE_ITER) {
-    if (st->done || st->dual_only) {
+    if (st->done || st->dual_only || not_mine()) {
       // nothing to do: complete the stages in flight before the CTA exits
       if (warp == kFsProdWarp && lane == 0) {
         for (int k = 0; k < S && k < mytiles; ++k) issue_side(k, k, a.u);
@@ -463,8 +479,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
   if (cs > 1) cluster_barrier();
   else __syncthreads();
 
-  constexpr int NB = LIN ? 1 : NV * VE;           // candidate N / zeta accumulators (unused: LIN)
-  double accR[NV * VE], accN[NB], accZ[NB];
+  constexpr int NBN = HASN ? NV * VE : 1, NBZ = HASZ ? NV * VE : 1;
+  double accR[NV * VE], accN[NBN], accZ[NBZ];
   double loss_acc = 0.0, f_acc[3] = {0.0, 0.0, 0.0};
   int bad = 0, gbad_R = 0, gbad_N = 0;
 
@@ -649,14 +665,18 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
           yi = y_pre;
           up = (mode == MODE_ITER) ? up_pre : u;
         }
-        if (ONE == 2 && f < 3) {
-          // SPEC: the no-restart candidate only (fista.py:161-162)
+        if ((ONE == 2 || ONE == 3) && f < 3) {
+          // SPEC: the no-restart candidate (fista.py:161-162); ONE = 3 also zeta_t (fista.py:152)
           if (f == 0) {
             const double arg = dadd(u, dmul(cN, dsub(u, up)));
             if (!isfinite(arg)) gbad_N = 1;
             sh.rr[buf][0][r] = F32F ? loss_grad_f32m(a.loss, arg, yi) : loss_grad(a.loss, arg, yi);
+          } else if (ONE == 3 && f == 2) {
+            const double g = F32F ? loss_grad_f32m(a.loss, u, yi) : loss_grad(a.loss, u, yi);
+            sh.rr[buf][2][r] = -g;
+            if (crank == 0 && want_z) conj_accumulate(a.loss, -g, yi, f_acc);
           }
-        } else if (LIN && f < 3) {
+        } else if (ONE == 1 && f < 3) {
           // f = 0: grad F(u_t) (= -zeta_t); f = 1, 2: X gamma of the two
           // momenta must be finite (loss_gradient raises otherwise, model.py:215)
           if (f == 0) {
@@ -687,7 +707,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
           if (!isfinite(u)) bad = 1;
           loss_acc += F32F ? loss_term_f32m(a.loss, u, yi) : loss_term(a.loss, u, yi);
         }
-      } else if (f < (LIN ? 1 : 3)) {
+      } else if (f < (LIN ? 1 : 3)) {   // rows past n of a partial tile
         sh.rr[buf][f][r] = 0.0;
       }
       __syncwarp();
@@ -712,7 +732,9 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
 #pragma unroll
     for (int i = 0; i < NV * VE; ++i) accR[i] = 0.0;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) { accN[i] = 0.0; accZ[i] = 0.0; }
+    for (int i = 0; i < NBN; ++i) accN[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NBZ; ++i) accZ[i] = 0.0;
     int buf = 0;
     uint32_t ph = 0;
     for (int k = 0; k < mytiles; ++k) {
@@ -728,9 +750,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           aint = aint && isfinite(sh.rr[buf][0][r] * kRebias);
-          if constexpr (!LIN)
-            aint = aint && isfinite(sh.rr[buf][1][r] * kRebias) &&
-                   (!want_z || isfinite(sh.rr[buf][2][r] * kRebias));
+          if constexpr (HASN) aint = aint && isfinite(sh.rr[buf][1][r] * kRebias);
+          if constexpr (HASZ) aint = aint && (!want_z || isfinite(sh.rr[buf][2][r] * kRebias));
         }
       }
       auto acc_full = [&](auto INT) {
@@ -750,8 +771,9 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
           for (int h = 0; h < RP; ++h) {
             const int r = r0 + h;
             const double rR = sh.rr[buf][0][r] * sc;
-            const double rN = LIN ? 0.0 : sh.rr[buf][1][r] * sc;
-            const double rZ = (!LIN && want_z) ? sh.rr[buf][2][r] * sc : 0.0;
+            const double rN = HASN ? sh.rr[buf][1][r] * sc : 0.0;
+            const double rZ = (HASZ && want_z) ? sh.rr[buf][2][r] * sc : 0.0;
+            (void)rN; (void)rZ;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               double x[VE];
@@ -760,9 +782,9 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
 #pragma unroll
               for (int e = 0; e < VE; ++e) {
                 accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-                if constexpr (!LIN) accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+                if constexpr (HASN) accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
               }
-              if constexpr (!LIN) {
+              if constexpr (HASZ) {
                 if (want_z) {
 #pragma unroll
                   for (int e = 0; e < VE; ++e) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
@@ -780,7 +802,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
         // the last, partial tile of the grid: rows past n hold stale data
         for (int r = 0; r < rows; ++r) {
           const double rR = sh.rr[buf][0][r];
-          const double rN = LIN ? 0.0 : sh.rr[buf][1][r], rZ = LIN ? 0.0 : sh.rr[buf][2][r];
+          const double rN = HASN ? sh.rr[buf][1][r] : 0.0, rZ = HASZ ? sh.rr[buf][2][r] : 0.0;
+          (void)rN; (void)rZ;
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             double x[VE];
@@ -788,8 +811,8 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
 #pragma unroll
             for (int e = 0; e < VE; ++e) {
               accR[v * VE + e] = fma(x[e], rR, accR[v * VE + e]);
-              if constexpr (!LIN) {
-                accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+              if constexpr (HASN) accN[v * VE + e] = fma(x[e], rN, accN[v * VE + e]);
+              if constexpr (HASZ) {
                 if (want_z) accZ[v * VE + e] = fma(x[e], rZ, accZ[v * VE + e]);
               }
             }
@@ -803,7 +826,7 @@ __global__ void __launch_bounds__(fs_block<fs_gather<TX, R>()>(), 1) kf_fused_s(
     }
   }
   __syncthreads();
-  kf_finish<NV * VE, VE, LIN>(a, mode, t, want_z, cid, crank, c0, warp >= kFsAccWarp0,
+  kf_finish<NV * VE, VE, HASN, HASZ>(a, mode, t, want_z, cid, crank, c0, warp >= kFsAccWarp0,
                          tid - kFsAccWarp0 * 32, accR, accN, accZ, loss_acc, f_acc, bad, gbad_R, gbad_N,
                          &sh.bad, sh.red);
 }
@@ -832,6 +855,7 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
   pdl_wait();     // KF (programmatic dependent launch: this grid may be resident before KF ends)
   pdl_launch();   // ... and K3 behind this one
   const State* st = a.st;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st->kf_token = 1;   // next iteration's single pass
   if (st->done) return;
   const int64_t pv = a.pv, p = a.p;
   const bool wg = st->dual_only == 0;
@@ -844,20 +868,32 @@ __global__ void __launch_bounds__(kK2Slab) kr_reduce(EngineArgs a, int mode, int
   const bool use_R = (mode != MODE_ITER) || st->last_restarted;
   double g = 0.0, gn = 0.0, v = 0.0;
   if (a.fz_one == 2) {
-    // SPEC: KF accumulated the no-restart candidate; the restart candidate,
-    // X^T zeta of bound checks and bound-only passes belong to the K2 launch
-    // that follows (the two halves of the slab epilogue are independent)
-    if (mode == MODE_ITER && (st->last_restarted || st->dual_only)) return;
-    if (j < p)
-      for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
-    if (j < p) a.gv[j] = g;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && mode == MODE_ITER && ((int)a.gv[2 * pv + 6] & 4)) {
+    // SPEC: KF accumulated the no-restart candidate and, on bound-check
+    // iterations (fz_spec2: the ONE = 3 kernel), X^T zeta_t; the restart
+    // candidate, bound-only passes and (without fz_spec2) X^T zeta belong to
+    // the K2 launch that follows (the two halves of the slab epilogue are
+    // independent)
+    if (mode == MODE_ITER && st->dual_only) return;
+    const bool wg2 = mode != MODE_ITER || !st->last_restarted;
+    const bool wz2 = mode == MODE_ITER && a.fz_spec2 && st->dual_pending;
+    if (!wg2 && !wz2) return;
+    if (j < p) {
+      if (wg2) {
+        for (int c = 0; c < ncl; ++c) g += __ldcg(a.fz_part + (int64_t)c * pv + j);
+        a.gv[j] = g;
+      }
+      if (wz2) {
+        for (int c = 0; c < ncl; ++c) v += __ldcg(a.fz_part + (2 * (int64_t)ncl + c) * pv + j);
+        a.gv[pv + j] = v;
+      }
+    }
+    if (wg2 && blockIdx.x == 0 && threadIdx.x == 0 && mode == MODE_ITER && ((int)a.gv[2 * pv + 6] & 4)) {
       State* sw = a.st;   // non-finite X gamma: loss_gradient raises (model.py:215)
       atomicExch(&sw->err, (int)ST_INVALID);
       sw->err_iter = sw->t + 1;
       sw->done = 1;
     }
-    slab_epilogue(a, blockIdx.x, st->t + 1, momentum(st->phi), true, false, g, 0.0, sm);
+    slab_epilogue(a, blockIdx.x, st->t + 1, momentum(st->phi), wg2, wz2, g, v, sm);
     return;
   }
   if (a.fz_one == 1) {
@@ -991,7 +1027,7 @@ static KfFn kfs_pick_r(int rows, int nv) {
   }
   if (rows == 2) return kfs_pick_nv<TX, 2, F32F, ONE>(nv);
   if (rows == 4) {
-    if constexpr (ONE != 2) return kfs_pick_nv<TX, 4, F32F, ONE>(nv);
+    if constexpr (ONE != 2 && ONE != 3) return kfs_pick_nv<TX, 4, F32F, ONE>(nv);
   }
   return nullptr;
 }
@@ -1001,6 +1037,10 @@ static KfFn kfs_pick_one(int one, int rows, int nv) {
   if (one == 1) return kfs_pick_r<TX, F32F, 1>(rows, nv);
   if (one == 2) {
     if constexpr (sizeof(TX) == 4) return kfs_pick_r<TX, F32F, 2>(rows, nv);
+    return nullptr;
+  }
+  if (one == 3) {
+    if constexpr (sizeof(TX) == 4) return kfs_pick_r<TX, F32F, 3>(rows, nv);
     return nullptr;
   }
   return kfs_pick_r<TX, F32F, 0>(rows, nv);

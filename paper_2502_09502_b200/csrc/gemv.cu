@@ -467,8 +467,9 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_transpose(EngineArgs a, int 
     // behind the SPEC single-pass kernel (fused.cu): only the iterations KR left
     // (restart: the restart candidate; bound pass: X^T zeta -- the gradient of a
     // bound-check iteration that did not restart stays KR's)
-    if (a.k2_cond && !(st->last_restarted || st->dual_pending || st->dual_only)) return;
-    wz = st->dual_pending != 0;
+    if (a.k2_cond == 1 && !(st->last_restarted || st->dual_pending || st->dual_only)) return;
+    if (a.k2_cond == 2 && !(st->last_restarted || st->dual_only)) return;
+    wz = st->dual_pending != 0 && (a.k2_cond != 2 || st->dual_only);
     wg = st->dual_only == 0 && (!a.k2_cond || st->last_restarted);
     t = st->t + 1;
     c = momentum(st->phi);

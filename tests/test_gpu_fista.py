@@ -393,8 +393,9 @@ def test_k3_variants_agree(engine, monkeypatch):
 def test_single_pass_kernel_variants_agree(engine, monkeypatch, case):
     """The one-vector single-pass kernels -- LIN (squared error: both momentum
     candidates and X^T zeta from A_t = X^T grad F(u_t) by linearity) and SPEC
-    (non-linear loss on fp32 X: the no-restart candidate, restarts and bound
-    passes through the conditional K2 launch) -- against the three-vector
+    (non-linear loss on fp32 X: the no-restart candidate, plus X^T zeta in the
+    two-vector kernel of bound-check iterations; restarts and bound-only passes
+    through the conditional K2 launch) -- against the three-vector
     kernel they replace (L0_FZ_LIN=0 / L0_FZ_SPEC=0) and the two-pass engine:
     same iterations, restarts and termination, values to summation order."""
     kw = {}
@@ -418,8 +419,11 @@ def test_single_pass_kernel_variants_agree(engine, monkeypatch, case):
     if var == "L0_FZ_LIN":
         L *= 0.55   # over-long steps: the momentum overshoots and the restart rule fires early
     res = {}
-    for mode in ("two_pass", "0", "1"):
-        monkeypatch.setenv(var, "1" if mode == "two_pass" else mode)
+    modes = ("two_pass", "0", "1") + (("k2z",) if var == "L0_FZ_SPEC" else ())
+    for mode in modes:
+        monkeypatch.setenv(var, "0" if mode == "0" else "1")
+        # "k2z": SPEC without the two-vector bound-check kernel (X^T zeta from the conditional K2)
+        monkeypatch.setenv("L0_FZ_SPEC2", "0" if mode == "k2z" else "1")
         # a fresh instance per variant: the plan is fixed when the device problem is created
         inst = engine.ProblemInstance(X, cd.y, engine.LossKind(cd.loss), cd.k, cd.M, cd.lambda2,
                                       dtype=cd.dtype)
@@ -435,13 +439,13 @@ def test_single_pass_kernel_variants_agree(engine, monkeypatch, case):
         assert rep.stats["single_pass"] == (mode != "two_pass")
     a, ra = res["two_pass"]
     if case == "time_limit":
-        for mode in ("0", "1"):
+        for mode in modes[1:]:
             b, _ = res[mode]
             assert b.termination == engine.Termination.TIME_LIMIT
             assert np.isfinite(b.dual_bound) and b.dual_bound <= b.primal_value + 1e-9 * abs(b.primal_value)
         return
     assert a.restarts > 0 or case == "hinge"
-    for mode in ("0", "1"):
+    for mode in modes[1:]:
         b, rb = res[mode]
         assert b.iterations == a.iterations == iters
         assert b.restarts == a.restarts and b.termination == a.termination
