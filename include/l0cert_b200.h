@@ -82,8 +82,11 @@ typedef struct l0_fista_opts {
   int32_t stop_on_gap;          /* 0: fixed-iteration mode (no gap stop) */
   int32_t chunk_iterations;     /* iterations per captured CUDA graph (0: auto) */
   int32_t profile;              /* 1: time the kernels with CUDA events (report fields) */
-  int32_t engine_path;          /* 0 auto (single pass for fp64 X when it fits a <= 8-CTA cluster
-                                   plan, else two-pass), 1 two-pass, 2 single pass */
+  int32_t engine_path;          /* 0 auto (single pass when X is beyond L2 and fits a <= 8-CTA
+                                   cluster plan: from 128 MB for the one-vector kernels -- squared
+                                   error, or another loss on fp32 X -- and from 512 MB with
+                                   clusters of 4-8 otherwise; else two-pass), 1 two-pass,
+                                   2 single pass */
   int32_t fp32_forward;         /* fp32 X, single pass: X beta with fp32 products and fp64
                                    reductions (the fp32 mode, 1e-5 relative); 0: fp64 products */
 } l0_fista_opts;
