@@ -504,9 +504,11 @@ def run_config(name, iters):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    t_host = time.perf_counter()
     rep = eng.solve_relaxation(inst, opts=o(iters, False), return_device=True)
     e1.record()
     torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t_host) * 1e3
     ms = e0.elapsed_time(e1)
     rep_p = eng.solve_relaxation(inst, opts=o(iters, True), return_device=True)
     st = rep_p.stats
@@ -545,6 +547,8 @@ def run_config(name, iters):
            "engine_path": "single_pass" if st.get("single_pass") else "two_pass",
            "x_bytes": xb, "l2_resident": xb < 100e6, "kernels": kern, "peak_gbs": peak,
            "primal": rep.primal_value, "dual": rep.dual_bound, "restarts": rep.restarts,
+           "gpu_launches": rep.stats.get("gpu_launches"),
+           "prox_full_passes": rep.stats.get("prox_full_passes"), "host_wall_ms": wall_ms,
            "setup_s": gen_s}
     if cd.dtype == "fp32" and st.get("single_pass"):
         src = measured_peak()[1]

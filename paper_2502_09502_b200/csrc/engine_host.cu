@@ -99,8 +99,11 @@ struct Problem {
   State* h_st[2] = {nullptr, nullptr};  // pinned mirrors (double-buffered chunks)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_chunk[2] = {nullptr, nullptr};
-  Graph graphs[2][2];   // [profile][double-buffer slot]: both variants stay captured
-  Graph* graph = graphs[0];
+  // [profile][K3 variant: windowed / full key sort][double-buffer slot]: every
+  // variant stays captured, so a solve that switches K3 variants (C3) does not
+  // re-capture its graphs in every call
+  Graph graphs[2][2][2];
+  Graph* graph = graphs[0][0];
   int fused_planned = 0;
   // single-pass plans: [0] the default kernel of the loss (LIN for squared
   // error, three vectors otherwise), [1] SPEC (one vector; non-linear losses
@@ -250,12 +253,13 @@ static uint64_t carve(Problem& P, char* base) {
 }
 
 static void destroy_graphs(Problem& P) {
-  for (auto& set : P.graphs)
-    for (auto& g : set) {
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-      for (auto e : g.ev) cudaEventDestroy(e);
-      g = Graph{};
-    }
+  for (auto& prof : P.graphs)
+    for (auto& set : prof)
+      for (auto& g : set) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (auto e : g.ev) cudaEventDestroy(e);
+        g = Graph{};
+      }
 }
 
 static int fused_tail(Problem& P, int mode, cudaStream_t s) {
@@ -756,7 +760,7 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     G = (int)std::max<int64_t>(1, (need + nch - 1) / nch);
   }
   int64_t launched_its = 0;
-  P->graph = P->graphs[o->profile ? 1 : 0];
+  P->graph = P->graphs[o->profile ? 1 : 0][a.prox_full_sort ? 1 : 0];
   for (int w = 0; w < 2; ++w) {
     rc = build_graph(*P, w, G, o->profile ? 1 : 0);
     if (rc) return rc;
@@ -855,8 +859,15 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     // with nothing in flight a chunk is launched anyway (never strand a solve)
     if (launched_its >= need && !stop_sent && inflight > 0) continue;
     if (P->graph[w].full_sort != a.prox_full_sort) {
+      // (the chunk still in flight was launched from the other variant's set;
+      // its kernel count is the same up to the sort kernels -- a statistic only)
+      P->graph = P->graphs[o->profile ? 1 : 0][a.prox_full_sort ? 1 : 0];
       rc = build_graph(*P, w, G, o->profile ? 1 : 0);
       if (rc) return rc;
+      if (!P->graph[w ^ 1].exec) {   // never leave an empty slot behind the pointer
+        rc = build_graph(*P, w ^ 1, G, o->profile ? 1 : 0);
+        if (rc) return rc;
+      }
     }
     rc = launch_chunk(w);
     if (rc) return rc;
