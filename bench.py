@@ -98,7 +98,8 @@ def c5_config(n, p, world, shard="rows"):
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "clocks.mem,temperature.gpu,temperature.memory")
 
     def __init__(self, index=0):
         self.index = index
@@ -130,6 +131,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
+        mem, power, temp = [], [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
@@ -143,9 +145,16 @@ class ClockSampler:
             for nm, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            for dst, idx in ((power, 2), (mem, 8), (temp, 10)):
+                try:
+                    dst.append(float(parts[idx]))
+                except (ValueError, IndexError):
+                    pass
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "mem_mhz": statistics.median(mem) if mem else None,
+                "power_w_max": max(power) if power else None,
+                "mem_temp_c_max": max(temp) if temp else None}
 
 
 def measured_peak():
@@ -503,12 +512,15 @@ def run_config(name, iters):
     eng.solve_relaxation(inst, opts=o(5, False), return_device=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(0)      # a throttled GPU shows here (C3 has read 706-800 it/s instead of
+    clocks.start()                # ~1000 with identical launches and per-kernel event times)
     e0.record()
     t_host = time.perf_counter()
     rep = eng.solve_relaxation(inst, opts=o(iters, False), return_device=True)
     e1.record()
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - t_host) * 1e3
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     rep_p = eng.solve_relaxation(inst, opts=o(iters, True), return_device=True)
     st = rep_p.stats
@@ -549,6 +561,7 @@ def run_config(name, iters):
            "primal": rep.primal_value, "dual": rep.dual_bound, "restarts": rep.restarts,
            "gpu_launches": rep.stats.get("gpu_launches"),
            "prox_full_passes": rep.stats.get("prox_full_passes"), "host_wall_ms": wall_ms,
+           "clocks": clk,
            "setup_s": gen_s}
     if cd.dtype == "fp32" and st.get("single_pass"):
         src = measured_peak()[1]
