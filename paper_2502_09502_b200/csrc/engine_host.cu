@@ -411,7 +411,13 @@ static int auto_chunk(const Problem& P, int bci) {
   const EngineArgs& a = P.a;
   const double bytes = 2.0 * (double)a.n * (double)a.ld * (a.dtype == F64 ? 8.0 : 4.0);
   const double t_it = bytes / 6.0e12 + 40e-6;  // seconds, rough
-  int G = (int)std::ceil(4e-3 / t_it);
+  // ~16 ms of work per replay (L0_CHUNK_MS overrides): the loop is host-driven
+  // -- every replay boundary needs the host thread within one chunk time to
+  // keep two in flight -- and on a busy host 4 ms chunks lost up to 25-40% of a
+  // C3 solve (C3 run-to-run); the bench's 20-iteration C2 solve
+  // becomes a single replay
+  const double chunk_s = getenv("L0_CHUNK_MS") ? std::max(0.5, atof(getenv("L0_CHUNK_MS"))) * 1e-3 : 16e-3;
+  int G = (int)std::ceil(chunk_s / t_it);
   G = std::max(4, std::min(G, 100));
   (void)bci;
   return G;
@@ -761,10 +767,6 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   }
   int64_t launched_its = 0;
   P->graph = P->graphs[o->profile ? 1 : 0][a.prox_full_sort ? 1 : 0];
-  for (int w = 0; w < 2; ++w) {
-    rc = build_graph(*P, w, G, o->profile ? 1 : 0);
-    if (rc) return rc;
-  }
   int64_t trace_seen = 0;
   int64_t chunks = 0;
   bool aborted = false, stop_sent = false, abort_deferred = false;
@@ -774,6 +776,9 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
   int inflight = 0;
   int next = 0;
   auto launch_chunk = [&](int w) -> int {
+    // captured on first use (a solve that fits one replay never builds the second slot)
+    int brc = build_graph(*P, w, G, o->profile ? 1 : 0);
+    if (brc) return brc;
     L0_CUDA_TRY(cudaGraphLaunch(P->graph[w].exec, s));
     L0_CUDA_TRY(cudaEventRecord(P->ev_chunk[w], s));
     launched_its += G;
@@ -798,7 +803,9 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
     if (o->profile) {
       const int64_t did = std::max<int64_t>(0, std::min<int64_t>(G, h->t - t_prev));
       Graph& g = P->graph[w];
-      for (int64_t i = 0; i < did; ++i) {
+      // (right after a K3-variant switch this slot of the new set may not be
+      // captured yet: the chunk that just finished belonged to the other set)
+      for (int64_t i = 0; i < did && (size_t)(i * 6 + 5) < g.ev.size(); ++i) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 0], g.ev[i * 6 + 1]) == cudaSuccess) { rep->k2_ms += ms; rep->k2_count++; }
         if (cudaEventElapsedTime(&ms, g.ev[i * 6 + 2], g.ev[i * 6 + 3]) == cudaSuccess) { rep->k3_ms += ms; rep->k3_count++; }
@@ -862,12 +869,6 @@ int32_t l0_fista_solve(l0_problem* P, int64_t k, double M, double lambda2,
       // (the chunk still in flight was launched from the other variant's set;
       // its kernel count is the same up to the sort kernels -- a statistic only)
       P->graph = P->graphs[o->profile ? 1 : 0][a.prox_full_sort ? 1 : 0];
-      rc = build_graph(*P, w, G, o->profile ? 1 : 0);
-      if (rc) return rc;
-      if (!P->graph[w ^ 1].exec) {   // never leave an empty slot behind the pointer
-        rc = build_graph(*P, w ^ 1, G, o->profile ? 1 : 0);
-        if (rc) return rc;
-      }
     }
     rc = launch_chunk(w);
     if (rc) return rc;
