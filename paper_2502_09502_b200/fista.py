@@ -9,7 +9,7 @@ pass + gradient step), K3 (bound check, sort, PAVA, scatter, envelope) and K1
 the device; the host only reads the state between graph replays.
 
 Differences a caller can observe (documented in DESIGN.md):
-* ``time_limit`` is checked between graph replays (a few ms apart), not after
+* ``time_limit`` is checked between graph replays (~16 ms of work apart), not after
   every iteration;
 * ``trace_hook`` is called with the same records, in order, but in batches;
 * engine-only options: ``gap_tolerance_rel``, ``stop_on_gap``,
